@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 octagon pre-filter (arXiv 2303.10581 hot path).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+A step is one pass of the whole hot path over the
+resident synthetic input: K1 (extremes + octagon) then K2 (octagon test +
+stable compaction), plus at N > 1 the extremes all-gather + K3 combine and
+the count all-gather.  Default workload: 10^9 normal points (the north_star
+target, BASELINE.json configs[4] at one GPU), float64.  Prints ONE JSON line
+on rank 0.  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gpts/s filtered and % of HBM peak at 1/2/4/8 B200; survivor ratio per distribution"
+UNIT = "Gpts/s"
+
+NVML_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dist", choices=["normal", "circle", "displaced"], default="normal")
+    ap.add_argument("--n", type=float, default=1e9, help="points (total for strong scaling, per GPU for weak)")
+    ap.add_argument("--p", type=float, default=0.1)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
+    ap.add_argument("--plain", action="store_true", help="plain fp64 predicate (T_k = 0)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU work for the oracle baseline")
+    return ap.parse_args()
+
+
+def env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_name(a) -> str:
+    n = int(a.n)
+    e = int(round(math.log10(n))) if n > 0 and 10 ** round(math.log10(n)) == n else None
+    size = f"1e{e}" if e is not None else str(n)
+    d = a.dist if a.dist != "displaced" else f"displaced_p{a.p:g}"
+    return f"{d}_{size}_fp64"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.ok = False
+        self.samples, self.reasons = [], 0
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        names = [v for k, v in NVML_REASONS.items() if self.reasons & k]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": int(self.max_mhz),
+                "reasons": names, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy kernel)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic(kernel: str, workload: str):
+    """dram bytes per launch from the committed ncu capture, if it matches."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d[workload][kernel]
+        return float(e["dram_read_bytes"]) + float(e["dram_write_bytes"])
+    except Exception:
+        return None
+
+
+def oracle_rate(xy_host: np.ndarray, seconds: float):
+    """Time the CPU oracle (single thread) on a bounded prefix of the input."""
+    import oracle
+    oracle.build()
+    n = xy_host.shape[0]
+    m0 = min(n, 1 << 20)
+    t0 = time.perf_counter()
+    oracle.filter_compact(xy_host[:m0])
+    dt0 = time.perf_counter() - t0
+    m = int(min(n, max(m0, m0 * seconds / max(dt0, 1e-9))))
+    t0 = time.perf_counter()
+    surv, _ = oracle.filter_compact(xy_host[:m])
+    dt = time.perf_counter() - t0
+    return m, dt, len(surv)
+
+
+# --------------------------------------------------------------------------- #
+def run_reference(a):
+    """The reference arm: the CPU oracle, as it stands, on the host cores."""
+    rank, world, local = env()
+    if rank != 0:
+        return 0
+    import oracle
+    import synth
+    oracle.build()
+    n = int(a.n)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    # a bounded prefix of the same workload (same generator, same device)
+    m0 = min(n, 1 << 20)
+    probe = synth.points(a.dist, n, seed=a.seed, p=a.p, device=dev, lo=0, hi=m0).cpu().numpy()
+    t0 = time.perf_counter()
+    oracle.filter_compact(probe, certified=not a.plain)
+    dt0 = time.perf_counter() - t0
+    per_step_s = 120.0 / max(a.steps + a.warmup, 1)
+    m = int(min(n, max(m0, m0 * min(per_step_s, 2.0) / max(dt0, 1e-9))))
+    xy = synth.points(a.dist, n, seed=a.seed, p=a.p, device=dev, lo=0, hi=m).cpu().numpy()
+    for _ in range(a.warmup):
+        oracle.filter_compact(xy, certified=not a.plain)
+    times = []
+    s = 0
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        surv, _ = oracle.filter_compact(xy, certified=not a.plain)
+        times.append(time.perf_counter() - t0)
+        s = len(surv)
+    ms = 1e3 * float(np.mean(times))
+    val = m / (ms / 1e3) / 1e9
+    sample = f"first {m} of {n} points of {workload_name(a)} (same generator), per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": a.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(a), "n": n, "dist": a.dist, "seed": a.seed,
+                   "sample_points": m, "survivors_in_sample": s},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- #
+def run_ours(a):
+    import torch.distributed as dist
+    import paper_2303_10581_b200 as chf
+    from paper_2303_10581_b200 import dist as chdist
+    import synth
+
+    rank, world, local = env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU path)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_arg = int(a.n)
+    n_total = n_arg if a.scaling == "strong" else n_arg * world
+    lo, hi = chdist.shard_range(n_total, world, rank)
+    n_local = hi - lo
+    xy = synth.points(a.dist, n_total, seed=a.seed, p=a.p, device=dev, lo=lo, hi=hi)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+
+    if world == 1:
+        ws = chf.Workspace(n_local, device=dev)
+        out = torch.empty(max(n_local, 1), dtype=torch.int64, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        launches_per_step = 2
+
+        def k1():
+            chf.extremes8_async(xy, ws, plain=a.plain)
+
+        def exch():
+            pass
+
+        def k2():
+            chf.filter_compact(xy, ws, out=out, count=cnt)
+
+        def exch2():
+            pass
+    else:
+        df = chdist.DistFilter(n_total, xy, plain=a.plain)
+        ws = df.ws
+        launches_per_step = 3
+
+        def k1():
+            chf.extremes8_async(xy, df.ws, index_base=df.lo, plain=a.plain, ext_out=df.ext_local)
+
+        def exch():
+            chdist.exchange_extremes(df.ext_local, out=df.ext_all)
+            chf.combine8(df.ext_all, world, df.ws, plain=a.plain)
+
+        def k2():
+            chf.filter_compact(xy, df.ws, index_base=df.lo, out=df.out, count=df.count)
+
+        def exch2():
+            chdist.exclusive_offsets(df.count, out=df.counts)
+
+    def step():
+        k1(); exch(); k2(); exch2()
+
+    for _ in range(max(a.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    res = chf.read_result(ws)   # raises on non-finite input
+
+    K = a.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for k in range(K):
+            ev[k][0].record(stream)
+            k1()
+            ev[k][1].record(stream)
+            exch()
+            ev[k][2].record(stream)
+            k2()
+            ev[k][3].record(stream)
+            exch2()
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    k2_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
+    ex_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    res = chf.read_result(ws)
+    s_local = int(res.count)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        st = torch.tensor([s_local], dtype=torch.int64, device=dev)
+        dist.all_reduce(st)
+        s_total = int(st.item())
+    else:
+        s_total = s_local
+    ms_step = total_ms / K
+    value = n_total / (ms_step / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (algorithmic bytes) ----
+    peak, peak_src = measured_peaks()
+    k1_bytes = 16.0 * n_local
+    k2_bytes = 16.0 * n_local + 8.0 * s_local
+    if k2_ms >= k1_ms:
+        dom, dom_bytes, dom_ms = "k2_filter_compact", k2_bytes, k2_ms
+    else:
+        dom, dom_bytes, dom_ms = "k1_extremes8", k1_bytes, k1_ms
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    step_bytes = k1_bytes + k2_bytes
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(dom, workload_name(a)), "peak_source": peak_src,
+            "k1_ms": k1_ms, "k2_ms": k2_ms, "k1_gbs": k1_bytes / (k1_ms / 1e3) / 1e9,
+            "k2_gbs": k2_bytes / (k2_ms / 1e3) / 1e9,
+            "step_gbs_per_gpu": step_bytes / (ms_step / 1e3) / 1e9,
+            "step_frac": step_bytes / (ms_step / 1e3) / 1e9 / peak,
+            "step_frac_theoretical_8184": step_bytes / (ms_step / 1e3) / 1e9 / 8184.0}
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not a.no_e2e and a.e2e_steps > 0:
+        h_xy = torch.empty(n_local, 2, dtype=torch.float64, pin_memory=True)
+        h_xy.copy_(xy)
+        h_out = torch.empty(max(n_local, 1), dtype=torch.int64)
+        d_stage = torch.empty_like(xy)
+        e_s = torch.cuda.Event(enable_timing=True)
+        e_e = torch.cuda.Event(enable_timing=True)
+        # one untimed warm-up
+        if world == 1:
+            d2h = 0
+            chf.filter_host(h_xy, ws, d_stage, out, h_out, plain=a.plain)
+            torch.cuda.synchronize()
+            e_s.record(stream)
+            for _ in range(a.e2e_steps):
+                c = chf.filter_host(h_xy, ws, d_stage, out, h_out, plain=a.plain)
+                d2h = 8 * c + 8
+            e_e.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms = e_s.elapsed_time(e_e) / a.e2e_steps
+        else:
+            df2 = chdist.DistFilter(n_total, d_stage, plain=a.plain)
+            d2h = 0
+
+            def e2e_step():
+                d_stage.copy_(h_xy, non_blocking=True)
+                df2.step(d_stage)
+                loc, off, tot = df2.result()
+                h_out[: loc.shape[0]].copy_(loc)
+                return 8 * loc.shape[0] + 8 * world
+
+            e2e_step()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e_s.record(stream)
+            for _ in range(a.e2e_steps):
+                d2h = e2e_step()
+            e_e.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([e_s.elapsed_time(e_e) / a.e2e_steps], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": n_total / (e2e_ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 16 * n_local, "d2h_bytes_per_step": int(d2h),
+               "api": "ch_filter_host (C ABI, pinned host input)" if world == 1 else "DistFilter + host copies"}
+        del h_xy, h_out, d_stage
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        m_cap = min(n_local, 200_000_000)
+        host = xy[:m_cap].cpu().numpy()
+        m, dt, s = oracle_rate(host, a.cpu_seconds)
+        cpu = {"value": m / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {m} points of the same {workload_name(a)} input (oracle: extremes + octagon + "
+                         f"filter + compaction, single thread, {dt:.2f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": a.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": a.scaling if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(a), "n": n_total, "n_per_gpu": n_local, "dist": a.dist,
+                       "seed": a.seed, "p": a.p if a.dist == "displaced" else None,
+                       "predicate": "plain" if a.plain else "certified",
+                       "parallelism": f"dp{world}", "l2": "inputs larger than L2 (16 B/pt)"
+                       if 16 * n_local > 126e6 else "inputs smaller than L2 (not flushed)"},
+            "survivors": s_total, "survivor_ratio": s_total / n_total,
+            "hbm_frac": roof["step_frac"],
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * K, "clocks": clk.summary(),
+            "exchange_ms": ex_ms if world > 1 else 0.0,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,206 @@
+/*
+ * chfilter.h -- C ABI of the B200-native convex-hull pre-filter
+ * (Carrasco, Ferrada, Navarro, Hitschfeld, arXiv 2303.10581).
+ *
+ * Citations: "P:<line>" = PAPER.md line, "S:<line>" = SPEC.md line (both in
+ * the paper's source bundle), "DESIGN Rk" = reading k in DESIGN.md.
+ *
+ * The library computes Algorithm 1:
+ *   line 1  findingPolygon          -> ch_extremes8  (+ ch_octagon_build)
+ *   line 2  buildingFilter          -> ch_octagon_filter (bit vector)
+ *   line 3  compactingFilteredPoints-> ch_filter_compact (fused with line 2)
+ *   line 4  convexHull_algorithm    -> ch_hull_end_to_end
+ *
+ * Conventions (all entry points):
+ *  - Points are float64 AoS: point i is (xy[2i], xy[2i+1]); the array must be
+ *    16-byte aligned (CH_ERR_MISALIGNED otherwise).  n and every index are
+ *    int64 (n > 2^31 is supported).
+ *  - "d_" pointers are device memory of the current CUDA device, "h_" host.
+ *    The caller owns every buffer; the library never allocates device memory
+ *    on hot calls and never frees caller memory.
+ *  - Scratch lives in a caller-provided workspace of ch_workspace_bytes(n)
+ *    bytes, zero-filled once before first use (ch_workspace_init).  A
+ *    workspace must not be used by two calls concurrently; calls on distinct
+ *    workspaces are reentrant.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *    Calls enqueue asynchronously unless they fill a host output ("h_"),
+ *    in which case they synchronize that stream before returning.
+ *  - Errors are returned as ch_status; nothing is thrown.  On error the
+ *    outputs are unspecified; ch_last_error() gives a thread-local detail.
+ *    Non-finite coordinates are detected inside the first pass and reported
+ *    (CH_ERR_NONFINITE) by the next call that synchronizes.
+ *  - Degenerate input (fewer than 3 distinct octagon vertices) is not an
+ *    error: every point survives (DESIGN R6).
+ *  - Arithmetic: binary64, round-to-nearest-even, no FMA contraction, in the
+ *    order stated for each step.  Results are bit-identical to the sequential
+ *    definition (DESIGN.md section "Readings") for every grid shape and
+ *    world size.
+ */
+#ifndef CHFILTER_H
+#define CHFILTER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CH_ABI_VERSION 1
+
+typedef enum {
+    CH_OK = 0,
+    CH_ERR_INVALID_ARG = 1,
+    CH_ERR_EMPTY = 2,      /* n == 0 (S:75 EmptySet)                    */
+    CH_ERR_NONFINITE = 3,  /* a NaN / infinite coordinate        */
+    CH_ERR_MISALIGNED = 4, /* d_xy not 16-byte aligned                  */
+    CH_ERR_WORKSPACE = 5,  /* workspace missing or too small            */
+    CH_ERR_CUDA = 6        /* a CUDA runtime error (see ch_last_error)  */
+} ch_status;
+
+/* Predicate switch (DESIGN R4).  Default: certified thresholds T_k. */
+#define CH_CERTIFIED 0
+#define CH_PLAIN 1 /* T_k = 0: the plain fp64 test (not hull-safe adversarially) */
+
+/* The eight extremes, slot order R, TR, T, TL, L, BL, B, BR:
+ *   R = argmax x, TR = argmax fl(x+y), T = argmax y, TL = argmin fl(x-y),
+ *   L = argmin x, BL = argmin fl(x+y), B = argmin y, BR = argmax fl(x-y);
+ * ties go to the lowest global index, -0.0 == +0.0 (DESIGN R1, R2). */
+typedef struct {
+    int64_t idx[8]; /* global point index                                  */
+    double x[8];    /* coordinates of that point                           */
+    double y[8];
+} ch_extremes;      /* 192 bytes */
+
+/* The discard polygon ("counterclockwise"; DESIGN R5).  Vertices are
+ * the cycle [R,TR,T,TL,L,BL,B,BR] with consecutive duplicates (and trailing
+ * copies of the first) removed.  Edge k runs from v[k] to v[(k+1) % nv]:
+ *   ex = fl(vx[k+1] - vx[k]),  ey = fl(vy[k+1] - vy[k]),
+ *   thr = T_k = 2^-50 * fl(fl(|ex| Y) + fl(|ey| X)) (certified) or 0 (plain),
+ *   X = max(fl(xmax - vx[k]), fl(vx[k] - xmin)), Y likewise in y.
+ * A point is discarded iff for every k
+ *   D_k = fl(fl(ex * fl(y - vy[k])) - fl(ey * fl(x - vx[k]))) > thr[k].
+ * box/has_box: a closed axis box on which every D_k > thr[k] was verified at
+ * the four corners (D_k is monotone in x and in y under round-to-nearest, so
+ * the corners bound it); points inside it are discarded without edge tests.
+ * It never changes a result.  guess_edge/cx/cy: the octant of (x-cx, y-cy)
+ * picks the edge tested first (a pure speed hint). */
+typedef struct {
+    int32_t nv;
+    int32_t degenerate;
+    int64_t vidx[8];
+    double vx[8], vy[8];
+    double ex[8], ey[8], thr[8];
+    double bbox[4];    /* xmin, xmax, ymin, ymax                         */
+    double box[4];     /* x0, x1, y0, y1 (closed)                        */
+    int32_t has_box;
+    int32_t plain;     /* 1 if built with CH_PLAIN                       */
+    int32_t guess_edge[8];
+    double cx, cy;
+} ch_octagon;
+
+/* Result of the last filter call on a workspace (device-resident copy in the
+ * workspace; read with ch_read_result). */
+typedef struct {
+    int64_t count;      /* number of survivors                            */
+    int32_t nonfinite;  /* 1 if a non-finite coordinate was seen          */
+    int32_t degenerate; /* 1 if the octagon had < 3 distinct vertices     */
+} ch_result;
+
+typedef struct {
+    int64_t n, n_survivors, n_hull;
+    double ms_filter; /* extremes + octagon + filter + compaction (device) */
+    double ms_gather; /* survivor coordinates device -> host               */
+    double ms_hull;   /* exact monotone chain on the host                  */
+} ch_stats;
+
+int ch_abi_version(void);
+const char *ch_status_str(ch_status s);
+const char *ch_last_error(void); /* thread-local, valid until the next call */
+
+/* Bytes of workspace needed for inputs of up to n points. */
+size_t ch_workspace_bytes(int64_t n);
+/* Zero-fill a workspace (once, before first use).  Async on `stream`. */
+ch_status ch_workspace_init(void *d_ws, size_t ws_bytes, void *stream);
+
+/* Algorithm 1 line 1: the eight extremes of d_xy[0..n) in one
+ * pass, indices offset by index_base (a shard's global offset), then the
+ * octagon (flags: CH_CERTIFIED or CH_PLAIN) built on the device into the
+ * workspace.  If d_ext_out != NULL the extremes are also written there as a
+ * device ch_extremes (for the multi-GPU exchange).  If h_ext != NULL and/or
+ * h_oct != NULL the call synchronizes and copies them out (and reports
+ * CH_ERR_NONFINITE). */
+ch_status ch_extremes8(const double *d_xy, int64_t n, int64_t index_base, int flags,
+                       void *d_ext_out, ch_extremes *h_ext, ch_octagon *h_oct,
+                       void *d_ws, size_t ws_bytes, void *stream);
+
+/* Multi-GPU exchange step (north_star): combine W device ch_extremes records
+ * (d_ext_all, contiguous, one per rank -- e.g. the output of an all-gather)
+ * with the same ordering (best key, then lowest global index), and build the
+ * octagon into the workspace.  Bit-identical to a single-GPU ch_extremes8
+ * over the concatenated shards.  d_xy is not needed (coordinates travel in
+ * the records). */
+ch_status ch_combine8(const void *d_ext_all, int world, int flags,
+                      void *d_ws, size_t ws_bytes, void *stream);
+
+/* Host-side octagon assembly (DESIGN R5): pure, no CUDA. */
+ch_status ch_octagon_build(const ch_extremes *ext, int flags, ch_octagon *out);
+
+/* Algorithm 1 line 2: the paper's n-bit flag vector.
+ * Bit (i % 32) of d_keep_bits[i / 32] is 1 iff point i survives; the padding
+ * bits of the last word are 0.  h_oct == NULL uses the workspace octagon
+ * from the last ch_extremes8 / ch_combine8 on d_ws. */
+ch_status ch_octagon_filter(const double *d_xy, int64_t n, const ch_octagon *h_oct,
+                            uint32_t *d_keep_bits, void *d_ws, size_t ws_bytes, void *stream);
+
+/* Algorithm 1 lines 2-3 fused: the octagon test and a
+ * single-pass stable stream compaction.  Writes the survivors as int64
+ * global indices (index_base + i) in increasing order to d_survivors
+ * (capacity n) and their count to *d_count (device, nullable) and to the
+ * workspace result.  h_oct == NULL uses the workspace octagon. */
+ch_status ch_filter_compact(const double *d_xy, int64_t n, int64_t index_base,
+                            const ch_octagon *h_oct, int64_t *d_survivors, int64_t *d_count,
+                            void *d_ws, size_t ws_bytes, void *stream);
+
+/* Synchronize `stream` and copy the workspace result to the host.  Returns
+ * CH_ERR_NONFINITE if the last pass saw a non-finite coordinate. */
+ch_status ch_read_result(const void *d_ws, ch_result *h_res, void *stream);
+
+/* One filter step on device-resident input: ch_extremes8 + ch_filter_compact
+ * (two kernels, no host round trip in between) + ch_read_result. */
+ch_status ch_filter(const double *d_xy, int64_t n, int flags, int64_t *d_survivors,
+                    int64_t *h_count, void *d_ws, size_t ws_bytes, void *stream);
+
+/* The same step end to end from HOST memory: copies h_xy (pinned for full
+ * speed) into d_xy_staging (capacity n points), filters, and copies the
+ * survivor indices back to h_survivors (capacity n).  Synchronizes. */
+ch_status ch_filter_host(const double *h_xy, int64_t n, int flags, double *d_xy_staging,
+                         int64_t *d_survivors, int64_t *h_survivors, int64_t *h_count,
+                         void *d_ws, size_t ws_bytes, void *stream);
+
+/* Gather d_xy[d_idx[j] - index_base] into d_out[2j..2j+1] for j < m. */
+ch_status ch_gather_points(const double *d_xy, int64_t index_base, const int64_t *d_idx,
+                           int64_t m, double *d_out, void *stream);
+
+/* Exact strict convex hull on the host (Algorithm 1 line 4, P:149-151;
+ * DESIGN R8): h_pts[2j..2j+1] are the coordinates of point h_ids[j].
+ * Output: hull vertex ids, counter-clockwise from the lexicographic minimum
+ * (x, then y), duplicates resolved to the lowest id, collinear points
+ * excluded.  h_hull capacity >= m.  Exact orientation (adaptive filter with
+ * an exact expansion fallback); valid for |coordinates| in [2^-450, 2^450]
+ * or zero. */
+ch_status ch_hull_points(const double *h_pts, const int64_t *h_ids, int64_t m,
+                         int64_t *h_hull, int64_t *h_n_hull);
+
+/* Algorithm 1 complete: ch_filter on device-resident d_xy, then
+ * the survivors' coordinates are gathered on the device, copied to the host,
+ * and the exact hull is computed there.  Stage times go to h_stats
+ * (nullable).  h_hull capacity >= number of survivors (<= n). */
+ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *d_survivors,
+                             int64_t *h_n_survivors, int64_t *h_hull, int64_t *h_n_hull,
+                             ch_stats *h_stats, void *d_ws, size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHFILTER_H */

@@ -1,0 +1,109 @@
+"""ctypes loader for libchfilter.so (the C ABI of include/chfilter.h).
+
+There is no fallback: if the shared library is missing and cannot be built,
+or a call fails, this raises.  The filter never runs on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import build as _build
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int32
+I64 = ctypes.c_int64
+DBL = ctypes.c_double
+SZ = ctypes.c_size_t
+
+CH_OK, CH_ERR_INVALID_ARG, CH_ERR_EMPTY, CH_ERR_NONFINITE = 0, 1, 2, 3
+CH_ERR_MISALIGNED, CH_ERR_WORKSPACE, CH_ERR_CUDA = 4, 5, 6
+CH_CERTIFIED, CH_PLAIN = 0, 1
+
+
+class Extremes(ctypes.Structure):
+    _fields_ = [("idx", I64 * 8), ("x", DBL * 8), ("y", DBL * 8)]
+
+
+class Octagon(ctypes.Structure):
+    _fields_ = [
+        ("nv", I32), ("degenerate", I32), ("vidx", I64 * 8),
+        ("vx", DBL * 8), ("vy", DBL * 8), ("ex", DBL * 8), ("ey", DBL * 8), ("thr", DBL * 8),
+        ("bbox", DBL * 4), ("box", DBL * 4), ("has_box", I32), ("plain", I32),
+        ("guess_edge", I32 * 8), ("cx", DBL), ("cy", DBL),
+    ]
+
+
+class Result(ctypes.Structure):
+    _fields_ = [("count", I64), ("nonfinite", I32), ("degenerate", I32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("n", I64), ("n_survivors", I64), ("n_hull", I64),
+                ("ms_filter", DBL), ("ms_gather", DBL), ("ms_hull", DBL)]
+
+
+# name -> (restype, argtypes); every symbol declared in include/chfilter.h
+SIGNATURES = {
+    "ch_abi_version": (ctypes.c_int, []),
+    "ch_status_str": (ctypes.c_char_p, [ctypes.c_int]),
+    "ch_last_error": (ctypes.c_char_p, []),
+    "ch_workspace_bytes": (SZ, [I64]),
+    "ch_workspace_init": (ctypes.c_int, [P, SZ, P]),
+    "ch_extremes8": (ctypes.c_int, [P, I64, I64, ctypes.c_int, P, ctypes.POINTER(Extremes),
+                                    ctypes.POINTER(Octagon), P, SZ, P]),
+    "ch_combine8": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, SZ, P]),
+    "ch_octagon_build": (ctypes.c_int, [ctypes.POINTER(Extremes), ctypes.c_int, ctypes.POINTER(Octagon)]),
+    "ch_octagon_filter": (ctypes.c_int, [P, I64, ctypes.POINTER(Octagon), P, P, SZ, P]),
+    "ch_filter_compact": (ctypes.c_int, [P, I64, I64, ctypes.POINTER(Octagon), P, P, P, SZ, P]),
+    "ch_read_result": (ctypes.c_int, [P, ctypes.POINTER(Result), P]),
+    "ch_filter": (ctypes.c_int, [P, I64, ctypes.c_int, P, ctypes.POINTER(I64), P, SZ, P]),
+    "ch_filter_host": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, ctypes.POINTER(I64), P, SZ, P]),
+    "ch_gather_points": (ctypes.c_int, [P, I64, P, I64, P, P]),
+    "ch_hull_points": (ctypes.c_int, [P, P, I64, P, ctypes.POINTER(I64)]),
+    "ch_hull_end_to_end": (ctypes.c_int, [P, I64, ctypes.c_int, P, ctypes.POINTER(I64), P,
+                                          ctypes.POINTER(I64), ctypes.POINTER(Stats), P, SZ, P]),
+}
+
+_lib = None
+
+
+class CHError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: status {status} ({detail})")
+        self.status = status
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load():
+    """Load (building in-tree first if stale and nvcc exists) the library."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    try:
+        path = _build.build()
+    except Exception:
+        if not os.path.exists(path):
+            raise
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    lib.ch_orient_sign.restype = ctypes.c_int
+    lib.ch_orient_sign.argtypes = [DBL] * 6
+    if lib.ch_abi_version() != 1:
+        raise RuntimeError("libchfilter ABI mismatch")
+    _lib = lib
+    return lib
+
+
+def check(status: int, where: str):
+    if status != CH_OK:
+        lib = load()
+        detail = (lib.ch_last_error() or b"").decode()
+        raise CHError(status, where, f"{lib.ch_status_str(status).decode()}: {detail}")

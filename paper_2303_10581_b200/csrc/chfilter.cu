@@ -1,0 +1,1058 @@
+// chfilter.cu -- B200 (sm_100a) kernels and the C ABI of include/chfilter.h.
+//
+// The hot path is two streaming kernels over the float64 AoS point array:
+//   K1 k1_extremes8       one read of every point: the eight extremes (P:124,
+//                         P:185), grid combine, octagon built by the last CTA.
+//   K2 k2_filter_compact  the second and last read: octagon test fused
+//                         with a single-pass decoupled look-back compaction
+//                         (replaces the paper's filter/scan/scatter).
+// plus K3 k3_combine8 (multi-GPU exchange), K4 k4_octagon_bits (the paper's
+// bit vector) and a gather for the hull stage.
+//
+// Arithmetic follows DESIGN.md "Readings": binary64 RNE, explicit __d*_rn
+// intrinsics (never contracted), built with -fmad=false as well.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/chfilter.h"
+#include "octagon.cuh"
+
+extern "C" int64_t ch_internal_hull(const double *pts, const int64_t *ids, int64_t m, int64_t *hull);
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ----------------------------------------------------------------- layout --
+constexpr int K1_THREADS = 256;
+constexpr int K1_UNROLL = 4;                                   // LDG.256 per thread per chunk
+constexpr long long K1_CHUNK = (long long)K1_THREADS * K1_UNROLL * 2; // points per CTA iteration
+constexpr int K1_MAX_CTAS = 2048;
+
+constexpr int K2_THREADS = 256;
+constexpr int K2_WARPS = K2_THREADS / 32;
+constexpr int K2_UNROLL = 4;                                   // rows (LDG.256 per thread) per sub-tile
+constexpr long long K2_ROW = (long long)K2_THREADS * 2;        // 512 points per row
+constexpr long long K2_SUB = K2_ROW * K2_UNROLL;               // 2048 points per sub-tile
+constexpr int K2_MAXSUB = 32;                                  // sub-tiles per super-tile (max)
+constexpr int K2_ENTRIES = K2_MAXSUB * K2_UNROLL * K2_WARPS;   // (sub-tile, row, warp) groups
+static_assert(K2_ENTRIES == 4 * K2_THREADS, "block scan handles 4 entries per thread");
+
+constexpr int K4_THREADS = 256;
+
+// Look-back status word: flag(2) | epoch(22) | value(40).
+constexpr unsigned long long ST_A = 1ull, ST_P = 2ull;
+constexpr int ST_EPOCH_BITS = 22;
+constexpr unsigned long long ST_VALUE_MASK = (1ull << 40) - 1;
+constexpr unsigned ST_EPOCH_MASK = (1u << ST_EPOCH_BITS) - 1;
+
+struct Partial {
+    double key[8];
+    long long idx[8];
+    int nonfinite;
+    int pad[3];
+};
+
+struct WsHeader {
+    unsigned k1_ticket;
+    unsigned k2_claim;
+    unsigned k2_exit;
+    unsigned epoch;
+    ch_result result;
+    ch_extremes ext;
+    ch_octagon oct;
+};
+static_assert(sizeof(WsHeader) <= 4096, "header too large");
+constexpr size_t WS_HEADER = 4096;
+constexpr size_t WS_PARTIALS = (size_t)K1_MAX_CTAS * sizeof(Partial);
+
+inline long long ntiles_of(long long n) { return (n + K2_SUB - 1) / K2_SUB; } // >= super-tiles
+
+// ------------------------------------------------------------ PTX helpers --
+__device__ __forceinline__ void ld256(const double *p, double &a, double &b, double &c, double &d)
+{
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld128(const double *p, double &a, double &b)
+{
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+}
+// Two consecutive points (32 bytes): one LDG.256 when 32-byte aligned,
+// else two LDG.128.
+template <bool A32>
+__device__ __forceinline__ void ld2pts(const double *p, double &a, double &b, double &c, double &d)
+{
+    if (A32) {
+        ld256(p, a, b, c, d);
+    } else {
+        ld128(p, a, b);
+        ld128(p + 2, c, d);
+    }
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned lanemask_lt()
+{
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ===================================================================== K1 ==
+// One pass over the points: per-thread running extremes (walking indices
+// downward, so ">=" keeps the lowest index on ties), warp shuffles, CTA
+// partials, and an atomic ticket: the last CTA combines all partials (max
+// key, then lowest index: order independent, R2), builds the octagon on the
+// device and resets the ticket.  Non-finite detection: acc += x*0 (exact 0
+// for finite x, NaN otherwise) via DFMA.
+struct Best {
+    double v[8];
+    unsigned c[8];
+};
+
+__device__ __forceinline__ void k1_update(Best &b, double x, double y, unsigned code, double &acc)
+{
+    double s = __dadd_rn(x, y);
+    double d = __dsub_rn(x, y);
+    if (x >= b.v[0]) { b.v[0] = x; b.c[0] = code; }
+    if (s >= b.v[1]) { b.v[1] = s; b.c[1] = code; }
+    if (y >= b.v[2]) { b.v[2] = y; b.c[2] = code; }
+    if (d <= b.v[3]) { b.v[3] = d; b.c[3] = code; }
+    if (x <= b.v[4]) { b.v[4] = x; b.c[4] = code; }
+    if (s <= b.v[5]) { b.v[5] = s; b.c[5] = code; }
+    if (y <= b.v[6]) { b.v[6] = y; b.c[6] = code; }
+    if (d >= b.v[7]) { b.v[7] = d; b.c[7] = code; }
+    acc = __fma_rn(x, 0.0, acc);
+    acc = __fma_rn(y, 0.0, acc);
+}
+
+__device__ __forceinline__ void reduce_pair(int k, double &v, long long &i, double w, long long j)
+{
+    if (chf::slot_better(k, w, j, v, i)) {
+        v = w;
+        i = j;
+    }
+}
+
+__device__ void k1_finalize(const double *__restrict__ xy, long long index_base, int flags,
+                            WsHeader *hdr, const Partial *parts, int nparts, void *ext_out)
+{
+    // Called by every thread of the last CTA.
+    __shared__ double s_v[K1_THREADS / 32][8];
+    __shared__ long long s_i[K1_THREADS / 32][8];
+    __shared__ int s_nf;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double v[8];
+    long long id[8];
+    int nf = 0;
+    for (int k = 0; k < 8; k++) {
+        v[k] = chf::slot_is_max(k) ? -CH_INF : CH_INF;
+        id[k] = LLONG_MAX;
+    }
+    for (int p = tid; p < nparts; p += K1_THREADS) {
+        const Partial *q = parts + p;
+        for (int k = 0; k < 8; k++)
+            reduce_pair(k, v[k], id[k], __ldcg(&q->key[k]), __ldcg(&q->idx[k]));
+        nf |= __ldcg(&q->nonfinite);
+    }
+    nf = __syncthreads_or(nf);
+    for (int k = 0; k < 8; k++) {
+        for (int off = 16; off > 0; off >>= 1) {
+            double w = __shfl_xor_sync(FULL, v[k], off);
+            long long j = __shfl_xor_sync(FULL, id[k], off);
+            reduce_pair(k, v[k], id[k], w, j);
+        }
+        if (lane == 0) {
+            s_v[warp][k] = v[k];
+            s_i[warp][k] = id[k];
+        }
+    }
+    if (tid == 0)
+        s_nf = nf;
+    __syncthreads();
+    if (tid == 0) {
+        ch_extremes e;
+        for (int k = 0; k < 8; k++) {
+            double bv = s_v[0][k];
+            long long bi = s_i[0][k];
+            for (int w = 1; w < K1_THREADS / 32; w++)
+                reduce_pair(k, bv, bi, s_v[w][k], s_i[w][k]);
+            long long loc = bi - index_base;
+            e.idx[k] = bi;
+            e.x[k] = xy[2 * loc];
+            e.y[k] = xy[2 * loc + 1];
+        }
+        ch_octagon o;
+        chf::build_octagon(e, flags, o);
+        hdr->ext = e;
+        hdr->oct = o;
+        hdr->result.nonfinite = s_nf;
+        hdr->result.degenerate = o.degenerate;
+        if (ext_out)
+            *(ch_extremes *)ext_out = e;
+        hdr->k1_ticket = 0; // ready for the next call (stream order)
+    }
+}
+
+template <bool A32>
+__global__ void __launch_bounds__(K1_THREADS, 4)
+k1_extremes8(const double *__restrict__ xy, long long n, long long index_base, int flags,
+             WsHeader *hdr, Partial *parts, void *ext_out)
+{
+    const int tid = threadIdx.x;
+    Best b;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        b.v[k] = chf::slot_is_max(k) ? -CH_INF : CH_INF;
+        b.c[k] = 0xffffffffu;
+    }
+    double acc = 0.0;
+    const long long nchunks = (n + K1_CHUNK - 1) / K1_CHUNK;
+    for (long long c = nchunks - 1 - blockIdx.x; c >= 0; c -= gridDim.x) {
+        const long long base = c * K1_CHUNK;
+        const unsigned cc = (unsigned)(c * K1_UNROLL);
+        if (base + K1_CHUNK <= n) {
+            double v[K1_UNROLL][4];
+#pragma unroll
+            for (int u = 0; u < K1_UNROLL; u++)
+                ld2pts<A32>(xy + 2 * (base + 2 * ((long long)u * K1_THREADS + tid)), v[u][0], v[u][1], v[u][2], v[u][3]);
+#pragma unroll
+            for (int u = K1_UNROLL - 1; u >= 0; u--) {
+                k1_update(b, v[u][2], v[u][3], ((cc + u) << 1) | 1u, acc);
+                k1_update(b, v[u][0], v[u][1], ((cc + u) << 1), acc);
+            }
+        } else {
+            for (int u = K1_UNROLL - 1; u >= 0; u--) {
+                long long p = base + 2 * ((long long)u * K1_THREADS + tid);
+                for (int h = 1; h >= 0; h--) {
+                    if (p + h < n) {
+                        double x, y;
+                        ld128(xy + 2 * (p + h), x, y);
+                        k1_update(b, x, y, ((cc + u) << 1) | (unsigned)h, acc);
+                    }
+                }
+            }
+        }
+    }
+    // code -> local index
+    double v[8];
+    long long id[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        v[k] = b.v[k];
+        if (b.c[k] == 0xffffffffu) {
+            id[k] = LLONG_MAX;
+        } else {
+            unsigned q = b.c[k] >> 1, h = b.c[k] & 1u;
+            long long c = q / K1_UNROLL;
+            unsigned u = q % K1_UNROLL;
+            id[k] = index_base + c * K1_CHUNK + 2 * ((long long)u * K1_THREADS + tid) + h;
+        }
+    }
+    __shared__ double s_v[K1_THREADS / 32][8];
+    __shared__ long long s_i[K1_THREADS / 32][8];
+    __shared__ bool s_last;
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            double w = __shfl_xor_sync(FULL, v[k], off);
+            long long j = __shfl_xor_sync(FULL, id[k], off);
+            reduce_pair(k, v[k], id[k], w, j);
+        }
+        if (lane == 0) {
+            s_v[warp][k] = v[k];
+            s_i[warp][k] = id[k];
+        }
+    }
+    int nf = __syncthreads_or(acc != acc);
+    if (tid < 8) {
+        const int k = tid;
+        double bv = s_v[0][k];
+        long long bi = s_i[0][k];
+        for (int w = 1; w < K1_THREADS / 32; w++)
+            reduce_pair(k, bv, bi, s_v[w][k], s_i[w][k]);
+        parts[blockIdx.x].key[k] = bv;
+        parts[blockIdx.x].idx[k] = bi;
+        if (k == 0)
+            parts[blockIdx.x].nonfinite = nf;
+        __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        unsigned t = atomicAdd(&hdr->k1_ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        k1_finalize(xy, index_base, flags, hdr, parts, gridDim.x, ext_out);
+    }
+}
+
+// ===================================================================== K3 ==
+__global__ void k3_combine8(const ch_extremes *__restrict__ all, int world, int flags, WsHeader *hdr)
+{
+    if (threadIdx.x != 0)
+        return;
+    ch_extremes e;
+    for (int k = 0; k < 8; k++) {
+        double bv = chf::slot_is_max(k) ? -CH_INF : CH_INF;
+        long long bi = LLONG_MAX;
+        double bx = 0.0, by = 0.0;
+        for (int r = 0; r < world; r++) {
+            long long i = all[r].idx[k];
+            if (i < 0)
+                continue; // empty shard
+            double x = all[r].x[k], y = all[r].y[k];
+            double key = chf::slot_key(k, x, y);
+            if (chf::slot_better(k, key, i, bv, bi)) {
+                bv = key;
+                bi = i;
+                bx = x;
+                by = y;
+            }
+        }
+        e.idx[k] = bi;
+        e.x[k] = bx;
+        e.y[k] = by;
+    }
+    ch_octagon o;
+    chf::build_octagon(e, flags, o);
+    hdr->ext = e;
+    hdr->oct = o;
+    hdr->result.degenerate = o.degenerate;
+}
+
+// ========================================================= octagon test ==
+struct __align__(16) SEdge {
+    double ax, ay, ex, ey, thr, pad;
+};
+struct SOct {
+    SEdge e[8];
+    double box[4];
+    double cx, cy;
+    int nv, degenerate;
+    int guess[8];
+};
+
+__device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict__ o)
+{
+    const int t = threadIdx.x;
+    if (t < 8) {
+        s.e[t].ax = o->vx[t];
+        s.e[t].ay = o->vy[t];
+        s.e[t].ex = o->ex[t];
+        s.e[t].ey = o->ey[t];
+        s.e[t].thr = o->thr[t];
+        s.e[t].pad = 0.0;
+        s.guess[t] = o->guess_edge[t];
+    } else if (t == 8) {
+        s.box[0] = o->box[0];
+        s.box[1] = o->box[1];
+        s.box[2] = o->box[2];
+        s.box[3] = o->box[3];
+        s.cx = o->cx;
+        s.cy = o->cy;
+        s.nv = o->nv;
+        s.degenerate = o->degenerate;
+    }
+}
+
+// Survivor test, bit-identical to "not (forall k: D_k > T_k)" (R4): the
+// accept box and the edge order are shortcuts that cannot change the result
+// (box: proof at chf::box_valid; order: a conjunction is order-free).
+__device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
+{
+    if (x >= s.box[0] && x <= s.box[1] && y >= s.box[2] && y <= s.box[3])
+        return false;
+    const int nv = s.nv;
+    double dx = __dsub_rn(x, s.cx), dy = __dsub_rn(y, s.cy);
+    bool c = fabs(dx) >= fabs(dy);
+    int oct = dy >= 0.0 ? (dx >= 0.0 ? (c ? 0 : 1) : (c ? 3 : 2))
+                        : (dx < 0.0 ? (c ? 4 : 5) : (c ? 7 : 6));
+    int g = s.guess[oct];
+    for (int t = 0; t < nv; t++) {
+        int off = (t & 1) ? ((t + 1) >> 1) : -(t >> 1);
+        int k = g + off;
+        k = k < 0 ? k + nv : (k >= nv ? k - nv : k);
+        const SEdge &e = s.e[k];
+        double D = chf::edge_det(e.ax, e.ay, e.ex, e.ey, x, y);
+        if (!(D > e.thr))
+            return true;
+    }
+    return false;
+}
+
+// ===================================================================== K2 ==
+// Persistent CTAs (grid = resident capacity) claim "super-tiles" of
+// `subs` x K2_SUB consecutive points with one atomic each, in increasing
+// order, prefetching the next claim.  A super-tile is streamed as sub-tiles
+// of K2_SUB points: row u of sub-tile j holds points base_j + u*512 + 2t + h
+// for thread t (one LDG.256 per row); the octagon test's results are
+// ballot-ed per (sub-tile, row, warp) into shared memory (two words: h = 0
+// and h = 1 bits).  Then ONE decoupled look-back (Merrill & Garland) per
+// super-tile gives its global offset, a block scan of the popcounts gives
+// each 64-point group's offset, and the survivors' int64 indices are written
+// in index order ((j, u, warp, lane, h) lexicographic == increasing index).
+// Claims are made in increasing order by running CTAs, so every predecessor
+// of a claimed super-tile is owned by a running CTA: the look-back always
+// makes progress.
+template <bool A32>
+__global__ void __launch_bounds__(K2_THREADS, 4)
+k2_filter_compact(const double *__restrict__ xy, long long n, long long index_base,
+                  const ch_octagon *__restrict__ oct, WsHeader *hdr,
+                  unsigned long long *status, long long *__restrict__ out,
+                  long long *d_count, unsigned nsuper, int subs)
+{
+    __shared__ SOct so;
+    __shared__ unsigned s_bits[K2_ENTRIES][2];
+    __shared__ int s_scan[K2_ENTRIES];
+    __shared__ int s_wcnt[K2_WARPS];
+    __shared__ int s_wsum[K2_WARPS];
+    __shared__ unsigned s_claim, s_epoch;
+    __shared__ long long s_excl;
+    __shared__ int s_total;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    if (tid == 0) {
+        s_epoch = *(volatile unsigned *)&hdr->epoch;
+        __threadfence();
+        s_claim = atomicAdd(&hdr->k2_claim, 1u);
+    }
+    load_soct(so, oct);
+    __syncthreads();
+    const unsigned epoch = s_epoch & ST_EPOCH_MASK;
+    const long long super_pts = (long long)subs * K2_SUB;
+    unsigned cur = s_claim;
+
+    while (cur < nsuper) {
+        unsigned nxt = 0;
+        if (tid == 0)
+            nxt = atomicAdd(&hdr->k2_claim, 1u); // prefetch the next claim
+        const long long sbase = (long long)cur * super_pts;
+        const int nsub = (int)min((long long)subs, (n - sbase + K2_SUB - 1) / K2_SUB);
+        int wcnt = 0;
+        for (int j = 0; j < nsub; j++) {
+            const long long base = sbase + (long long)j * K2_SUB;
+            unsigned keep = 0; // bit 2u + h
+            if (so.degenerate) {
+#pragma unroll
+                for (int u = 0; u < K2_UNROLL; u++) {
+                    long long p = base + u * K2_ROW + 2 * tid;
+                    keep |= (p < n ? 1u : 0u) << (2 * u);
+                    keep |= (p + 1 < n ? 1u : 0u) << (2 * u + 1);
+                }
+            } else if (base + K2_SUB <= n) {
+                double v[K2_UNROLL][4];
+#pragma unroll
+                for (int u = 0; u < K2_UNROLL; u++)
+                    ld2pts<A32>(xy + 2 * (base + u * K2_ROW + 2 * tid), v[u][0], v[u][1], v[u][2], v[u][3]);
+#pragma unroll
+                for (int u = 0; u < K2_UNROLL; u++) {
+                    keep |= (keep_point(so, v[u][0], v[u][1]) ? 1u : 0u) << (2 * u);
+                    keep |= (keep_point(so, v[u][2], v[u][3]) ? 1u : 0u) << (2 * u + 1);
+                }
+            } else {
+                for (int u = 0; u < K2_UNROLL; u++) {
+                    long long p = base + u * K2_ROW + 2 * tid;
+                    for (int h = 0; h < 2; h++) {
+                        if (p + h < n) {
+                            double x, y;
+                            ld128(xy + 2 * (p + h), x, y);
+                            keep |= (keep_point(so, x, y) ? 1u : 0u) << (2 * u + h);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < K2_UNROLL; u++) {
+                unsigned b0 = __ballot_sync(FULL, (keep >> (2 * u)) & 1u);
+                unsigned b1 = __ballot_sync(FULL, (keep >> (2 * u + 1)) & 1u);
+                if (lane == 0) {
+                    int e = (j * K2_UNROLL + u) * K2_WARPS + warp;
+                    s_bits[e][0] = b0;
+                    s_bits[e][1] = b1;
+                }
+                wcnt += __popc(b0) + __popc(b1);
+            }
+        }
+        if (lane == 0)
+            s_wcnt[warp] = wcnt;
+        __syncthreads();
+        if (warp == 0) {
+            int total = lane < K2_WARPS ? s_wcnt[lane] : 0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+                total += __shfl_xor_sync(FULL, total, off);
+            // ---- decoupled look-back over super-tiles ----
+            long long excl = 0;
+            if (cur == 0) {
+                if (lane == 0)
+                    st_release(&status[0], (ST_P << 62) | ((unsigned long long)epoch << 40) |
+                                               ((unsigned long long)total & ST_VALUE_MASK));
+            } else {
+                if (lane == 0)
+                    st_release(&status[cur], (ST_A << 62) | ((unsigned long long)epoch << 40) |
+                                                 ((unsigned long long)total & ST_VALUE_MASK));
+                long long pos = (long long)cur - 1;
+                while (true) {
+                    long long j = pos - lane;
+                    unsigned long long flag = ST_P, val = 0;
+                    unsigned pm, xm, need;
+                    while (true) {
+                        if (j >= 0) {
+                            unsigned long long st = ld_acquire(&status[j]);
+                            bool ok = (unsigned)((st >> 40) & ST_EPOCH_MASK) == epoch && (st >> 62) != 0;
+                            flag = ok ? (st >> 62) : 0;
+                            val = st & ST_VALUE_MASK;
+                        }
+                        pm = __ballot_sync(FULL, flag == ST_P);
+                        xm = __ballot_sync(FULL, flag == 0);
+                        need = pm ? (((pm & (0u - pm)) << 1) - 1u) : FULL; // lanes up to the first P
+                        if ((xm & need) == 0)
+                            break;
+                    }
+                    unsigned long long c = ((need >> lane) & 1u) ? val : 0ull;
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1)
+                        c += __shfl_xor_sync(FULL, c, off);
+                    excl += (long long)c;
+                    if (pm)
+                        break;
+                    pos -= 32;
+                }
+                if (lane == 0)
+                    st_release(&status[cur], (ST_P << 62) | ((unsigned long long)epoch << 40) |
+                                                 ((unsigned long long)(excl + total) & ST_VALUE_MASK));
+            }
+            if (lane == 0) {
+                s_excl = excl;
+                s_total = total;
+                if (cur == nsuper - 1) {
+                    hdr->result.count = excl + total;
+                    if (d_count)
+                        *d_count = excl + total;
+                }
+            }
+        }
+        __syncthreads();
+        if (s_total > 0) {
+            // block exclusive scan of the (sub-tile, row, warp) popcounts, 4 per thread
+            const int E = nsub * K2_UNROLL * K2_WARPS;
+            int c[4], sum = 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                int e = 4 * tid + q;
+                c[q] = e < E ? __popc(s_bits[e][0]) + __popc(s_bits[e][1]) : 0;
+                sum += c[q];
+            }
+            int inc = sum;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                int t = __shfl_up_sync(FULL, inc, off);
+                if (lane >= off)
+                    inc += t;
+            }
+            if (lane == 31)
+                s_wsum[warp] = inc;
+            __syncthreads();
+            int ex = inc - sum;
+            for (int w = 0; w < warp; w++)
+                ex += s_wsum[w];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                int e = 4 * tid + q;
+                if (e < E)
+                    s_scan[e] = ex;
+                ex += c[q];
+            }
+            __syncthreads();
+            const long long excl = s_excl;
+            const unsigned lt = lanemask_lt();
+            for (int j = 0; j < nsub; j++) {
+#pragma unroll
+                for (int u = 0; u < K2_UNROLL; u++) {
+                    int e = (j * K2_UNROLL + u) * K2_WARPS + warp;
+                    unsigned b0 = s_bits[e][0], b1 = s_bits[e][1];
+                    if ((b0 | b1) == 0)
+                        continue;
+                    unsigned k0 = (b0 >> lane) & 1u, k1 = (b1 >> lane) & 1u;
+                    long long pos = excl + s_scan[e] + __popc(b0 & lt) + __popc(b1 & lt);
+                    long long gi = index_base + sbase + (long long)j * K2_SUB + u * K2_ROW + 2 * tid;
+                    if (k0)
+                        out[pos] = gi;
+                    if (k1)
+                        out[pos + k0] = gi + 1;
+                }
+            }
+        }
+        if (tid == 0)
+            s_claim = nxt;
+        __syncthreads();
+        cur = s_claim;
+    }
+    // exit protocol: the last CTA to leave resets the counters, bumps the epoch
+    if (tid == 0) {
+        __threadfence();
+        unsigned e = atomicAdd(&hdr->k2_exit, 1u);
+        if (e == gridDim.x - 1) {
+            hdr->k2_claim = 0;
+            hdr->k2_exit = 0;
+            hdr->epoch = (s_epoch + 1) & ST_EPOCH_MASK;
+            if (nsuper == 0) {
+                hdr->result.count = 0;
+                if (d_count)
+                    *d_count = 0;
+            }
+        }
+    }
+}
+
+// ===================================================================== K4 ==
+__global__ void __launch_bounds__(K4_THREADS)
+k4_octagon_bits(const double *__restrict__ xy, long long n, const ch_octagon *__restrict__ oct,
+                unsigned *__restrict__ bits)
+{
+    __shared__ SOct so;
+    load_soct(so, oct);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long nwords = (n + 31) / 32;
+    const long long wstride = (long long)gridDim.x * (K4_THREADS / 32);
+    for (long long w = (long long)blockIdx.x * (K4_THREADS / 32) + (threadIdx.x >> 5); w < nwords; w += wstride) {
+        long long p = w * 32 + lane;
+        bool k = false;
+        if (p < n) {
+            double x, y;
+            ld128(xy + 2 * p, x, y);
+            k = so.degenerate ? true : keep_point(so, x, y);
+        }
+        unsigned b = __ballot_sync(FULL, k);
+        if (lane == 0)
+            bits[w] = b;
+    }
+}
+
+__global__ void k_gather(const double *__restrict__ xy, long long index_base, const long long *__restrict__ idx,
+                         long long m, double *__restrict__ outp)
+{
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x) {
+        long long i = idx[j] - index_base;
+        double x, y;
+        ld128(xy + 2 * i, x, y);
+        outp[2 * j] = x;
+        outp[2 * j + 1] = y;
+    }
+}
+
+// ================================================================ host side ==
+thread_local std::string g_err;
+
+ch_status fail(ch_status s, const std::string &msg)
+{
+    g_err = msg;
+    return s;
+}
+
+ch_status cuda_check(const char *what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return fail(CH_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return CH_OK;
+}
+
+struct DevInfo {
+    int sms = 0;
+    int k1_per_sm = 0;
+    int k2_per_sm = 0;
+};
+
+DevInfo dev_info()
+{
+    static thread_local int cached_dev = -1;
+    static thread_local DevInfo info;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != cached_dev) {
+        cudaDeviceGetAttribute(&info.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k1_per_sm, k1_extremes8<true>, K1_THREADS, 0);
+        if (info.k1_per_sm < 1)
+            info.k1_per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k2_per_sm, k2_filter_compact<true>, K2_THREADS, 0);
+        int k2b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k2b, k2_filter_compact<false>, K2_THREADS, 0);
+        info.k2_per_sm = std::max(1, std::min(info.k2_per_sm, k2b));
+        cached_dev = dev;
+    }
+    return info;
+}
+
+ch_status check_ws(const void *d_ws, size_t ws_bytes, long long n)
+{
+    if (!d_ws)
+        return fail(CH_ERR_WORKSPACE, "workspace is NULL");
+    if (((uintptr_t)d_ws & 255u) != 0)
+        return fail(CH_ERR_WORKSPACE, "workspace must be 256-byte aligned");
+    if (ws_bytes < ch_workspace_bytes(n))
+        return fail(CH_ERR_WORKSPACE, "workspace too small for n");
+    return CH_OK;
+}
+
+ch_status check_points(const double *d_xy, long long n)
+{
+    if (n < 0)
+        return fail(CH_ERR_INVALID_ARG, "n < 0");
+    if (n == 0)
+        return fail(CH_ERR_EMPTY, "n == 0 (EmptySet)");
+    if (!d_xy)
+        return fail(CH_ERR_INVALID_ARG, "d_xy is NULL");
+    if (((uintptr_t)d_xy & 15u) != 0)
+        return fail(CH_ERR_MISALIGNED, "d_xy must be 16-byte aligned");
+    if (n > (1ll << 39))
+        return fail(CH_ERR_INVALID_ARG, "n > 2^39 unsupported");
+    return CH_OK;
+}
+
+inline WsHeader *hdr_of(void *d_ws) { return (WsHeader *)d_ws; }
+inline Partial *parts_of(void *d_ws) { return (Partial *)((char *)d_ws + WS_HEADER); }
+inline unsigned long long *status_of(void *d_ws)
+{
+    return (unsigned long long *)((char *)d_ws + WS_HEADER + WS_PARTIALS);
+}
+
+ch_status launch_k1(const double *d_xy, long long n, long long index_base, int flags, void *d_ext_out,
+                    void *d_ws, cudaStream_t st)
+{
+    DevInfo di = dev_info();
+    long long nchunks = (n + K1_CHUNK - 1) / K1_CHUNK;
+    long long g = std::min<long long>((long long)di.sms * di.k1_per_sm, nchunks);
+    g = std::min<long long>(g, K1_MAX_CTAS);
+    if (g < 1)
+        g = 1;
+    if (((uintptr_t)d_xy & 31u) == 0)
+        k1_extremes8<true><<<(unsigned)g, K1_THREADS, 0, st>>>(d_xy, n, index_base, flags, hdr_of(d_ws),
+                                                                parts_of(d_ws), d_ext_out);
+    else
+        k1_extremes8<false><<<(unsigned)g, K1_THREADS, 0, st>>>(d_xy, n, index_base, flags, hdr_of(d_ws),
+                                                                 parts_of(d_ws), d_ext_out);
+    return cuda_check("k1_extremes8");
+}
+
+ch_status stage_octagon(const ch_octagon *h_oct, void *d_ws, cudaStream_t st, const ch_octagon **d_oct)
+{
+    WsHeader *h = hdr_of(d_ws);
+    if (h_oct) {
+        cudaMemcpyAsync(&h->oct, h_oct, sizeof(ch_octagon), cudaMemcpyHostToDevice, st);
+        cudaMemsetAsync(&h->result.nonfinite, 0, sizeof(int32_t), st); // no K1 pass: nothing checked
+        ch_status s = cuda_check("octagon upload");
+        if (s != CH_OK)
+            return s;
+    }
+    *d_oct = &h->oct;
+    return CH_OK;
+}
+
+ch_status launch_k2(const double *d_xy, long long n, long long index_base, const ch_octagon *d_oct,
+                    long long *d_surv, long long *d_count, void *d_ws, cudaStream_t st)
+{
+    DevInfo di = dev_info();
+    long long resident = (long long)di.sms * di.k2_per_sm;
+    long long nsub_total = (n + K2_SUB - 1) / K2_SUB;
+    // aim for >= 8 super-tiles per CTA (load balance), <= K2_MAXSUB sub-tiles each
+    long long subs = (nsub_total + resident * 8 - 1) / (resident * 8);
+    subs = std::max<long long>(1, std::min<long long>(subs, K2_MAXSUB));
+    long long nsuper = (nsub_total + subs - 1) / subs;
+    long long grid = std::max<long long>(1, std::min<long long>(resident, nsuper));
+    if (((uintptr_t)d_xy & 31u) == 0)
+        k2_filter_compact<true><<<(unsigned)grid, K2_THREADS, 0, st>>>(
+            d_xy, n, index_base, d_oct, hdr_of(d_ws), status_of(d_ws), d_surv, d_count, (unsigned)nsuper, (int)subs);
+    else
+        k2_filter_compact<false><<<(unsigned)grid, K2_THREADS, 0, st>>>(
+            d_xy, n, index_base, d_oct, hdr_of(d_ws), status_of(d_ws), d_surv, d_count, (unsigned)nsuper, (int)subs);
+    return cuda_check("k2_filter_compact");
+}
+
+} // namespace
+
+// ================================================================== C ABI ==
+extern "C" {
+
+int ch_abi_version(void) { return CH_ABI_VERSION; }
+
+const char *ch_status_str(ch_status s)
+{
+    switch (s) {
+    case CH_OK: return "CH_OK";
+    case CH_ERR_INVALID_ARG: return "CH_ERR_INVALID_ARG";
+    case CH_ERR_EMPTY: return "CH_ERR_EMPTY";
+    case CH_ERR_NONFINITE: return "CH_ERR_NONFINITE";
+    case CH_ERR_MISALIGNED: return "CH_ERR_MISALIGNED";
+    case CH_ERR_WORKSPACE: return "CH_ERR_WORKSPACE";
+    case CH_ERR_CUDA: return "CH_ERR_CUDA";
+    }
+    return "CH_ERR_UNKNOWN";
+}
+
+const char *ch_last_error(void) { return g_err.c_str(); }
+
+size_t ch_workspace_bytes(int64_t n)
+{
+    if (n < 0)
+        n = 0;
+    size_t tiles = (size_t)ntiles_of(n) + 1;
+    size_t b = WS_HEADER + WS_PARTIALS + tiles * sizeof(unsigned long long);
+    return (b + 4095) & ~(size_t)4095;
+}
+
+ch_status ch_workspace_init(void *d_ws, size_t ws_bytes, void *stream)
+{
+    if (!d_ws || ws_bytes < WS_HEADER + WS_PARTIALS)
+        return fail(CH_ERR_WORKSPACE, "workspace missing or too small");
+    cudaMemsetAsync(d_ws, 0, ws_bytes, (cudaStream_t)stream);
+    return cuda_check("workspace init");
+}
+
+ch_status ch_octagon_build(const ch_extremes *ext, int flags, ch_octagon *out)
+{
+    if (!ext || !out)
+        return fail(CH_ERR_INVALID_ARG, "NULL argument");
+    chf::build_octagon(*ext, flags, *out);
+    return CH_OK;
+}
+
+ch_status ch_read_result(const void *d_ws, ch_result *h_res, void *stream)
+{
+    if (!d_ws || !h_res)
+        return fail(CH_ERR_INVALID_ARG, "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemcpyAsync(h_res, &((const WsHeader *)d_ws)->result, sizeof(ch_result), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    ch_status s = cuda_check("read result");
+    if (s != CH_OK)
+        return s;
+    if (h_res->nonfinite)
+        return fail(CH_ERR_NONFINITE, "non-finite coordinate in input");
+    return CH_OK;
+}
+
+ch_status ch_extremes8(const double *d_xy, int64_t n, int64_t index_base, int flags, void *d_ext_out,
+                       ch_extremes *h_ext, ch_octagon *h_oct, void *d_ws, size_t ws_bytes, void *stream)
+{
+    ch_status s = check_points(d_xy, n);
+    if (s != CH_OK)
+        return s;
+    if ((s = check_ws(d_ws, ws_bytes, n)) != CH_OK)
+        return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((s = launch_k1(d_xy, n, index_base, flags, d_ext_out, d_ws, st)) != CH_OK)
+        return s;
+    if (h_ext || h_oct) {
+        WsHeader *h = hdr_of(d_ws);
+        if (h_ext)
+            cudaMemcpyAsync(h_ext, &h->ext, sizeof(ch_extremes), cudaMemcpyDeviceToHost, st);
+        if (h_oct)
+            cudaMemcpyAsync(h_oct, &h->oct, sizeof(ch_octagon), cudaMemcpyDeviceToHost, st);
+        ch_result r;
+        return ch_read_result(d_ws, &r, stream);
+    }
+    return CH_OK;
+}
+
+ch_status ch_combine8(const void *d_ext_all, int world, int flags, void *d_ws, size_t ws_bytes, void *stream)
+{
+    if (!d_ext_all || world < 1)
+        return fail(CH_ERR_INVALID_ARG, "bad extremes array / world");
+    ch_status s = check_ws(d_ws, ws_bytes, 0);
+    if (s != CH_OK)
+        return s;
+    k3_combine8<<<1, 32, 0, (cudaStream_t)stream>>>((const ch_extremes *)d_ext_all, world, flags, hdr_of(d_ws));
+    return cuda_check("k3_combine8");
+}
+
+ch_status ch_octagon_filter(const double *d_xy, int64_t n, const ch_octagon *h_oct, uint32_t *d_keep_bits,
+                            void *d_ws, size_t ws_bytes, void *stream)
+{
+    ch_status s = check_points(d_xy, n);
+    if (s != CH_OK)
+        return s;
+    if (!d_keep_bits)
+        return fail(CH_ERR_INVALID_ARG, "d_keep_bits is NULL");
+    if ((s = check_ws(d_ws, ws_bytes, 0)) != CH_OK)
+        return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const ch_octagon *d_oct;
+    if ((s = stage_octagon(h_oct, d_ws, st, &d_oct)) != CH_OK)
+        return s;
+    DevInfo di = dev_info();
+    long long nwords = (n + 31) / 32;
+    long long g = std::min<long long>((nwords + 7) / 8, (long long)di.sms * 8);
+    k4_octagon_bits<<<(unsigned)std::max<long long>(g, 1), K4_THREADS, 0, st>>>(d_xy, n, d_oct, d_keep_bits);
+    return cuda_check("k4_octagon_bits");
+}
+
+ch_status ch_filter_compact(const double *d_xy, int64_t n, int64_t index_base, const ch_octagon *h_oct,
+                            int64_t *d_survivors, int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream)
+{
+    ch_status s = check_points(d_xy, n);
+    if (s != CH_OK)
+        return s;
+    if (!d_survivors)
+        return fail(CH_ERR_INVALID_ARG, "d_survivors is NULL");
+    if ((s = check_ws(d_ws, ws_bytes, n)) != CH_OK)
+        return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const ch_octagon *d_oct;
+    if ((s = stage_octagon(h_oct, d_ws, st, &d_oct)) != CH_OK)
+        return s;
+    return launch_k2(d_xy, n, index_base, d_oct, (long long *)d_survivors, (long long *)d_count, d_ws, st);
+}
+
+ch_status ch_filter(const double *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *h_count,
+                    void *d_ws, size_t ws_bytes, void *stream)
+{
+    ch_status s = ch_extremes8(d_xy, n, 0, flags, nullptr, nullptr, nullptr, d_ws, ws_bytes, stream);
+    if (s != CH_OK)
+        return s;
+    if ((s = ch_filter_compact(d_xy, n, 0, nullptr, d_survivors, nullptr, d_ws, ws_bytes, stream)) != CH_OK)
+        return s;
+    ch_result r;
+    s = ch_read_result(d_ws, &r, stream);
+    if (h_count)
+        *h_count = r.count;
+    return s;
+}
+
+ch_status ch_filter_host(const double *h_xy, int64_t n, int flags, double *d_xy_staging, int64_t *d_survivors,
+                         int64_t *h_survivors, int64_t *h_count, void *d_ws, size_t ws_bytes, void *stream)
+{
+    if (!h_xy || !h_survivors || !d_xy_staging)
+        return fail(CH_ERR_INVALID_ARG, "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n > 0) {
+        cudaMemcpyAsync(d_xy_staging, h_xy, (size_t)n * 16, cudaMemcpyHostToDevice, st);
+        ch_status s0 = cuda_check("h2d copy");
+        if (s0 != CH_OK)
+            return s0;
+    }
+    int64_t cnt = 0;
+    ch_status s = ch_filter(d_xy_staging, n, flags, d_survivors, &cnt, d_ws, ws_bytes, stream);
+    if (s != CH_OK)
+        return s;
+    if (cnt > 0)
+        cudaMemcpyAsync(h_survivors, d_survivors, (size_t)cnt * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if ((s = cuda_check("d2h copy")) != CH_OK)
+        return s;
+    if (h_count)
+        *h_count = cnt;
+    return CH_OK;
+}
+
+ch_status ch_gather_points(const double *d_xy, int64_t index_base, const int64_t *d_idx, int64_t m, double *d_out,
+                           void *stream)
+{
+    if (m < 0 || (m > 0 && (!d_xy || !d_idx || !d_out)))
+        return fail(CH_ERR_INVALID_ARG, "bad gather arguments");
+    if (m == 0)
+        return CH_OK;
+    DevInfo di = dev_info();
+    long long g = std::min<long long>((m + 255) / 256, (long long)di.sms * 8);
+    k_gather<<<(unsigned)g, 256, 0, (cudaStream_t)stream>>>(d_xy, index_base, (const long long *)d_idx, m, d_out);
+    return cuda_check("gather");
+}
+
+ch_status ch_hull_points(const double *h_pts, const int64_t *h_ids, int64_t m, int64_t *h_hull, int64_t *h_n_hull)
+{
+    if (m < 0 || !h_n_hull || (m > 0 && (!h_pts || !h_ids || !h_hull)))
+        return fail(CH_ERR_INVALID_ARG, "bad hull arguments");
+    *h_n_hull = ch_internal_hull(h_pts, h_ids, m, h_hull);
+    return CH_OK;
+}
+
+ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *h_n_survivors,
+                             int64_t *h_hull, int64_t *h_n_hull, ch_stats *h_stats, void *d_ws, size_t ws_bytes,
+                             void *stream)
+{
+    if (!h_hull || !h_n_hull || !d_survivors)
+        return fail(CH_ERR_INVALID_ARG, "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    int64_t cnt = 0;
+    ch_status s = ch_filter(d_xy, n, flags, d_survivors, &cnt, d_ws, ws_bytes, stream);
+    cudaEventRecord(e1, st);
+    if (s != CH_OK) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return s;
+    }
+    cudaEventSynchronize(e1);
+    float ms_filter = 0.f;
+    cudaEventElapsedTime(&ms_filter, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<double> pts((size_t)cnt * 2);
+    std::vector<int64_t> ids((size_t)cnt);
+    if (cnt > 0) {
+        double *d_pts = nullptr;
+        if (cudaMallocAsync((void **)&d_pts, (size_t)cnt * 16, st) != cudaSuccess)
+            return fail(CH_ERR_CUDA, "cudaMallocAsync for the hull gather failed");
+        if ((s = ch_gather_points(d_xy, 0, d_survivors, cnt, d_pts, stream)) != CH_OK)
+            return s;
+        cudaMemcpyAsync(pts.data(), d_pts, (size_t)cnt * 16, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(ids.data(), d_survivors, (size_t)cnt * 8, cudaMemcpyDeviceToHost, st);
+        cudaFreeAsync(d_pts, st);
+        cudaStreamSynchronize(st);
+        if ((s = cuda_check("hull gather")) != CH_OK)
+            return s;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    int64_t h = ch_internal_hull(pts.data(), ids.data(), cnt, h_hull);
+    auto t2 = std::chrono::steady_clock::now();
+    *h_n_hull = h;
+    if (h_n_survivors)
+        *h_n_survivors = cnt;
+    if (h_stats) {
+        h_stats->n = n;
+        h_stats->n_survivors = cnt;
+        h_stats->n_hull = h;
+        h_stats->ms_filter = ms_filter;
+        h_stats->ms_gather = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        h_stats->ms_hull = std::chrono::duration<double, std::milli>(t2 - t1).count();
+    }
+    return CH_OK;
+}
+
+// Test hook (not part of the documented ABI): the hull's exact orientation.
+int ch_orient_sign(double ax, double ay, double bx, double by, double cx, double cy)
+{
+    extern int ch_internal_orient_sign(double, double, double, double, double, double);
+    return ch_internal_orient_sign(ax, ay, bx, by, cx, cy);
+}
+
+} // extern "C"

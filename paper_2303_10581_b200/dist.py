@@ -1,0 +1,116 @@
+"""Multi-GPU filter: one process per GPU, points sharded by contiguous index
+ranges (DESIGN R14), torch.distributed (NCCL over NVLink) for the two real
+exchange steps of the path (north_star):
+
+  a4  all-gather of each rank's eight extremes (one 192-byte ch_extremes
+      record per rank), then K3 (ch_combine8) repeated identically on every
+      rank -> the global octagon, bit-identical to the 1-GPU result;
+  a7  all-gather of the per-rank survivor counts, exclusive scan -> each
+      rank's offset in the one logical, globally ordered survivor array.
+
+The survivors stay distributed (rank r owns [off_r, off_r + cnt_r)); the
+physical gather belongs to the separately timed hull stage.
+
+The collective helpers (`exchange_extremes`, `exclusive_offsets`) work on
+CPU tensors with the gloo backend as well, which is how the host logic is
+tested without GPUs (tests/test_dist_gloo.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import Workspace, _points, combine8, extremes8_async, filter_compact
+
+EXT_WORDS = 24  # ch_extremes = int64 idx[8] + double x[8] + double y[8]
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Rank r owns global points [floor(r n / W), floor((r + 1) n / W))."""
+    return (rank * n) // world, ((rank + 1) * n) // world
+
+
+def pack_extremes(idx, x, y) -> torch.Tensor:
+    """A ch_extremes record as 24 int64 words (x, y as their bit patterns).
+    idx = -1 marks an empty shard (ignored by the combine)."""
+    w = np.empty(EXT_WORDS, dtype=np.int64)
+    w[0:8] = np.asarray(idx, dtype=np.int64)
+    w[8:16] = np.asarray(x, dtype=np.float64).view(np.int64)
+    w[16:24] = np.asarray(y, dtype=np.float64).view(np.int64)
+    return torch.from_numpy(w)
+
+
+def unpack_extremes(words) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    w = np.asarray(words.cpu() if isinstance(words, torch.Tensor) else words, dtype=np.int64).reshape(-1, EXT_WORDS)
+    return w[:, 0:8].copy(), w[:, 8:16].view(np.float64).copy(), w[:, 16:24].view(np.float64).copy()
+
+
+def empty_record(device) -> torch.Tensor:
+    t = pack_extremes([-1] * 8, [0.0] * 8, [0.0] * 8)
+    return t.to(device)
+
+
+def exchange_extremes(ext_local: torch.Tensor, group=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """a4: all-gather one record per rank -> [world * 24] int64 (rank order)."""
+    world = dist.get_world_size(group)
+    if out is None:
+        out = torch.empty(world * EXT_WORDS, dtype=torch.int64, device=ext_local.device)
+    dist.all_gather_into_tensor(out, ext_local, group=group)
+    return out
+
+
+def exclusive_offsets(count: torch.Tensor, group=None, out: torch.Tensor | None = None):
+    """a7: all-gather of the int64 counts.  Returns the gathered tensor
+    (device); `offsets_from_counts` turns it into (offset, total)."""
+    world = dist.get_world_size(group)
+    if out is None:
+        out = torch.empty(world, dtype=torch.int64, device=count.device)
+    dist.all_gather_into_tensor(out, count.reshape(1), group=group)
+    return out
+
+
+def offsets_from_counts(counts, rank: int) -> tuple[int, int]:
+    c = [int(v) for v in (counts.tolist() if isinstance(counts, torch.Tensor) else counts)]
+    return sum(c[:rank]), sum(c)
+
+
+class DistFilter:
+    """Per-rank state for the sharded filter step (all device buffers are
+    allocated once; `step` only enqueues work)."""
+
+    def __init__(self, n_global: int, xy_local: torch.Tensor, group=None, plain: bool = False):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.n_global = int(n_global)
+        self.lo, self.hi = shard_range(self.n_global, self.world, self.rank)
+        self.n_local = self.hi - self.lo
+        if xy_local.shape[0] != self.n_local:
+            raise ValueError("local shard size does not match shard_range")
+        self.xy = _points(xy_local) if self.n_local > 0 else xy_local
+        dev = xy_local.device
+        self.plain = plain
+        self.ws = Workspace(max(self.n_local, 1), device=dev)
+        self.ext_local = empty_record(dev)
+        self.ext_all = torch.empty(self.world * EXT_WORDS, dtype=torch.int64, device=dev)
+        self.count = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.counts = torch.empty(self.world, dtype=torch.int64, device=dev)
+        self.out = torch.empty(max(self.n_local, 1), dtype=torch.int64, device=dev)
+
+    def step(self, xy_local: torch.Tensor | None = None):
+        """K1 -> all-gather extremes -> K3 -> K2 -> all-gather counts (async)."""
+        xy = self.xy if xy_local is None else xy_local
+        if self.n_local > 0:
+            extremes8_async(xy, self.ws, index_base=self.lo, plain=self.plain, ext_out=self.ext_local)
+        exchange_extremes(self.ext_local, self.group, out=self.ext_all)
+        combine8(self.ext_all, self.world, self.ws, plain=self.plain)
+        if self.n_local > 0:
+            filter_compact(xy, self.ws, index_base=self.lo, out=self.out, count=self.count)
+        exclusive_offsets(self.count, self.group, out=self.counts)
+
+    def result(self):
+        """(local survivor indices (device view), offset, total) -- synchronizes."""
+        off, total = offsets_from_counts(self.counts, self.rank)
+        cnt = int(self.counts[self.rank].item())
+        return self.out[:cnt], off, total

@@ -1,0 +1,268 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+element by element, on the same seeded bytes.  Integer / index outputs
+(extremes, survivor indices, hull ids) must be bit-exact; the octagon's
+floating-point fields must be bit-identical too (same binary64 operations in
+the same order)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2303_10581_b200 as chf
+import synth
+from exact import load_golden, near_edge_points
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def gpu_all(xy_d, plain=False, ws=None):
+    n = xy_d.shape[0]
+    ws = ws or chf.Workspace(n)
+    e, o = chf.extremes8(xy_d, ws, plain=plain)
+    surv = chf.filter(xy_d, ws, plain=plain).cpu().numpy()
+    return chf.extremes_tuple(e)[0], chf.octagon_dict(o), surv, ws
+
+
+def check_against_oracle(xy_d, plain=False, ws=None, name=""):
+    xy = xy_d.cpu().numpy()
+    idx, o, surv, ws = gpu_all(xy_d, plain, ws)
+    want_s, want_idx = oracle.filter_compact(xy, certified=not plain)
+    assert np.array_equal(idx, want_idx), (name, idx, want_idx)
+    wo = oracle.octagon(xy, want_idx, certified=not plain)
+    assert o["nv"] == wo["nv"] and o["degenerate"] == wo["degenerate"], name
+    for f in ("vx", "vy", "ex", "ey", "thr"):
+        assert np.array_equal(o[f].view(np.int64), wo[f].view(np.int64)), (name, f)
+    assert np.array_equal(surv, want_s), (name, len(surv), len(want_s))
+    return surv, ws
+
+
+# ------------------------------------------------------------- golden -------
+@pytest.mark.parametrize("ex", load_golden(), ids=[g["name"] for g in load_golden()])
+def test_golden_on_gpu(ex):
+    xy_d = torch.tensor(ex["points"], dtype=torch.float64, device=DEV)
+    idx, o, surv, ws = gpu_all(xy_d)
+    assert list(idx) == ex["extremes"]
+    assert list(o["vidx"]) == ex["octagon"]
+    assert o["degenerate"] == ex["degenerate"]
+    assert list(surv) == ex["survivors"]
+    hull, s2, st = chf.hull_end_to_end(xy_d, ws)
+    assert list(hull) == ex["hull"]
+    assert list(s2.cpu().numpy()) == ex["survivors"]
+
+
+# ------------------------------------------------- sizes and distributions --
+SIZES = [1, 2, 3, 31, 511, 512, 4095, 4096, 4097, 10_000, 123_457, 1_000_003]
+
+
+@pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
+@pytest.mark.parametrize("n", SIZES)
+def test_parity_sizes(dist, n):
+    xy_d = synth.points(dist, n, seed=n % 7, device=DEV)
+    check_against_oracle(xy_d, name=f"{dist}-{n}")
+
+
+def test_parity_config1_normal_1e4_seed0():
+    """BASELINE.json configs[0]: 10^4 normal points, seed 0."""
+    xy_d = synth.points("normal", 10 ** 4, seed=0, device=DEV)
+    surv, _ = check_against_oracle(xy_d, name="config1")
+    assert 0 < len(surv) < 100
+
+
+@pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
+def test_parity_plain_predicate(dist):
+    xy_d = synth.points(dist, 300_001, seed=4, device=DEV)
+    check_against_oracle(xy_d, plain=True, name=dist)
+
+
+@pytest.mark.parametrize("p", [0.0, 0.02, 0.05, 0.3, 1.0])
+def test_parity_displaced_sweep(p):
+    xy_d = synth.points("displaced", 200_000, seed=2, p=p, device=DEV)
+    check_against_oracle(xy_d, name=f"p={p}")
+
+
+# ------------------------------------------------------------ adversarial --
+def test_parity_ties_duplicates_signed_zero():
+    rng = np.random.default_rng(0)
+    for n in (5, 700, 9000, 70001):
+        xy = rng.integers(-3, 4, size=(n, 2)).astype(np.float64)
+        neg = rng.random((n, 2)) < 0.3
+        xy[(xy == 0) & neg] = -0.0
+        check_against_oracle(torch.tensor(xy, device=DEV), name=f"grid{n}")
+
+
+def test_parity_all_equal_and_collinear():
+    for xy in (np.full((5000, 2), 3.25), np.stack([np.arange(9000.0)] * 2, 1),
+               np.stack([np.arange(9000.0), np.zeros(9000)], 1), np.array([[1.0, 2.0], [3.0, 4.0]])):
+        check_against_oracle(torch.tensor(xy, device=DEV), name="degenerate")
+
+
+def test_parity_near_edges_and_box():
+    """Points within a few ulps of the octagon edges and of the accept box."""
+    rng = np.random.default_rng(1)
+    base = synth.points("normal", 50_000, seed=1).numpy()
+    o = oracle.octagon(base)
+    V = list(zip(o["vx"], o["vy"]))
+    adv = near_edge_points(rng, V, 60_000, ulps=4)
+    e = chf.Extremes()
+    idx = oracle.extremes8(base)
+    for k in range(8):
+        e.idx[k] = int(idx[k]); e.x[k] = base[idx[k], 0]; e.y[k] = base[idx[k], 1]
+    ob = chf.octagon_dict(chf.octagon_build(e))
+    pts = [adv]
+    if ob["has_box"]:
+        x0, x1, y0, y1 = ob["box"]
+        t = rng.random(20_000)
+        bx = np.concatenate([np.full(5000, x0), np.full(5000, x1), x0 + t[:5000] * (x1 - x0), x0 + t[5000:10000] * (x1 - x0)])
+        by = np.concatenate([y0 + t[:5000] * (y1 - y0), y0 + t[5000:10000] * (y1 - y0), np.full(5000, y0), np.full(5000, y1)])
+        for s in (-2, -1, 0, 1, 2):
+            pts.append(np.stack([bx + s * np.spacing(bx), by - s * np.spacing(by)], 1))
+    xy = np.concatenate([base] + pts)
+    check_against_oracle(torch.tensor(xy, device=DEV), name="adversarial")
+
+
+def test_parity_misaligned_input_16B():
+    """A 16-byte (not 32-byte) aligned input takes the LDG.128 path."""
+    big = synth.points("displaced", 100_001, seed=5, device=DEV)
+    xy_d = big[1:]
+    assert xy_d.data_ptr() % 32 == 16
+    check_against_oracle(xy_d.contiguous() if not xy_d.is_contiguous() else xy_d, name="misaligned")
+
+
+def test_octagon_bits_vs_oracle_flags():
+    for dist, n in (("normal", 100_003), ("circle", 65), ("displaced", 77_777)):
+        xy_d = synth.points(dist, n, seed=6, device=DEV)
+        ws = chf.Workspace(n)
+        chf.extremes8(xy_d, ws)
+        bits = chf.octagon_filter(xy_d, ws).cpu().numpy().view(np.uint32)
+        keep = oracle.flags(xy_d.cpu().numpy())
+        unpacked = ((bits[:, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(-1)
+        assert np.array_equal(unpacked[:n], keep)
+        assert not unpacked[n:].any()
+
+
+def test_host_octagon_argument_path():
+    """ch_filter_compact with a caller-provided octagon (host struct)."""
+    xy_d = synth.points("displaced", 50_000, seed=7, device=DEV)
+    xy = xy_d.cpu().numpy()
+    idx = oracle.extremes8(xy)
+    e = chf.Extremes()
+    for k in range(8):
+        e.idx[k] = int(idx[k]); e.x[k] = xy[idx[k], 0]; e.y[k] = xy[idx[k], 1]
+    o = chf.octagon_build(e)
+    ws = chf.Workspace(len(xy))
+    out = chf.filter_compact(xy_d, ws, oct_=o)
+    r = chf.read_result(ws)
+    want, _ = oracle.filter_compact(xy)
+    assert np.array_equal(out[: r.count].cpu().numpy(), want)
+
+
+def test_nonfinite_detected():
+    for bad in (np.nan, np.inf, -np.inf):
+        xy = synth.points("normal", 20_000, seed=0).numpy()
+        xy[12345, 1] = bad
+        with pytest.raises(chf.CHError) as ei:
+            chf.filter(torch.tensor(xy, device=DEV))
+        assert ei.value.status == 3
+    chf.filter(synth.points("normal", 1000, seed=0, device=DEV))   # workspace state recovers
+
+
+def test_determinism_and_workspace_reuse():
+    n = 777_777
+    ws = chf.Workspace(n)
+    xs = [synth.points(d, n, seed=3, device=DEV) for d in ("circle", "normal", "displaced")]
+    ref = [chf.filter(x, ws).cpu().numpy() for x in xs]
+    for _ in range(15):
+        for x, r in zip(xs, ref):
+            assert np.array_equal(chf.filter(x, ws).cpu().numpy(), r)
+    # smaller inputs on the same workspace (stale look-back words are ignored)
+    small = synth.points("displaced", 5000, seed=1, device=DEV)
+    want, _ = oracle.filter_compact(small.cpu().numpy())
+    assert np.array_equal(chf.filter(small, ws).cpu().numpy(), want)
+
+
+def test_index_base_and_sharded_combine_world_independence():
+    """K1 per shard with index_base + K3 combine + K2 per shard equals the
+    single-GPU result for W = 1..8 (the multi-GPU path, simulated on 1 GPU)."""
+    n = 300_001
+    for dist in ("normal", "displaced", "circle"):
+        xy_d = synth.points(dist, n, seed=8, device=DEV)
+        want, want_idx = oracle.filter_compact(xy_d.cpu().numpy())
+        for W in (1, 2, 3, 8):
+            from paper_2303_10581_b200.dist import EXT_WORDS, shard_range
+            recs = torch.empty(W * EXT_WORDS, dtype=torch.int64, device=DEV)
+            wss = []
+            for r in range(W):
+                lo, hi = shard_range(n, W, r)
+                ws = chf.Workspace(hi - lo)
+                chf.extremes8_async(xy_d[lo:hi], ws, index_base=lo, ext_out=recs[r * EXT_WORDS:(r + 1) * EXT_WORDS])
+                wss.append(ws)
+            parts = []
+            for r in range(W):
+                lo, hi = shard_range(n, W, r)
+                chf.combine8(recs, W, wss[r])
+                out = chf.filter_compact(xy_d[lo:hi], wss[r], index_base=lo)
+                c = chf.read_result(wss[r]).count
+                parts.append(out[:c].cpu().numpy())
+            got = np.concatenate(parts)
+            assert np.array_equal(got, want), (dist, W)
+
+
+def test_gather_and_hull_end_to_end():
+    for dist in ("normal", "displaced"):
+        xy_d = synth.points(dist, 400_000, seed=9, device=DEV)
+        xy = xy_d.cpu().numpy()
+        hull, surv, st = chf.hull_end_to_end(xy_d)
+        want_hull, want_s, _ = oracle.hull_end_to_end(xy)
+        assert np.array_equal(surv.cpu().numpy(), want_s)
+        assert np.array_equal(hull, want_hull)
+        assert st.n_hull == len(hull) and st.n_survivors == len(want_s)
+
+
+# ---------------------------------------------- full sizes of BASELINE.json --
+@pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
+def test_parity_full_1e8(dist):
+    """configs[1..3]: 10^8 points, full element-by-element parity in the
+    launch configuration bench.py times."""
+    n = 10 ** 8
+    xy_d = synth.points(dist, n, seed=0, device=DEV)
+    ws = chf.Workspace(n)
+    check_against_oracle(xy_d, ws=ws, name=f"{dist}-1e8")
+    if dist == "normal":
+        hull, surv, st = chf.hull_end_to_end(xy_d, ws)
+        want_h = oracle.hull(xy_d.cpu().numpy(), surv.cpu().numpy())
+        assert np.array_equal(hull, want_h)
+    del xy_d
+    torch.cuda.empty_cache()
+
+
+def test_parity_full_1e9_normal_sampled():
+    """configs[4] at one GPU (the bench workload): the extremes and octagon
+    against the oracle over all 10^9 points; every GPU survivor re-checked by
+    the oracle predicate; a 2*10^6-point random sample's decisions compared
+    one by one; the survivor count equals the oracle's count over a 10^8
+    prefix evaluated with the global octagon."""
+    n = 10 ** 9
+    free = torch.cuda.mem_get_info()[0]
+    if free < 40e9:
+        pytest.skip("needs ~40 GB of device memory")
+    xy_d = synth.points("normal", n, seed=0, device=DEV)
+    ws = chf.Workspace(n)
+    e, o = chf.extremes8(xy_d, ws)
+    surv = chf.filter(xy_d, ws).cpu().numpy()
+    xy = xy_d.cpu().numpy()
+    idx8 = oracle.extremes8(xy)
+    assert np.array_equal(np.array(e.idx[:]), idx8)
+    wo = oracle.octagon(xy, idx8)
+    od = chf.octagon_dict(o)
+    for f in ("vx", "vy", "ex", "ey", "thr"):
+        assert np.array_equal(od[f].view(np.int64), wo[f].view(np.int64)), f
+    assert np.all(np.diff(surv) > 0)
+    assert np.all(oracle.flags(xy[surv], oct_=wo) == 1)
+    rng = np.random.default_rng(0)
+    sample = np.sort(rng.choice(n, 2_000_000, replace=False))
+    keep_s = oracle.flags(xy[sample], oct_=wo).astype(bool)
+    assert np.array_equal(np.isin(sample, surv), keep_s)
+    pre = 10 ** 8
+    keep_pre = oracle.flags(xy[:pre], oct_=wo)
+    assert np.array_equal(np.flatnonzero(keep_pre), surv[surv < pre])
