@@ -36,14 +36,15 @@ constexpr int K1_UNROLL = 4;                                   // LDG.256 per th
 constexpr long long K1_CHUNK = (long long)K1_THREADS * K1_UNROLL * 2; // points per CTA iteration
 constexpr int K1_MAX_CTAS = 2048;
 
-constexpr int K2_THREADS = 256;
-constexpr int K2_WARPS = K2_THREADS / 32;
+constexpr int K2_CWARPS = 8;                                   // compute warps per CTA
+constexpr int K2_CTHREADS = K2_CWARPS * 32;
+constexpr int K2_THREADS = K2_CTHREADS + 32;                   // + 1 publisher warp
 constexpr int K2_UNROLL = 4;                                   // rows (LDG.256 per thread) per sub-tile
-constexpr long long K2_ROW = (long long)K2_THREADS * 2;        // 512 points per row
+constexpr long long K2_ROW = (long long)K2_CTHREADS * 2;       // 512 points per row
 constexpr long long K2_SUB = K2_ROW * K2_UNROLL;               // 2048 points per sub-tile
 constexpr int K2_MAXSUB = 32;                                  // sub-tiles per super-tile (max)
-constexpr int K2_ENTRIES = K2_MAXSUB * K2_UNROLL * K2_WARPS;   // (sub-tile, row, warp) groups
-static_assert(K2_ENTRIES == 4 * K2_THREADS, "block scan handles 4 entries per thread");
+constexpr int K2_ENTRIES = K2_MAXSUB * K2_UNROLL * K2_CWARPS;  // (sub-tile, row, warp) groups
+constexpr int K2_NP = 2 * K2_UNROLL;                           // points per thread per sub-tile
 
 constexpr int K4_THREADS = 256;
 
@@ -403,118 +404,220 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
     return false;
 }
 
+// Survivor mask for NP points of one thread (bit i = point i), bit-identical
+// to "not (forall k: D_k > T_k)" for every valid point (R4).  Stages, each
+// skipped when no lane of the warp needs it (warp-uniform branches):
+//  1. the certified accept box (4 DSETP): inside => discarded (proof at
+//     chf::box_valid);
+//  2. the guessed edge of the point's octant: D_g <= T_g => kept (this IS
+//     the oracle's exists-k condition, no proof needed).  Adaptive: a warp
+//     that needed stage 3 anyway skips stage 2 for the next 15 sub-tiles;
+//  3. every edge for every still-undecided point: nv x NP independent
+//     chains (ILP), edge parameters broadcast from shared memory.
+template <int NP>
+__device__ __forceinline__ unsigned classify(const SOct &s, const double (&px)[NP], const double (&py)[NP],
+                                             unsigned valid, int &guess_mode)
+{
+    unsigned und = 0;
+#pragma unroll
+    for (int i = 0; i < NP; i++) {
+        bool inbox = px[i] >= s.box[0] && px[i] <= s.box[1] && py[i] >= s.box[2] && py[i] <= s.box[3];
+        und |= (inbox ? 0u : 1u) << i;
+    }
+    und &= valid;
+    if (!__any_sync(FULL, und))
+        return 0u;
+    unsigned keep = 0;
+    if (guess_mode <= 0) {
+#pragma unroll
+        for (int i = 0; i < NP; i++) {
+            double dx = __dsub_rn(px[i], s.cx), dy = __dsub_rn(py[i], s.cy);
+            bool c = fabs(dx) >= fabs(dy);
+            int oct = dy >= 0.0 ? (dx >= 0.0 ? (c ? 0 : 1) : (c ? 3 : 2))
+                                : (dx < 0.0 ? (c ? 4 : 5) : (c ? 7 : 6));
+            const SEdge &e = s.e[s.guess[oct]];
+            double D = chf::edge_det(e.ax, e.ay, e.ex, e.ey, px[i], py[i]);
+            keep |= (D > e.thr ? 0u : 1u) << i;
+        }
+        keep &= und;
+        und &= ~keep;
+        if (!__any_sync(FULL, und))
+            return keep;
+        guess_mode = 16; // stage 3 was needed anyway: skip stage 2 for a while
+    }
+    guess_mode--;
+    unsigned disc = und;
+    const int nv = s.nv;
+    for (int k = 0; k < nv; k++) {
+        const double ax = s.e[k].ax, ay = s.e[k].ay, ex = s.e[k].ex, ey = s.e[k].ey, thr = s.e[k].thr;
+#pragma unroll
+        for (int i = 0; i < NP; i++) {
+            double D = chf::edge_det(ax, ay, ex, ey, px[i], py[i]);
+            disc &= ~((D > thr ? 0u : 1u) << i);
+        }
+    }
+    return keep | (und & ~disc);
+}
+
 // ===================================================================== K2 ==
-// Persistent CTAs (grid = resident capacity) claim "super-tiles" of
-// `subs` x K2_SUB consecutive points with one atomic each, in increasing
-// order, prefetching the next claim.  A super-tile is streamed as sub-tiles
-// of K2_SUB points: row u of sub-tile j holds points base_j + u*512 + 2t + h
-// for thread t (one LDG.256 per row); the octagon test's results are
-// ballot-ed per (sub-tile, row, warp) into shared memory (two words: h = 0
-// and h = 1 bits).  Then ONE decoupled look-back (Merrill & Garland) per
-// super-tile gives its global offset, a block scan of the popcounts gives
-// each 64-point group's offset, and the survivors' int64 indices are written
-// in index order ((j, u, warp, lane, h) lexicographic == increasing index).
+// Persistent CTAs (grid = resident capacity) of 8 compute warps + 1
+// publisher warp.  Compute warps claim "super-tiles" of `subs` x K2_SUB
+// consecutive points with one atomic each (in increasing order; the next
+// claim is prefetched) and stream them as sub-tiles: row u of sub-tile j
+// holds points base_j + u*512 + 2t + h for compute thread t (one LDG.256 per
+// row).  The octagon test's results are ballot-ed per (sub-tile, row, warp)
+// into one of two shared-memory buffers (words for h = 0 and h = 1).  The
+// publisher warp takes a full buffer, publishes the super-tile's count and
+// runs ONE decoupled look-back (Merrill & Garland) for it, then writes the
+// survivors' int64 indices in index order ((j, u, warp, lane, h)
+// lexicographic == increasing index) and hands the buffer back -- while the
+// compute warps already stream the next super-tile into the other buffer.
 // Claims are made in increasing order by running CTAs, so every predecessor
 // of a claimed super-tile is owned by a running CTA: the look-back always
-// makes progress.
+// makes progress.  Hand-offs use named barriers (bar.arrive / bar.sync).
+constexpr int BAR_FULL = 1;    // + buffer: compute warps arrive, publisher syncs
+constexpr int BAR_EMPTY = 3;   // + buffer: publisher arrives, compute warps sync
+constexpr int BAR_COMPUTE = 5; // compute warps only
+constexpr unsigned TILE_DONE = 0xffffffffu;
+
+__device__ __forceinline__ void bar_sync(int id, int nthreads)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int nthreads)
+{
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 template <bool A32>
-__global__ void __launch_bounds__(K2_THREADS, 4)
+__global__ void __launch_bounds__(K2_THREADS, 3)
 k2_filter_compact(const double *__restrict__ xy, long long n, long long index_base,
                   const ch_octagon *__restrict__ oct, WsHeader *hdr,
                   unsigned long long *status, long long *__restrict__ out,
                   long long *d_count, unsigned nsuper, int subs)
 {
     __shared__ SOct so;
-    __shared__ unsigned s_bits[K2_ENTRIES][2];
-    __shared__ int s_scan[K2_ENTRIES];
-    __shared__ int s_wcnt[K2_WARPS];
-    __shared__ int s_wsum[K2_WARPS];
-    __shared__ unsigned s_claim, s_epoch;
-    __shared__ long long s_excl;
-    __shared__ int s_total;
+    __shared__ unsigned s_bits[2][K2_ENTRIES][2];
+    __shared__ int s_wcnt[2][K2_CWARPS];
+    __shared__ unsigned s_tile[2];
+    __shared__ int s_nsub[2];
+    __shared__ unsigned s_next[2];
+    __shared__ unsigned s_epoch;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     if (tid == 0) {
         s_epoch = *(volatile unsigned *)&hdr->epoch;
         __threadfence();
-        s_claim = atomicAdd(&hdr->k2_claim, 1u);
+        s_next[1] = atomicAdd(&hdr->k2_claim, 1u);
     }
     load_soct(so, oct);
     __syncthreads();
-    const unsigned epoch = s_epoch & ST_EPOCH_MASK;
     const long long super_pts = (long long)subs * K2_SUB;
-    unsigned cur = s_claim;
 
-    while (cur < nsuper) {
-        unsigned nxt = 0;
-        if (tid == 0)
-            nxt = atomicAdd(&hdr->k2_claim, 1u); // prefetch the next claim
-        const long long sbase = (long long)cur * super_pts;
-        const int nsub = (int)min((long long)subs, (n - sbase + K2_SUB - 1) / K2_SUB);
-        int wcnt = 0;
-        for (int j = 0; j < nsub; j++) {
-            const long long base = sbase + (long long)j * K2_SUB;
-            unsigned keep = 0; // bit 2u + h
-            if (so.degenerate) {
+    if (warp < K2_CWARPS) {
+        // ------------------------------------------------ compute warps --
+        unsigned cur = s_next[1];
+        int b = 0, uses0 = 0, uses1 = 0;
+        int guess_mode = 0; // adaptive: see classify()
+        while (cur < nsuper) {
+            unsigned nxt = 0;
+            if (tid == 0)
+                nxt = atomicAdd(&hdr->k2_claim, 1u); // prefetch the next claim
+            if ((b ? uses1 : uses0) > 0)
+                bar_sync(BAR_EMPTY + b, K2_THREADS); // publisher released buffer b
+            const long long sbase = (long long)cur * super_pts;
+            const int nsub = (int)min((long long)subs, (n - sbase + K2_SUB - 1) / K2_SUB);
+            int wcnt = 0;
+            for (int j = 0; j < nsub; j++) {
+                const long long base = sbase + (long long)j * K2_SUB;
+                double px[K2_NP], py[K2_NP];
+                unsigned valid;
+                if (base + K2_SUB <= n) {
+                    double v[K2_UNROLL][4];
 #pragma unroll
-                for (int u = 0; u < K2_UNROLL; u++) {
-                    long long p = base + u * K2_ROW + 2 * tid;
-                    keep |= (p < n ? 1u : 0u) << (2 * u);
-                    keep |= (p + 1 < n ? 1u : 0u) << (2 * u + 1);
-                }
-            } else if (base + K2_SUB <= n) {
-                double v[K2_UNROLL][4];
+                    for (int u = 0; u < K2_UNROLL; u++)
+                        ld2pts<A32>(xy + 2 * (base + u * K2_ROW + 2 * tid), v[u][0], v[u][1], v[u][2], v[u][3]);
 #pragma unroll
-                for (int u = 0; u < K2_UNROLL; u++)
-                    ld2pts<A32>(xy + 2 * (base + u * K2_ROW + 2 * tid), v[u][0], v[u][1], v[u][2], v[u][3]);
+                    for (int u = 0; u < K2_UNROLL; u++) {
+                        px[2 * u] = v[u][0];
+                        py[2 * u] = v[u][1];
+                        px[2 * u + 1] = v[u][2];
+                        py[2 * u + 1] = v[u][3];
+                    }
+                    valid = (1u << K2_NP) - 1u;
+                } else {
+                    valid = 0;
 #pragma unroll
-                for (int u = 0; u < K2_UNROLL; u++) {
-                    keep |= (keep_point(so, v[u][0], v[u][1]) ? 1u : 0u) << (2 * u);
-                    keep |= (keep_point(so, v[u][2], v[u][3]) ? 1u : 0u) << (2 * u + 1);
-                }
-            } else {
-                for (int u = 0; u < K2_UNROLL; u++) {
-                    long long p = base + u * K2_ROW + 2 * tid;
-                    for (int h = 0; h < 2; h++) {
-                        if (p + h < n) {
-                            double x, y;
-                            ld128(xy + 2 * (p + h), x, y);
-                            keep |= (keep_point(so, x, y) ? 1u : 0u) << (2 * u + h);
+                    for (int u = 0; u < K2_UNROLL; u++) {
+                        long long p = base + u * K2_ROW + 2 * tid;
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            px[2 * u + h] = 0.0;
+                            py[2 * u + h] = 0.0;
+                            if (p + h < n) {
+                                ld128(xy + 2 * (p + h), px[2 * u + h], py[2 * u + h]);
+                                valid |= 1u << (2 * u + h);
+                            }
                         }
                     }
                 }
-            }
+                const unsigned keep = so.degenerate ? valid : classify<K2_NP>(so, px, py, valid, guess_mode);
 #pragma unroll
-            for (int u = 0; u < K2_UNROLL; u++) {
-                unsigned b0 = __ballot_sync(FULL, (keep >> (2 * u)) & 1u);
-                unsigned b1 = __ballot_sync(FULL, (keep >> (2 * u + 1)) & 1u);
-                if (lane == 0) {
-                    int e = (j * K2_UNROLL + u) * K2_WARPS + warp;
-                    s_bits[e][0] = b0;
-                    s_bits[e][1] = b1;
+                for (int u = 0; u < K2_UNROLL; u++) {
+                    unsigned b0 = __ballot_sync(FULL, (keep >> (2 * u)) & 1u);
+                    unsigned b1 = __ballot_sync(FULL, (keep >> (2 * u + 1)) & 1u);
+                    if (lane == 0) {
+                        int e = (j * K2_UNROLL + u) * K2_CWARPS + warp;
+                        s_bits[b][e][0] = b0;
+                        s_bits[b][e][1] = b1;
+                    }
+                    wcnt += __popc(b0) + __popc(b1);
                 }
-                wcnt += __popc(b0) + __popc(b1);
             }
+            if (lane == 0)
+                s_wcnt[b][warp] = wcnt;
+            if (tid == 0) {
+                s_tile[b] = cur;
+                s_nsub[b] = nsub;
+                s_next[b] = nxt;
+            }
+            bar_arrive(BAR_FULL + b, K2_THREADS); // hand buffer b to the publisher
+            if (b) uses1++; else uses0++;
+            bar_sync(BAR_COMPUTE, K2_CTHREADS);
+            cur = s_next[b];
+            b ^= 1;
         }
-        if (lane == 0)
-            s_wcnt[warp] = wcnt;
-        __syncthreads();
-        if (warp == 0) {
-            int total = lane < K2_WARPS ? s_wcnt[lane] : 0;
+        if ((b ? uses1 : uses0) > 0)
+            bar_sync(BAR_EMPTY + b, K2_THREADS);
+        if (tid == 0)
+            s_tile[b] = TILE_DONE;
+        bar_arrive(BAR_FULL + b, K2_THREADS);
+    } else {
+        // ------------------------------------------------ publisher warp --
+        const unsigned epoch = s_epoch & ST_EPOCH_MASK;
+        const unsigned lt = lanemask_lt();
+        int b = 0;
+        while (true) {
+            bar_sync(BAR_FULL + b, K2_THREADS);
+            const unsigned tile = s_tile[b];
+            if (tile == TILE_DONE)
+                break;
+            const int nsub = s_nsub[b];
+            int total = lane < K2_CWARPS ? s_wcnt[b][lane] : 0;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1)
                 total += __shfl_xor_sync(FULL, total, off);
             // ---- decoupled look-back over super-tiles ----
             long long excl = 0;
-            if (cur == 0) {
+            if (tile == 0) {
                 if (lane == 0)
                     st_release(&status[0], (ST_P << 62) | ((unsigned long long)epoch << 40) |
                                                ((unsigned long long)total & ST_VALUE_MASK));
             } else {
                 if (lane == 0)
-                    st_release(&status[cur], (ST_A << 62) | ((unsigned long long)epoch << 40) |
-                                                 ((unsigned long long)total & ST_VALUE_MASK));
-                long long pos = (long long)cur - 1;
+                    st_release(&status[tile], (ST_A << 62) | ((unsigned long long)epoch << 40) |
+                                                  ((unsigned long long)total & ST_VALUE_MASK));
+                long long pos = (long long)tile - 1;
                 while (true) {
                     long long j = pos - lane;
                     unsigned long long flag = ST_P, val = 0;
@@ -531,6 +634,7 @@ k2_filter_compact(const double *__restrict__ xy, long long n, long long index_ba
                         need = pm ? (((pm & (0u - pm)) << 1) - 1u) : FULL; // lanes up to the first P
                         if ((xm & need) == 0)
                             break;
+                        __nanosleep(64);
                     }
                     unsigned long long c = ((need >> lane) & 1u) ? val : 0ull;
 #pragma unroll
@@ -542,75 +646,40 @@ k2_filter_compact(const double *__restrict__ xy, long long n, long long index_ba
                     pos -= 32;
                 }
                 if (lane == 0)
-                    st_release(&status[cur], (ST_P << 62) | ((unsigned long long)epoch << 40) |
-                                                 ((unsigned long long)(excl + total) & ST_VALUE_MASK));
+                    st_release(&status[tile], (ST_P << 62) | ((unsigned long long)epoch << 40) |
+                                                  ((unsigned long long)(excl + total) & ST_VALUE_MASK));
             }
-            if (lane == 0) {
-                s_excl = excl;
-                s_total = total;
-                if (cur == nsuper - 1) {
-                    hdr->result.count = excl + total;
-                    if (d_count)
-                        *d_count = excl + total;
-                }
+            if (tile == nsuper - 1 && lane == 0) {
+                hdr->result.count = excl + total;
+                if (d_count)
+                    *d_count = excl + total;
             }
-        }
-        __syncthreads();
-        if (s_total > 0) {
-            // block exclusive scan of the (sub-tile, row, warp) popcounts, 4 per thread
-            const int E = nsub * K2_UNROLL * K2_WARPS;
-            int c[4], sum = 0;
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                int e = 4 * tid + q;
-                c[q] = e < E ? __popc(s_bits[e][0]) + __popc(s_bits[e][1]) : 0;
-                sum += c[q];
-            }
-            int inc = sum;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                int t = __shfl_up_sync(FULL, inc, off);
-                if (lane >= off)
-                    inc += t;
-            }
-            if (lane == 31)
-                s_wsum[warp] = inc;
-            __syncthreads();
-            int ex = inc - sum;
-            for (int w = 0; w < warp; w++)
-                ex += s_wsum[w];
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                int e = 4 * tid + q;
-                if (e < E)
-                    s_scan[e] = ex;
-                ex += c[q];
-            }
-            __syncthreads();
-            const long long excl = s_excl;
-            const unsigned lt = lanemask_lt();
-            for (int j = 0; j < nsub; j++) {
-#pragma unroll
-                for (int u = 0; u < K2_UNROLL; u++) {
-                    int e = (j * K2_UNROLL + u) * K2_WARPS + warp;
-                    unsigned b0 = s_bits[e][0], b1 = s_bits[e][1];
-                    if ((b0 | b1) == 0)
+            // ---- survivors of this super-tile, in index order ----
+            if (total > 0) {
+                const long long sbase = (long long)tile * super_pts;
+                const int E = nsub * K2_UNROLL * K2_CWARPS;
+                long long run = excl;
+                for (int e = 0; e < E; e++) {
+                    const unsigned b0 = s_bits[b][e][0], b1 = s_bits[b][e][1];
+                    const int c = __popc(b0) + __popc(b1);
+                    if (c == 0)
                         continue;
-                    unsigned k0 = (b0 >> lane) & 1u, k1 = (b1 >> lane) & 1u;
-                    long long pos = excl + s_scan[e] + __popc(b0 & lt) + __popc(b1 & lt);
-                    long long gi = index_base + sbase + (long long)j * K2_SUB + u * K2_ROW + 2 * tid;
+                    const int w = e % K2_CWARPS, u = (e / K2_CWARPS) % K2_UNROLL, jj = e / (K2_CWARPS * K2_UNROLL);
+                    const unsigned k0 = (b0 >> lane) & 1u, k1 = (b1 >> lane) & 1u;
+                    const long long pos = run + __popc(b0 & lt) + __popc(b1 & lt);
+                    const long long gi = index_base + sbase + (long long)jj * K2_SUB + u * K2_ROW + 64 * w + 2 * lane;
                     if (k0)
                         out[pos] = gi;
                     if (k1)
                         out[pos + k0] = gi + 1;
+                    run += c;
                 }
             }
+            bar_arrive(BAR_EMPTY + b, K2_THREADS);
+            b ^= 1;
         }
-        if (tid == 0)
-            s_claim = nxt;
-        __syncthreads();
-        cur = s_claim;
     }
+    __syncthreads();
     // exit protocol: the last CTA to leave resets the counters, bumps the epoch
     if (tid == 0) {
         __threadfence();

@@ -1,0 +1,14 @@
+# parity tests + bench over the workload matrix (1 GPU); outputs in gpurun_out/
+set -x
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
+B="python bench.py --no-e2e --no-cpu-baseline"
+for N in 1e9 1e8; do for D in normal circle displaced; do
+  timeout 300 $B --dist $D --n $N --steps ${STEPS:-30} --warmup 3 > gpurun_out/bench_${D}_${N}.json 2>gpurun_out/bench_${D}_${N}.err; echo "bench $D $N rc=$?"
+done; done
+python - <<'PY'
+import json,glob
+for f in sorted(glob.glob("gpurun_out/bench_*.json")):
+    try: d=json.loads(open(f).read().strip().splitlines()[-1])
+    except Exception as e: print(f, "ERR", e); continue
+    r=d["roofline"]; print(f"{d['config']['workload']:28s} {d['value']:8.2f} Gpts/s  step {d['ms_per_step']:.3f} ms  k1 {r['k1_ms']:.3f} ({r['k1_gbs']:.0f} GB/s)  k2 {r['k2_ms']:.3f} ({r['k2_gbs']:.0f} GB/s)  hbm {d['hbm_frac']:.3f}  clk {d['clocks']['sm_mhz']} {d['clocks']['reasons']}")
+PY
