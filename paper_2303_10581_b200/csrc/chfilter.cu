@@ -36,15 +36,20 @@ constexpr int K1_UNROLL = 4;                                   // LDG.256 per th
 constexpr long long K1_CHUNK = (long long)K1_THREADS * K1_UNROLL * 2; // points per CTA iteration
 constexpr int K1_MAX_CTAS = 2048;
 
-constexpr int K2_CWARPS = 8;                                   // compute warps per CTA
+constexpr int K2_CWARPS = 8;                                   // consumer (compute) warps per CTA
 constexpr int K2_CTHREADS = K2_CWARPS * 32;
-constexpr int K2_THREADS = K2_CTHREADS + 32;                   // + 1 publisher warp
-constexpr int K2_UNROLL = 4;                                   // rows (LDG.256 per thread) per sub-tile
-constexpr long long K2_ROW = (long long)K2_CTHREADS * 2;       // 512 points per row
-constexpr long long K2_SUB = K2_ROW * K2_UNROLL;               // 2048 points per sub-tile
+constexpr int K2_PUB_WARP = K2_CWARPS;                         // publisher warp
+constexpr int K2_PROD_WARP = K2_CWARPS + 1;                    // TMA producer warp
+constexpr int K2_THREADS = K2_CTHREADS + 64;
+constexpr int K2_NP = 4;                                       // points per consumer thread per sub-tile
+constexpr long long K2_SUB = (long long)K2_CTHREADS * K2_NP;   // 1024 points (16 KB) per sub-tile
+constexpr int K2_STAGES = 6;                                   // TMA ring depth (sub-tiles)
 constexpr int K2_MAXSUB = 32;                                  // sub-tiles per super-tile (max)
-constexpr int K2_ENTRIES = K2_MAXSUB * K2_UNROLL * K2_CWARPS;  // (sub-tile, row, warp) groups
-constexpr int K2_NP = 2 * K2_UNROLL;                           // points per thread per sub-tile
+constexpr int K2_GROUPS = K2_NP * K2_CWARPS;                   // 32-point groups per sub-tile
+constexpr int K2_ENTRIES = K2_MAXSUB * K2_GROUPS;              // ballot words per super-tile
+static_assert(K2_ENTRIES == 4 * K2_CTHREADS, "block scan: 4 entries per consumer thread");
+constexpr size_t K2_DSMEM = (size_t)K2_STAGES * K2_SUB * 16 + 4 * K2_ENTRIES * 4; // stages + bits[2] + scan[2]
+constexpr int K2_BAR_BASE = 1;                                 // named barrier ids 1..5
 
 constexpr int K4_THREADS = 256;
 
@@ -114,6 +119,45 @@ __device__ __forceinline__ unsigned lanemask_lt()
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
+}
+
+// ------------------------------------------------- TMA bulk copy + mbarrier --
+__device__ __forceinline__ unsigned smem_u32(const void *p)
+{
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity)
+{
+    unsigned ok = 0;
+    while (true) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok)
+                     : "r"(smem_u32(bar)), "r"(parity)
+                     : "memory");
+        if (ok)
+            break;
+    }
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes, unsigned long long *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 // ===================================================================== K1 ==
@@ -460,24 +504,25 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const double (&px)[N
 }
 
 // ===================================================================== K2 ==
-// Persistent CTAs (grid = resident capacity) of 8 compute warps + 1
-// publisher warp.  Compute warps claim "super-tiles" of `subs` x K2_SUB
-// consecutive points with one atomic each (in increasing order; the next
-// claim is prefetched) and stream them as sub-tiles: row u of sub-tile j
-// holds points base_j + u*512 + 2t + h for compute thread t (one LDG.256 per
-// row).  The octagon test's results are ballot-ed per (sub-tile, row, warp)
-// into one of two shared-memory buffers (words for h = 0 and h = 1).  The
+// Persistent, warp-specialized CTAs: 8 consumer warps, 1 publisher warp and
+// 1 TMA producer warp.  The producer claims "super-tiles" of `subs` x K2_SUB
+// consecutive points with one atomic each (in increasing order, one claim
+// ahead) and streams them as 16 KB sub-tiles through a K2_STAGES-deep ring
+// in shared memory (cp.async.bulk + full/empty mbarriers), so loads stay in
+// flight while the consumers compute.  Consumer thread t tests points
+// base_j + u*256 + t (u < K2_NP) of sub-tile j; the results are
+// ballot-ed per (sub-tile, u, warp) -- 32 consecutive points -- into one of
+// two shared-memory buffers.  The
 // publisher warp takes a full buffer, publishes the super-tile's count and
 // runs ONE decoupled look-back (Merrill & Garland) for it, then writes the
-// survivors' int64 indices in index order ((j, u, warp, lane, h)
+// survivors' int64 indices in index order ((j, u, warp, lane)
 // lexicographic == increasing index) and hands the buffer back -- while the
 // compute warps already stream the next super-tile into the other buffer.
 // Claims are made in increasing order by running CTAs, so every predecessor
 // of a claimed super-tile is owned by a running CTA: the look-back always
 // makes progress.  Hand-offs use named barriers (bar.arrive / bar.sync).
-constexpr int BAR_FULL = 1;    // + buffer: compute warps arrive, publisher syncs
-constexpr int BAR_EMPTY = 3;   // + buffer: publisher arrives, compute warps sync
-constexpr int BAR_COMPUTE = 5; // compute warps only
+// named barriers K2_BAR_BASE + b: consumers arrive, publisher syncs (buffer b full);
+// K2_BAR_BASE + 2 + b: publisher arrives, consumers sync (buffer b empty).
 constexpr unsigned TILE_DONE = 0xffffffffu;
 
 __device__ __forceinline__ void bar_sync(int id, int nthreads)
@@ -489,134 +534,212 @@ __device__ __forceinline__ void bar_arrive(int id, int nthreads)
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <bool A32>
-__global__ void __launch_bounds__(K2_THREADS, 3)
+__global__ void __launch_bounds__(K2_THREADS, 2)
 k2_filter_compact(const double *__restrict__ xy, long long n, long long index_base,
                   const ch_octagon *__restrict__ oct, WsHeader *hdr,
                   unsigned long long *status, long long *__restrict__ out,
                   long long *d_count, unsigned nsuper, int subs)
 {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    double2 *stage = (double2 *)dsm;                                        // [K2_STAGES][K2_SUB]
+    unsigned *bits = (unsigned *)(dsm + (size_t)K2_STAGES * K2_SUB * 16);  // [2][K2_ENTRIES]
+    int *gscan = (int *)(bits + 2 * K2_ENTRIES);                            // [2][K2_ENTRIES]
     __shared__ SOct so;
-    __shared__ unsigned s_bits[2][K2_ENTRIES][2];
-    __shared__ int s_wcnt[2][K2_CWARPS];
+    __shared__ __align__(8) unsigned long long s_full[K2_STAGES], s_empty[K2_STAGES];
+    __shared__ unsigned s_desc_super[K2_STAGES];
+    __shared__ int s_desc_j[K2_STAGES], s_desc_nsub[K2_STAGES];
+    __shared__ int s_wsum[K2_CWARPS];
+    __shared__ int s_total[2];
     __shared__ unsigned s_tile[2];
     __shared__ int s_nsub[2];
-    __shared__ unsigned s_next[2];
+    __shared__ long long s_excl[2];
     __shared__ unsigned s_epoch;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long super_pts = (long long)subs * K2_SUB;
+    const unsigned lt = lanemask_lt();
 
     if (tid == 0) {
         s_epoch = *(volatile unsigned *)&hdr->epoch;
-        __threadfence();
-        s_next[1] = atomicAdd(&hdr->k2_claim, 1u);
+        for (int st = 0; st < K2_STAGES; st++) {
+            mbar_init(&s_full[st], 1);
+            mbar_init(&s_empty[st], K2_CWARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     load_soct(so, oct);
     __syncthreads();
-    const long long super_pts = (long long)subs * K2_SUB;
+    const unsigned epoch = s_epoch & ST_EPOCH_MASK;
 
-    if (warp < K2_CWARPS) {
-        // ------------------------------------------------ compute warps --
-        unsigned cur = s_next[1];
+    if (warp == K2_PROD_WARP) {
+        // ------------------------------------------------ TMA producer --
+        // Streams this CTA's claimed super-tiles, sub-tile by sub-tile, into
+        // the ring.  Claims are made one super-tile ahead, in increasing order.
+        if (lane == 0) {
+            __threadfence();
+            unsigned p_super = atomicAdd(&hdr->k2_claim, 1u);
+            unsigned p_next = p_super < nsuper ? atomicAdd(&hdr->k2_claim, 1u) : TILE_DONE;
+            int p_j = 0;
+            int p_nsub = 0;
+            if (p_super < nsuper)
+                p_nsub = (int)min((long long)subs, (n - (long long)p_super * super_pts + K2_SUB - 1) / K2_SUB);
+            for (unsigned seq = 0;; seq++) {
+                const int st = (int)(seq % K2_STAGES);
+                if (seq >= K2_STAGES)
+                    mbar_wait(&s_empty[st], ((seq / K2_STAGES) - 1) & 1u); // consumers released it
+                if (p_super >= nsuper) {
+                    s_desc_super[st] = TILE_DONE;
+                    mbar_arrive(&s_full[st]);
+                    break;
+                }
+                const long long base = (long long)p_super * super_pts + (long long)p_j * K2_SUB;
+                const unsigned cnt = (unsigned)min(K2_SUB, n - base);
+                s_desc_super[st] = p_super;
+                s_desc_j[st] = p_j;
+                s_desc_nsub[st] = p_nsub;
+                mbar_expect_tx(&s_full[st], cnt * 16u);
+                tma_load_1d(stage + (size_t)st * K2_SUB, xy + 2 * base, cnt * 16u, &s_full[st]);
+                if (++p_j == p_nsub) {
+                    p_super = p_next;
+                    p_next = p_super < nsuper ? atomicAdd(&hdr->k2_claim, 1u) : TILE_DONE;
+                    p_j = 0;
+                    p_nsub = 0;
+                    if (p_super < nsuper)
+                        p_nsub = (int)min((long long)subs,
+                                          (n - (long long)p_super * super_pts + K2_SUB - 1) / K2_SUB);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp < K2_CWARPS) {
+        // ------------------------------------------------ consumer warps --
+        // Survivors of the super-tile held in buffer bb, written by every
+        // consumer warp for its own 32-point groups, once the publisher has
+        // resolved the super-tile's global offset.
+        auto write_survivors = [&](int bb) {
+            bar_sync(K2_BAR_BASE + 2 + bb, K2_CTHREADS + 32); // offset of buffer bb is known
+            if (s_total[bb] > 0) {
+                const long long sbase = (long long)s_tile[bb] * super_pts + index_base;
+                const long long excl = s_excl[bb];
+                const unsigned *bw = bits + bb * K2_ENTRIES;
+                const int *sc = gscan + bb * K2_ENTRIES;
+                const int E = s_nsub[bb] * K2_GROUPS;
+                for (int e = warp; e < E; e += K2_CWARPS) {
+                    const unsigned m = bw[e];
+                    if (m == 0u)
+                        continue;
+                    const int u = (e / K2_CWARPS) % K2_NP, jj = e / K2_GROUPS;
+                    if ((m >> lane) & 1u)
+                        out[excl + sc[e] + __popc(m & lt)] =
+                            sbase + (long long)jj * K2_SUB + u * K2_CTHREADS + 32 * warp + lane;
+                }
+            }
+        };
         int b = 0, uses0 = 0, uses1 = 0;
         int guess_mode = 0; // adaptive: see classify()
-        while (cur < nsuper) {
-            unsigned nxt = 0;
-            if (tid == 0)
-                nxt = atomicAdd(&hdr->k2_claim, 1u); // prefetch the next claim
-            if ((b ? uses1 : uses0) > 0)
-                bar_sync(BAR_EMPTY + b, K2_THREADS); // publisher released buffer b
-            const long long sbase = (long long)cur * super_pts;
-            const int nsub = (int)min((long long)subs, (n - sbase + K2_SUB - 1) / K2_SUB);
-            int wcnt = 0;
-            for (int j = 0; j < nsub; j++) {
-                const long long base = sbase + (long long)j * K2_SUB;
-                double px[K2_NP], py[K2_NP];
-                unsigned valid;
-                if (base + K2_SUB <= n) {
-                    double v[K2_UNROLL][4];
-#pragma unroll
-                    for (int u = 0; u < K2_UNROLL; u++)
-                        ld2pts<A32>(xy + 2 * (base + u * K2_ROW + 2 * tid), v[u][0], v[u][1], v[u][2], v[u][3]);
-#pragma unroll
-                    for (int u = 0; u < K2_UNROLL; u++) {
-                        px[2 * u] = v[u][0];
-                        py[2 * u] = v[u][1];
-                        px[2 * u + 1] = v[u][2];
-                        py[2 * u + 1] = v[u][3];
-                    }
-                    valid = (1u << K2_NP) - 1u;
-                } else {
-                    valid = 0;
-#pragma unroll
-                    for (int u = 0; u < K2_UNROLL; u++) {
-                        long long p = base + u * K2_ROW + 2 * tid;
-#pragma unroll
-                        for (int h = 0; h < 2; h++) {
-                            px[2 * u + h] = 0.0;
-                            py[2 * u + h] = 0.0;
-                            if (p + h < n) {
-                                ld128(xy + 2 * (p + h), px[2 * u + h], py[2 * u + h]);
-                                valid |= 1u << (2 * u + h);
-                            }
-                        }
-                    }
-                }
-                const unsigned keep = so.degenerate ? valid : classify<K2_NP>(so, px, py, valid, guess_mode);
-#pragma unroll
-                for (int u = 0; u < K2_UNROLL; u++) {
-                    unsigned b0 = __ballot_sync(FULL, (keep >> (2 * u)) & 1u);
-                    unsigned b1 = __ballot_sync(FULL, (keep >> (2 * u + 1)) & 1u);
-                    if (lane == 0) {
-                        int e = (j * K2_UNROLL + u) * K2_CWARPS + warp;
-                        s_bits[b][e][0] = b0;
-                        s_bits[b][e][1] = b1;
-                    }
-                    wcnt += __popc(b0) + __popc(b1);
-                }
+        for (unsigned seq = 0;; seq++) {
+            const int st = (int)(seq % K2_STAGES);
+            mbar_wait(&s_full[st], (seq / K2_STAGES) & 1u);
+            const unsigned sup = s_desc_super[st];
+            if (sup == TILE_DONE)
+                break;
+            const int j = s_desc_j[st], nsub = s_desc_nsub[st];
+            if (j == 0 && (b ? uses1 : uses0) > 0) {
+                write_survivors(b);                    // super-tile handed off two rounds ago
+                bar_sync(K2_BAR_BASE + 4, K2_CTHREADS); // all warps done with buffer b
             }
+            const long long base = (long long)sup * super_pts + (long long)j * K2_SUB;
+            const double2 *sp = stage + (size_t)st * K2_SUB;
+            double px[K2_NP], py[K2_NP];
+            unsigned valid = 0;
+#pragma unroll
+            for (int u = 0; u < K2_NP; u++) {
+                double2 v = sp[u * K2_CTHREADS + tid];
+                px[u] = v.x;
+                py[u] = v.y;
+                valid |= (base + u * K2_CTHREADS + tid < n ? 1u : 0u) << u;
+            }
+            __syncwarp();
             if (lane == 0)
-                s_wcnt[b][warp] = wcnt;
-            if (tid == 0) {
-                s_tile[b] = cur;
-                s_nsub[b] = nsub;
-                s_next[b] = nxt;
+                mbar_arrive(&s_empty[st]); // this warp is done with stage st
+            const unsigned keep = so.degenerate ? valid : classify<K2_NP>(so, px, py, valid, guess_mode);
+            unsigned *bw = bits + b * K2_ENTRIES + j * K2_GROUPS;
+#pragma unroll
+            for (int u = 0; u < K2_NP; u++) {
+                unsigned m = __ballot_sync(FULL, (keep >> u) & 1u);
+                if (lane == 0)
+                    bw[u * K2_CWARPS + warp] = m;
             }
-            bar_arrive(BAR_FULL + b, K2_THREADS); // hand buffer b to the publisher
-            if (b) uses1++; else uses0++;
-            bar_sync(BAR_COMPUTE, K2_CTHREADS);
-            cur = s_next[b];
-            b ^= 1;
+            if (j == nsub - 1) {
+                // ---- end of super-tile: group prefix (block scan) + aggregate ----
+                bar_sync(K2_BAR_BASE + 4, K2_CTHREADS);
+                const int E = nsub * K2_GROUPS;
+                const unsigned *bb = bits + b * K2_ENTRIES;
+                int c[4], sum = 0;
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const int e = 4 * tid + q;
+                    c[q] = e < E ? __popc(bb[e]) : 0;
+                    sum += c[q];
+                }
+                int inc = sum;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    int t = __shfl_up_sync(FULL, inc, off);
+                    if (lane >= off)
+                        inc += t;
+                }
+                if (lane == 31)
+                    s_wsum[warp] = inc;
+                bar_sync(K2_BAR_BASE + 4, K2_CTHREADS);
+                int ex = inc - sum, total = 0;
+#pragma unroll
+                for (int w = 0; w < K2_CWARPS; w++) {
+                    const int v = s_wsum[w];
+                    ex += w < warp ? v : 0;
+                    total += v;
+                }
+                int *sc = gscan + b * K2_ENTRIES;
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    sc[4 * tid + q] = ex;
+                    ex += c[q];
+                }
+                if (tid == 0) {
+                    // Publish the aggregate right away (flag A; P for super-tile 0)
+                    // so successors' look-backs never wait on this CTA's publisher.
+                    st_release(&status[sup], ((sup == 0 ? ST_P : ST_A) << 62) | ((unsigned long long)epoch << 40) |
+                                                 ((unsigned long long)total & ST_VALUE_MASK));
+                    s_total[b] = total;
+                    s_tile[b] = sup;
+                    s_nsub[b] = nsub;
+                }
+                bar_arrive(K2_BAR_BASE + b, K2_CTHREADS + 32); // hand buffer b to the publisher
+                if (b) uses1++; else uses0++;
+                b ^= 1;
+            }
         }
+        // flush: the older pending buffer first
         if ((b ? uses1 : uses0) > 0)
-            bar_sync(BAR_EMPTY + b, K2_THREADS);
+            write_survivors(b);
+        if ((b ? uses0 : uses1) > 0)
+            write_survivors(b ^ 1);
+        bar_sync(K2_BAR_BASE + 4, K2_CTHREADS);
         if (tid == 0)
             s_tile[b] = TILE_DONE;
-        bar_arrive(BAR_FULL + b, K2_THREADS);
+        bar_arrive(K2_BAR_BASE + b, K2_CTHREADS + 32);
     } else {
         // ------------------------------------------------ publisher warp --
-        const unsigned epoch = s_epoch & ST_EPOCH_MASK;
-        const unsigned lt = lanemask_lt();
+        // Decoupled look-back (Merrill & Garland) for each handed-off
+        // super-tile: its global offset, then the inclusive prefix (flag P).
         int b = 0;
         while (true) {
-            bar_sync(BAR_FULL + b, K2_THREADS);
+            bar_sync(K2_BAR_BASE + b, K2_CTHREADS + 32);
             const unsigned tile = s_tile[b];
             if (tile == TILE_DONE)
                 break;
-            const int nsub = s_nsub[b];
-            int total = lane < K2_CWARPS ? s_wcnt[b][lane] : 0;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1)
-                total += __shfl_xor_sync(FULL, total, off);
-            // ---- decoupled look-back over super-tiles ----
+            const int total = s_total[b];
             long long excl = 0;
-            if (tile == 0) {
-                if (lane == 0)
-                    st_release(&status[0], (ST_P << 62) | ((unsigned long long)epoch << 40) |
-                                               ((unsigned long long)total & ST_VALUE_MASK));
-            } else {
-                if (lane == 0)
-                    st_release(&status[tile], (ST_A << 62) | ((unsigned long long)epoch << 40) |
-                                                  ((unsigned long long)total & ST_VALUE_MASK));
+            if (tile != 0) {
                 long long pos = (long long)tile - 1;
                 while (true) {
                     long long j = pos - lane;
@@ -624,10 +747,10 @@ k2_filter_compact(const double *__restrict__ xy, long long n, long long index_ba
                     unsigned pm, xm, need;
                     while (true) {
                         if (j >= 0) {
-                            unsigned long long st = ld_acquire(&status[j]);
-                            bool ok = (unsigned)((st >> 40) & ST_EPOCH_MASK) == epoch && (st >> 62) != 0;
-                            flag = ok ? (st >> 62) : 0;
-                            val = st & ST_VALUE_MASK;
+                            unsigned long long stw = ld_acquire(&status[j]);
+                            bool ok = (unsigned)((stw >> 40) & ST_EPOCH_MASK) == epoch && (stw >> 62) != 0;
+                            flag = ok ? (stw >> 62) : 0;
+                            val = stw & ST_VALUE_MASK;
                         }
                         pm = __ballot_sync(FULL, flag == ST_P);
                         xm = __ballot_sync(FULL, flag == 0);
@@ -649,33 +772,15 @@ k2_filter_compact(const double *__restrict__ xy, long long n, long long index_ba
                     st_release(&status[tile], (ST_P << 62) | ((unsigned long long)epoch << 40) |
                                                   ((unsigned long long)(excl + total) & ST_VALUE_MASK));
             }
-            if (tile == nsuper - 1 && lane == 0) {
-                hdr->result.count = excl + total;
-                if (d_count)
-                    *d_count = excl + total;
-            }
-            // ---- survivors of this super-tile, in index order ----
-            if (total > 0) {
-                const long long sbase = (long long)tile * super_pts;
-                const int E = nsub * K2_UNROLL * K2_CWARPS;
-                long long run = excl;
-                for (int e = 0; e < E; e++) {
-                    const unsigned b0 = s_bits[b][e][0], b1 = s_bits[b][e][1];
-                    const int c = __popc(b0) + __popc(b1);
-                    if (c == 0)
-                        continue;
-                    const int w = e % K2_CWARPS, u = (e / K2_CWARPS) % K2_UNROLL, jj = e / (K2_CWARPS * K2_UNROLL);
-                    const unsigned k0 = (b0 >> lane) & 1u, k1 = (b1 >> lane) & 1u;
-                    const long long pos = run + __popc(b0 & lt) + __popc(b1 & lt);
-                    const long long gi = index_base + sbase + (long long)jj * K2_SUB + u * K2_ROW + 64 * w + 2 * lane;
-                    if (k0)
-                        out[pos] = gi;
-                    if (k1)
-                        out[pos + k0] = gi + 1;
-                    run += c;
+            if (lane == 0) {
+                s_excl[b] = excl;
+                if (tile == nsuper - 1) {
+                    hdr->result.count = excl + total;
+                    if (d_count)
+                        *d_count = excl + total;
                 }
             }
-            bar_arrive(BAR_EMPTY + b, K2_THREADS);
+            bar_arrive(K2_BAR_BASE + 2 + b, K2_CTHREADS + 32);
             b ^= 1;
         }
     }
@@ -768,10 +873,9 @@ DevInfo dev_info()
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k1_per_sm, k1_extremes8<true>, K1_THREADS, 0);
         if (info.k1_per_sm < 1)
             info.k1_per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k2_per_sm, k2_filter_compact<true>, K2_THREADS, 0);
-        int k2b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k2b, k2_filter_compact<false>, K2_THREADS, 0);
-        info.k2_per_sm = std::max(1, std::min(info.k2_per_sm, k2b));
+        cudaFuncSetAttribute(k2_filter_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_DSMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k2_per_sm, k2_filter_compact, K2_THREADS, K2_DSMEM);
+        info.k2_per_sm = std::max(1, info.k2_per_sm);
         cached_dev = dev;
     }
     return info;
@@ -853,12 +957,8 @@ ch_status launch_k2(const double *d_xy, long long n, long long index_base, const
     subs = std::max<long long>(1, std::min<long long>(subs, K2_MAXSUB));
     long long nsuper = (nsub_total + subs - 1) / subs;
     long long grid = std::max<long long>(1, std::min<long long>(resident, nsuper));
-    if (((uintptr_t)d_xy & 31u) == 0)
-        k2_filter_compact<true><<<(unsigned)grid, K2_THREADS, 0, st>>>(
-            d_xy, n, index_base, d_oct, hdr_of(d_ws), status_of(d_ws), d_surv, d_count, (unsigned)nsuper, (int)subs);
-    else
-        k2_filter_compact<false><<<(unsigned)grid, K2_THREADS, 0, st>>>(
-            d_xy, n, index_base, d_oct, hdr_of(d_ws), status_of(d_ws), d_surv, d_count, (unsigned)nsuper, (int)subs);
+    k2_filter_compact<<<(unsigned)grid, K2_THREADS, K2_DSMEM, st>>>(
+        d_xy, n, index_base, d_oct, hdr_of(d_ws), status_of(d_ws), d_surv, d_count, (unsigned)nsuper, (int)subs);
     return cuda_check("k2_filter_compact");
 }
 
