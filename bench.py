@@ -372,7 +372,7 @@ def run_ours(a):
     # ---- CPU oracle baseline (rank 0, N = 1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        m_cap = min(n_local, 200_000_000)
+        m_cap = n_local
         host = xy[:m_cap].cpu().numpy()
         m, dt, s = oracle_rate(host, a.cpu_seconds)
         cpu = {"value": m / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",

@@ -51,13 +51,21 @@ def empty_record(device) -> torch.Tensor:
     return t.to(device)
 
 
+def _all_gather_flat(out: torch.Tensor, inp: torch.Tensor, group=None) -> torch.Tensor:
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, inp, group=group)   # one NCCL all-gather, in place
+    else:  # gloo (CPU tests)
+        parts = list(out.chunk(dist.get_world_size(group)))
+        dist.all_gather(parts, inp, group=group)
+    return out
+
+
 def exchange_extremes(ext_local: torch.Tensor, group=None, out: torch.Tensor | None = None) -> torch.Tensor:
     """a4: all-gather one record per rank -> [world * 24] int64 (rank order)."""
     world = dist.get_world_size(group)
     if out is None:
         out = torch.empty(world * EXT_WORDS, dtype=torch.int64, device=ext_local.device)
-    dist.all_gather_into_tensor(out, ext_local, group=group)
-    return out
+    return _all_gather_flat(out, ext_local, group)
 
 
 def exclusive_offsets(count: torch.Tensor, group=None, out: torch.Tensor | None = None):
@@ -66,8 +74,7 @@ def exclusive_offsets(count: torch.Tensor, group=None, out: torch.Tensor | None 
     world = dist.get_world_size(group)
     if out is None:
         out = torch.empty(world, dtype=torch.int64, device=count.device)
-    dist.all_gather_into_tensor(out, count.reshape(1), group=group)
-    return out
+    return _all_gather_flat(out, count.reshape(1), group)
 
 
 def offsets_from_counts(counts, rank: int) -> tuple[int, int]:
