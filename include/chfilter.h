@@ -84,7 +84,14 @@ typedef struct {
  * the four corners (D_k is monotone in x and in y under round-to-nearest, so
  * the corners bound it); points inside it are discarded without edge tests.
  * It never changes a result.  guess_edge/cx/cy: the octant of (x-cx, y-cy)
- * picks the edge tested first (a pure speed hint). */
+ * picks the edge tested first (a pure speed hint).
+ * f32_*: an fp32 pre-filter per edge with a static error bound (DESIGN.md
+ * "fp32 certification"): g = fma(a, fl32(x), fma(b, fl32(y), cin)) >= 0
+ * proves D_k > thr[k]; h = fma(a, fl32(x), fma(b, fl32(y), cout)) <= -0
+ * proves D_k < thr[k]; otherwise D_k is evaluated in fp64.  Valid only for
+ * points inside bbox, so the kernels use it only with octagons they built
+ * themselves (has_f32 is cleared on a caller-supplied octagon).  It never
+ * changes a result. */
 typedef struct {
     int32_t nv;
     int32_t degenerate;
@@ -97,6 +104,9 @@ typedef struct {
     int32_t plain;     /* 1 if built with CH_PLAIN                       */
     int32_t guess_edge[8];
     double cx, cy;
+    float f32_a[8], f32_b[8], f32_cin[8], f32_cout[8];
+    int32_t has_f32;
+    int32_t pad_;
 } ch_octagon;
 
 /* Result of the last filter call on a workspace (device-resident copy in the

@@ -31,6 +31,8 @@ class Octagon(ctypes.Structure):
         ("vx", DBL * 8), ("vy", DBL * 8), ("ex", DBL * 8), ("ey", DBL * 8), ("thr", DBL * 8),
         ("bbox", DBL * 4), ("box", DBL * 4), ("has_box", I32), ("plain", I32),
         ("guess_edge", I32 * 8), ("cx", DBL), ("cy", DBL),
+        ("f32_a", ctypes.c_float * 8), ("f32_b", ctypes.c_float * 8), ("f32_cin", ctypes.c_float * 8),
+        ("f32_cout", ctypes.c_float * 8), ("has_f32", I32), ("pad_", I32),
     ]
 
 

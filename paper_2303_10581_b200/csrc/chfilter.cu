@@ -141,11 +141,14 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long *bar)
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity)
 {
+    // try_wait with a suspend-time hint: the warp sleeps until the phase
+    // completes (or the hint expires) instead of spinning on issue slots.
     unsigned ok = 0;
     while (true) {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+                     " selp.u32 %0, 1, 0, p;\n}"
                      : "=r"(ok)
-                     : "r"(smem_u32(bar)), "r"(parity)
+                     : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
                      : "memory");
         if (ok)
             break;
@@ -392,11 +395,15 @@ __global__ void k3_combine8(const ch_extremes *__restrict__ all, int world, int 
 struct __align__(16) SEdge {
     double ax, ay, ex, ey, thr, pad;
 };
+struct __align__(16) FEdge {
+    float a, b, cin, cout;
+};
 struct SOct {
     SEdge e[8];
+    FEdge f[8];
     double box[4];
     double cx, cy;
-    int nv, degenerate;
+    int nv, degenerate, has_f32;
     int guess[8];
 };
 
@@ -411,6 +418,10 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.e[t].thr = o->thr[t];
         s.e[t].pad = 0.0;
         s.guess[t] = o->guess_edge[t];
+        s.f[t].a = o->f32_a[t];
+        s.f[t].b = o->f32_b[t];
+        s.f[t].cin = o->f32_cin[t];
+        s.f[t].cout = o->f32_cout[t];
     } else if (t == 8) {
         s.box[0] = o->box[0];
         s.box[1] = o->box[1];
@@ -420,6 +431,7 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.cy = o->cy;
         s.nv = o->nv;
         s.degenerate = o->degenerate;
+        s.has_f32 = o->has_f32;
     }
 }
 
@@ -453,15 +465,20 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
 // skipped when no lane of the warp needs it (warp-uniform branches):
 //  1. the certified accept box (4 DSETP): inside => discarded (proof at
 //     chf::box_valid);
-//  2. the guessed edge of the point's octant: D_g <= T_g => kept (this IS
-//     the oracle's exists-k condition, no proof needed).  Adaptive: a warp
-//     that needed stage 3 anyway skips stage 2 for the next 15 sub-tiles;
-//  3. every edge for every still-undecided point: nv x NP independent
-//     chains (ILP), edge parameters broadcast from shared memory.
+//  2. (has_f32) the fp32 pre-filter on every edge (proof at chf::build_f32):
+//     g_k >= 0 on every edge certifies discard, h_k <= 0 on some edge
+//     certifies keep; then
+//  3. fp64 D_k on every edge for the points left in the uncertainty band.
+// Before stage 2, adaptively: 2'. the guessed edge of the point's octant
+// (D_g <= T_g => kept, the oracle's exists-k condition); a warp whose
+// points 2' did not settle skips 2' for the next 15 sub-tiles.  Without
+// has_f32 (caller-supplied octagon) stage 3 runs on every edge of every
+// undecided point.
 template <int NP>
 __device__ __forceinline__ unsigned classify(const SOct &s, const double (&px)[NP], const double (&py)[NP],
                                              unsigned valid, int &guess_mode)
 {
+    static_assert(NP <= 32, "one mask bit per point");
     unsigned und = 0;
 #pragma unroll
     for (int i = 0; i < NP; i++) {
@@ -471,8 +488,10 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const double (&px)[N
     und &= valid;
     if (!__any_sync(FULL, und))
         return 0u;
+    const int nv = s.nv;
     unsigned keep = 0;
     if (guess_mode <= 0) {
+        // 2'. the guessed edge of the point's octant: D_g <= T_g => kept
 #pragma unroll
         for (int i = 0; i < NP; i++) {
             double dx = __dsub_rn(px[i], s.cx), dy = __dsub_rn(py[i], s.cy);
@@ -487,11 +506,58 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const double (&px)[N
         und &= ~keep;
         if (!__any_sync(FULL, und))
             return keep;
-        guess_mode = 16; // stage 3 was needed anyway: skip stage 2 for a while
+        guess_mode = 16; // the next stage was needed anyway: skip 2' for a while
     }
     guess_mode--;
+    if (s.has_f32) {
+        // fp32 certification on every edge: OR the sign bits of g_k (any
+        // g_k < 0 or -0 => not certified inside) and of h_k (any h_k <= -0
+        // => certified outside).  Proof at chf::build_f32.
+        float xf[NP], yf[NP];
+        unsigned sg[NP], sh[NP];
+#pragma unroll
+        for (int i = 0; i < NP; i++) {
+            xf[i] = __double2float_rn(px[i]);
+            yf[i] = __double2float_rn(py[i]);
+            sg[i] = 0u;
+            sh[i] = 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            if (k < nv) {
+                const FEdge f = s.f[k];
+#pragma unroll
+                for (int i = 0; i < NP; i++) {
+                    sg[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cin)));
+                    sh[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cout)));
+                }
+            }
+        }
+        unsigned in = 0, out = 0;
+#pragma unroll
+        for (int i = 0; i < NP; i++) {
+            in |= ((~sg[i]) >> 31) << i;
+            out |= (sh[i] >> 31) << i;
+        }
+        keep |= und & out;
+        und &= ~(in | out); // certified inside => discarded
+        if (!__any_sync(FULL, und))
+            return keep;
+        // fp64 on every edge for the (rare) points inside the uncertainty band
+        unsigned disc = und;
+        for (int k = 0; k < nv; k++) {
+            const double ax = s.e[k].ax, ay = s.e[k].ay, ex = s.e[k].ex, ey = s.e[k].ey, thr = s.e[k].thr;
+#pragma unroll
+            for (int i = 0; i < NP; i++) {
+                if ((und >> i) & 1u) {
+                    const double D = chf::edge_det(ax, ay, ex, ey, px[i], py[i]);
+                    disc &= ~((D > thr ? 0u : 1u) << i);
+                }
+            }
+        }
+        return keep | (und & ~disc);
+    }
     unsigned disc = und;
-    const int nv = s.nv;
     for (int k = 0; k < nv; k++) {
         const double ax = s.e[k].ax, ay = s.e[k].ay, ex = s.e[k].ex, ey = s.e[k].ey, thr = s.e[k].thr;
 #pragma unroll
@@ -938,6 +1004,9 @@ ch_status stage_octagon(const ch_octagon *h_oct, void *d_ws, cudaStream_t st, co
     if (h_oct) {
         cudaMemcpyAsync(&h->oct, h_oct, sizeof(ch_octagon), cudaMemcpyHostToDevice, st);
         cudaMemsetAsync(&h->result.nonfinite, 0, sizeof(int32_t), st); // no K1 pass: nothing checked
+        // the fp32 pre-filter's error bound assumes every point lies in the
+        // octagon's bbox, which only holds for octagons built from the data
+        cudaMemsetAsync(&h->oct.has_f32, 0, sizeof(int32_t), st);
         ch_status s = cuda_check("octagon upload");
         if (s != CH_OK)
             return s;

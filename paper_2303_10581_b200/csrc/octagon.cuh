@@ -22,12 +22,16 @@
 #define CH_SUB(a, b) __dsub_rn((a), (b))
 #define CH_MUL(a, b) __dmul_rn((a), (b))
 #define CH_INF (__longlong_as_double(0x7ff0000000000000LL))
+#define CH_F32(v) __double2float_rn(v)
+#define CH_NEXTF(a, b) nextafterf((a), (b))
 #else
 #define CH_HD inline
 #define CH_ADD(a, b) ((a) + (b))
 #define CH_SUB(a, b) ((a) - (b))
 #define CH_MUL(a, b) ((a) * (b))
 #define CH_INF (__builtin_inf())
+#define CH_F32(v) ((float)(v))
+#define CH_NEXTF(a, b) __builtin_nextafterf((a), (b))
 #endif
 
 namespace chf {
@@ -69,6 +73,63 @@ CH_HD bool box_valid(const ch_octagon &o, double x0, double x1, double y0, doubl
     return true;
 }
 
+// fp32 value >= v (round to nearest, then one step up if it fell below).
+CH_HD float f32_up(double v)
+{
+    float f = CH_F32(v);
+    return ((double)f < v) ? CH_NEXTF(f, __builtin_huge_valf()) : f;
+}
+CH_HD float f32_down(double v)
+{
+    float f = CH_F32(v);
+    return ((double)f > v) ? CH_NEXTF(f, -__builtin_huge_valf()) : f;
+}
+
+// fp32 certification of the edge predicate.
+// For a point inside the bounding box let E = a x + b y + c exactly, with
+// a = -ey, b = ex, c = ey ax - ex ay (ex, ey, ax, ay the stored doubles), so
+// E = ex (y - ay) - ey (x - ax).  Then (eps = 2^-53, u = 2^-24):
+//   |D_k - E| <= 3.001 eps S_k                           (five fp64 roundings)
+//   g = fma32(fl32(a), fl32(x), fma32(fl32(b), fl32(y), cin))
+//   |g - (a x + b y + cin)| <= 4.001 u (|a| Xm + |b| Ym + |cin|)
+// (Xm, Ym: largest |x|, |y| in the box).  cin is rounded DOWN from
+// fl(c) - T_k - M_k with M_k = 8 u (B0 + C + |T_k|) + 4 eps S_k + 2^-100,
+// B0 = |a| Xm + |b| Ym, C = |ey ax| + |ex ay| (>= |c| and bounding fl(c)'s
+// error by 3 eps C).  So c - T_k - cin >= M_k - 3 eps C, which exceeds
+// 4.001 u (B0 + |cin|) + 3.001 eps S_k, and g >= 0 implies E - T_k >
+// 3.001 eps S_k, i.e. D_k > T_k.  Symmetrically cout is rounded UP from
+// fl(c) - T_k + M_k and h <= 0 implies D_k < T_k.  The 2^-100 slack covers
+// fp32 subnormal roundings.  Enabled only when the box lies within
+// [-2^40, 2^40]^2 (no fp32 overflow).
+CH_HD void build_f32(ch_octagon &o)
+{
+    o.has_f32 = 0;
+    const double Xm = dmax(dabs(o.bbox[0]), dabs(o.bbox[1]));
+    const double Ym = dmax(dabs(o.bbox[2]), dabs(o.bbox[3]));
+    if (o.degenerate || !(Xm <= 0x1p40) || !(Ym <= 0x1p40))
+        return;
+    for (int k = 0; k < o.nv; k++) {
+        const double ax = o.vx[k], ay = o.vy[k], ex = o.ex[k], ey = o.ey[k];
+        const double c = CH_SUB(CH_MUL(ey, ax), CH_MUL(ex, ay));
+        const double C = CH_ADD(dabs(CH_MUL(ey, ax)), dabs(CH_MUL(ex, ay)));
+        const double B0 = CH_ADD(CH_MUL(dabs(ey), Xm), CH_MUL(dabs(ex), Ym));
+        const double X = dmax(CH_SUB(o.bbox[1], ax), CH_SUB(ax, o.bbox[0]));
+        const double Y = dmax(CH_SUB(o.bbox[3], ay), CH_SUB(ay, o.bbox[2]));
+        const double S = CH_ADD(CH_MUL(dabs(ex), Y), CH_MUL(dabs(ey), X));
+        const double T = o.thr[k];
+        // 1 + 2^-20 factors absorb the roundings of these fp64 bound computations
+        const double M = CH_MUL(CH_ADD(CH_ADD(CH_MUL(CH_ADD(CH_ADD(B0, C), dabs(T)), 8.0 * 0x1p-24),
+                                              CH_MUL(S, 4.0 * 0x1p-53)),
+                                       0x1p-100),
+                                1.0 + 0x1p-20);
+        o.f32_a[k] = CH_F32(-ey);
+        o.f32_b[k] = CH_F32(ex);
+        o.f32_cin[k] = f32_down(CH_SUB(CH_SUB(c, T), M));
+        o.f32_cout[k] = f32_up(CH_ADD(CH_SUB(c, T), M));
+    }
+    o.has_f32 = 1;
+}
+
 // Octagon assembly (DESIGN R5): cycle [R,TR,T,TL,L,BL,B,BR]; drop a vertex
 // equal (numeric ==) to the last kept one, then trailing vertices equal to
 // the first; nv < 3 => degenerate (every point survives, R6).  Certified
@@ -84,7 +145,10 @@ CH_HD void build_octagon(const ch_extremes &e, int flags, ch_octagon &o)
         o.vidx[k] = -1;
         o.vx[k] = o.vy[k] = o.ex[k] = o.ey[k] = o.thr[k] = 0.0;
         o.guess_edge[k] = 0;
+        o.f32_a[k] = o.f32_b[k] = o.f32_cin[k] = o.f32_cout[k] = 0.0f;
     }
+    o.has_f32 = 0;
+    o.pad_ = 0;
     for (int k = 0; k < 8; k++) {
         double x = e.x[k], y = e.y[k];
         if (!(o.nv > 0 && x == o.vx[o.nv - 1] && y == o.vy[o.nv - 1])) {
@@ -131,6 +195,8 @@ CH_HD void build_octagon(const ch_extremes &e, int flags, ch_octagon &o)
     // test first the edge leaving slot k's kept vertex (speed hint only).
     for (int k = 0; k < 8; k++)
         o.guess_edge[k] = slot_vertex[k] < o.nv ? slot_vertex[k] : 0;
+
+    build_f32(o);
 
     // Early-accept box from the corner vertices, validated (and shrunk
     // toward the centre until valid) with box_valid().

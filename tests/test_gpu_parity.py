@@ -266,3 +266,45 @@ def test_parity_full_1e9_normal_sampled():
     pre = 10 ** 8
     keep_pre = oracle.flags(xy[:pre], oct_=wo)
     assert np.array_equal(np.flatnonzero(keep_pre), surv[surv < pre])
+
+
+def _edge_band_points(rng, o, dists, per=400):
+    """Points at signed distances d * |edge| from every octagon edge (both
+    sides), around the fp32 pre-filter's uncertainty band."""
+    V = list(zip(o["vx"], o["vy"]))
+    nv = len(V)
+    pts = []
+    for k in range(nv):
+        a, b = np.array(V[k]), np.array(V[(k + 1) % nv])
+        ev = b - a
+        L = np.hypot(*ev)
+        nrm = np.array([-ev[1], ev[0]]) / L         # inward normal (CCW polygon)
+        for d in dists:
+            t = 0.02 + 0.96 * rng.random(per)
+            for sgn in (-1.0, 1.0):
+                pts.append(a[None, :] + t[:, None] * ev[None, :] + (sgn * d * L) * nrm[None, :])
+    return np.concatenate(pts)
+
+
+@pytest.mark.parametrize("dist", ["displaced", "circle", "normal"])
+def test_parity_fp32_prefilter_band(dist):
+    """Points straddling the fp32 certification margin (relative distances
+    1e-13 .. 1e-3 from each edge): certified, uncertain and fp64-decided paths."""
+    rng = np.random.default_rng(21)
+    base = synth.points(dist, 100_000, seed=21).numpy()
+    o = oracle.octagon(base)
+    band = _edge_band_points(rng, o, [10.0 ** -e for e in range(3, 14)])
+    xy = np.concatenate([base, band])
+    _, oc = chf.extremes8(torch.tensor(xy, device=DEV))
+    assert oc.has_f32 == 1
+    check_against_oracle(torch.tensor(xy, device=DEV), name=f"band-{dist}")
+
+
+@pytest.mark.parametrize("scale", [1e-40, 1e-20, 1e9, 1e15, 1e120])
+def test_parity_extreme_scales(scale):
+    """Scaled inputs: tiny (fp32 subnormal range), large, and beyond the fp32
+    pre-filter's 2^40 domain (fp64-only path)."""
+    xy = synth.points("displaced", 200_003, seed=22).numpy() * scale
+    _, oc = chf.extremes8(torch.tensor(xy, device=DEV))
+    assert oc.has_f32 == (1 if scale < 2.0 ** 40 / 0.3 else 0)
+    check_against_oracle(torch.tensor(xy, device=DEV), name=f"scale-{scale}")
