@@ -41,10 +41,10 @@ constexpr int K2_CTHREADS = K2_CWARPS * 32;
 constexpr int K2_PUB_WARP = K2_CWARPS;                         // publisher warp
 constexpr int K2_PROD_WARP = K2_CWARPS + 1;                    // TMA producer warp
 constexpr int K2_THREADS = K2_CTHREADS + 64;
-constexpr int K2_NP = 4;                                       // points per consumer thread per sub-tile
+constexpr int K2_NP = 8;                                       // points per consumer thread per sub-tile
 constexpr long long K2_SUB = (long long)K2_CTHREADS * K2_NP;   // 1024 points (16 KB) per sub-tile
-constexpr int K2_STAGES = 6;                                   // TMA ring depth (sub-tiles)
-constexpr int K2_MAXSUB = 32;                                  // sub-tiles per super-tile (max)
+constexpr int K2_STAGES = 3;                                   // TMA ring depth (sub-tiles)
+constexpr int K2_MAXSUB = 16;                                  // sub-tiles per super-tile (max)
 constexpr int K2_GROUPS = K2_NP * K2_CWARPS;                   // 32-point groups per sub-tile
 constexpr int K2_ENTRIES = K2_MAXSUB * K2_GROUPS;              // ballot words per super-tile
 static_assert(K2_ENTRIES == 4 * K2_CTHREADS, "block scan: 4 entries per consumer thread");
