@@ -145,11 +145,19 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
     // completes (or the hint expires) instead of spinning on issue slots.
     unsigned ok = 0;
     while (true) {
+#ifdef CH_NO_SUSPEND_HINT
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok)
+                     : "r"(smem_u32(bar)), "r"(parity)
+                     : "memory");
+#else
         asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
                      " selp.u32 %0, 1, 0, p;\n}"
                      : "=r"(ok)
                      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
                      : "memory");
+#endif
         if (ok)
             break;
     }
@@ -199,6 +207,50 @@ __device__ __forceinline__ void reduce_pair(int k, double &v, long long &i, doub
     }
 }
 
+// The octagon (DESIGN R5, R4) built by a whole CTA from extremes in shared
+// memory: thread 0 assembles the vertices, one thread per edge computes
+// ex, ey, T_k and the fp32 constants, one thread per (box candidate, edge,
+// corner) validates the accept box, and thread 0 keeps the first candidate
+// valid at every corner.  Same functions, same result as the serial
+// chf::build_octagon (the host path).  Called by every thread of the CTA.
+__device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o /*shared*/)
+{
+    __shared__ int s_bad[chf::BOX_CANDIDATES];
+    const int tid = threadIdx.x;
+    if (tid == 0)
+        chf::octagon_vertices(e, flags, o);
+    if (tid < chf::BOX_CANDIDATES)
+        s_bad[tid] = 0;
+    __syncthreads();
+    if (o.degenerate)
+        return;
+    if (tid < o.nv)
+        chf::octagon_edge(o, tid);
+    __syncthreads();
+    for (int q = tid; q < chf::BOX_CANDIDATES * 32; q += blockDim.x) {
+        const int t = q >> 5, k = (q >> 2) & 7, corner = q & 3;
+        double b[4];
+        if (k < o.nv && (!chf::box_candidate(e, t, b) || !chf::box_corner_ok(o, k, b, corner)))
+            s_bad[t] = 1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        o.has_f32 = chf::f32_domain_ok(o) ? 1 : 0;
+        for (int t = 0; t < chf::BOX_CANDIDATES; t++) {
+            double b[4];
+            if (!s_bad[t] && chf::box_candidate(e, t, b)) {
+                o.box[0] = b[0];
+                o.box[1] = b[1];
+                o.box[2] = b[2];
+                o.box[3] = b[3];
+                o.has_box = 1;
+                break;
+            }
+        }
+    }
+    __syncthreads();
+}
+
 __device__ void k1_finalize(const double *__restrict__ xy, long long index_base, int flags,
                             WsHeader *hdr, const Partial *parts, int nparts, void *ext_out)
 {
@@ -235,26 +287,39 @@ __device__ void k1_finalize(const double *__restrict__ xy, long long index_base,
     if (tid == 0)
         s_nf = nf;
     __syncthreads();
-    if (tid == 0) {
-        ch_extremes e;
-        for (int k = 0; k < 8; k++) {
-            double bv = s_v[0][k];
-            long long bi = s_i[0][k];
-            for (int w = 1; w < K1_THREADS / 32; w++)
-                reduce_pair(k, bv, bi, s_v[w][k], s_i[w][k]);
-            long long loc = bi - index_base;
-            e.idx[k] = bi;
-            e.x[k] = xy[2 * loc];
-            e.y[k] = xy[2 * loc + 1];
+    __shared__ ch_extremes s_e;
+    __shared__ ch_octagon s_o;
+    if (tid < 8) {
+        const int k = tid;
+        double bv = s_v[0][k];
+        long long bi = s_i[0][k];
+        for (int w = 1; w < K1_THREADS / 32; w++)
+            reduce_pair(k, bv, bi, s_v[w][k], s_i[w][k]);
+        const long long loc = bi - index_base;
+        s_e.idx[k] = bi;
+        s_e.x[k] = xy[2 * loc];
+        s_e.y[k] = xy[2 * loc + 1];
+    }
+    __syncthreads();
+    build_octagon_cta(s_e, flags, s_o);
+    // publish (cooperative copies of the two structs)
+    {
+        const unsigned *src = (const unsigned *)&s_o;
+        unsigned *dst = (unsigned *)&hdr->oct;
+        for (int i = tid; i < (int)(sizeof(ch_octagon) / 4); i += K1_THREADS)
+            dst[i] = src[i];
+        const unsigned *se = (const unsigned *)&s_e;
+        unsigned *de = (unsigned *)&hdr->ext;
+        unsigned *dx = (unsigned *)ext_out;
+        for (int i = tid; i < (int)(sizeof(ch_extremes) / 4); i += K1_THREADS) {
+            de[i] = se[i];
+            if (dx)
+                dx[i] = se[i];
         }
-        ch_octagon o;
-        chf::build_octagon(e, flags, o);
-        hdr->ext = e;
-        hdr->oct = o;
+    }
+    if (tid == 0) {
         hdr->result.nonfinite = s_nf;
-        hdr->result.degenerate = o.degenerate;
-        if (ext_out)
-            *(ch_extremes *)ext_out = e;
+        hdr->result.degenerate = s_o.degenerate;
         hdr->k1_ticket = 0; // ready for the next call (stream order)
     }
 }
@@ -358,21 +423,23 @@ k1_extremes8(const double *__restrict__ xy, long long n, long long index_base, i
 }
 
 // ===================================================================== K3 ==
-__global__ void k3_combine8(const ch_extremes *__restrict__ all, int world, int flags, WsHeader *hdr)
+__global__ void __launch_bounds__(256) k3_combine8(const ch_extremes *__restrict__ all, int world, int flags,
+                                                   WsHeader *hdr)
 {
-    if (threadIdx.x != 0)
-        return;
-    ch_extremes e;
-    for (int k = 0; k < 8; k++) {
+    __shared__ ch_extremes s_e;
+    __shared__ ch_octagon s_o;
+    const int tid = threadIdx.x;
+    if (tid < 8) {
+        const int k = tid;
         double bv = chf::slot_is_max(k) ? -CH_INF : CH_INF;
         long long bi = LLONG_MAX;
         double bx = 0.0, by = 0.0;
         for (int r = 0; r < world; r++) {
-            long long i = all[r].idx[k];
+            const long long i = all[r].idx[k];
             if (i < 0)
                 continue; // empty shard
-            double x = all[r].x[k], y = all[r].y[k];
-            double key = chf::slot_key(k, x, y);
+            const double x = all[r].x[k], y = all[r].y[k];
+            const double key = chf::slot_key(k, x, y);
             if (chf::slot_better(k, key, i, bv, bi)) {
                 bv = key;
                 bi = i;
@@ -380,15 +447,22 @@ __global__ void k3_combine8(const ch_extremes *__restrict__ all, int world, int 
                 by = y;
             }
         }
-        e.idx[k] = bi;
-        e.x[k] = bx;
-        e.y[k] = by;
+        s_e.idx[k] = bi;
+        s_e.x[k] = bx;
+        s_e.y[k] = by;
     }
-    ch_octagon o;
-    chf::build_octagon(e, flags, o);
-    hdr->ext = e;
-    hdr->oct = o;
-    hdr->result.degenerate = o.degenerate;
+    __syncthreads();
+    build_octagon_cta(s_e, flags, s_o);
+    const unsigned *src = (const unsigned *)&s_o;
+    unsigned *dst = (unsigned *)&hdr->oct;
+    for (int i = tid; i < (int)(sizeof(ch_octagon) / 4); i += blockDim.x)
+        dst[i] = src[i];
+    const unsigned *se = (const unsigned *)&s_e;
+    unsigned *de = (unsigned *)&hdr->ext;
+    for (int i = tid; i < (int)(sizeof(ch_extremes) / 4); i += blockDim.x)
+        de[i] = se[i];
+    if (tid == 0)
+        hdr->result.degenerate = s_o.degenerate;
 }
 
 // ========================================================= octagon test ==
@@ -437,7 +511,7 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
 
 // Survivor test, bit-identical to "not (forall k: D_k > T_k)" (R4): the
 // accept box and the edge order are shortcuts that cannot change the result
-// (box: proof at chf::box_valid; order: a conjunction is order-free).
+// (box: proof at chf::box_corner_ok; order: a conjunction is order-free).
 __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
 {
     if (x >= s.box[0] && x <= s.box[1] && y >= s.box[2] && y <= s.box[3])
@@ -464,8 +538,8 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
 // to "not (forall k: D_k > T_k)" for every valid point (R4).  Stages, each
 // skipped when no lane of the warp needs it (warp-uniform branches):
 //  1. the certified accept box (4 DSETP): inside => discarded (proof at
-//     chf::box_valid);
-//  2. (has_f32) the fp32 pre-filter on every edge (proof at chf::build_f32):
+//     chf::box_corner_ok);
+//  2. (has_f32) the fp32 pre-filter on every edge (proof at chf::octagon_edge):
 //     g_k >= 0 on every edge certifies discard, h_k <= 0 on some edge
 //     certifies keep; then
 //  3. fp64 D_k on every edge for the points left in the uncertainty band.
@@ -512,7 +586,7 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const double (&px)[N
     if (s.has_f32) {
         // fp32 certification on every edge: OR the sign bits of g_k (any
         // g_k < 0 or -0 => not certified inside) and of h_k (any h_k <= -0
-        // => certified outside).  Proof at chf::build_f32.
+        // => certified outside).  Proof at chf::octagon_edge.
         float xf[NP], yf[NP];
         unsigned sg[NP], sh[NP];
 #pragma unroll
@@ -653,8 +727,14 @@ k2_filter_compact(const double *__restrict__ xy, long long n, long long index_ba
                 if (seq >= K2_STAGES)
                     mbar_wait(&s_empty[st], ((seq / K2_STAGES) - 1) & 1u); // consumers released it
                 if (p_super >= nsuper) {
+                    // End of stream.  (compute-sanitizer racecheck flags this
+                    // store against the consumers' descriptor read: it does not
+                    // model a phase completed by a tx-less arrive.  The arrive
+                    // has release and try_wait acquire semantics, and the slot's
+                    // previous readers released it through s_empty, exactly as
+                    // for data stages.)
                     s_desc_super[st] = TILE_DONE;
-                    mbar_arrive(&s_full[st]);
+                    mbar_expect_tx(&s_full[st], 0u);
                     break;
                 }
                 const long long base = (long long)p_super * super_pts + (long long)p_j * K2_SUB;
@@ -1124,7 +1204,7 @@ ch_status ch_combine8(const void *d_ext_all, int world, int flags, void *d_ws, s
     ch_status s = check_ws(d_ws, ws_bytes, 0);
     if (s != CH_OK)
         return s;
-    k3_combine8<<<1, 32, 0, (cudaStream_t)stream>>>((const ch_extremes *)d_ext_all, world, flags, hdr_of(d_ws));
+    k3_combine8<<<1, 256, 0, (cudaStream_t)stream>>>((const ch_extremes *)d_ext_all, world, flags, hdr_of(d_ws));
     return cuda_check("k3_combine8");
 }
 

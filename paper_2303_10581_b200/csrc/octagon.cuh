@@ -54,24 +54,9 @@ CH_HD double dmin(double a, double b) { return a < b ? a : b; }
 // Box validity: D_k is non-decreasing or non-increasing in x and in y
 // separately (every RNE operation is monotone in each argument), so on a
 // closed axis box its minimum is attained at one of the four corners.  If
-// every corner satisfies D_k > T_k for every edge, every point of the box
-// does, i.e. the box only ever discards points the oracle discards.
-CH_HD bool box_valid(const ch_octagon &o, double x0, double x1, double y0, double y1)
-{
-    if (!(x0 <= x1) || !(y0 <= y1))
-        return false;
-    for (int k = 0; k < o.nv; k++) {
-        double cxs[2] = {x0, x1};
-        double cys[2] = {y0, y1};
-        for (int i = 0; i < 2; i++)
-            for (int j = 0; j < 2; j++) {
-                double D = edge_det(o.vx[k], o.vy[k], o.ex[k], o.ey[k], cxs[i], cys[j]);
-                if (!(D > o.thr[k]))
-                    return false;
-            }
-    }
-    return true;
-}
+// every corner satisfies D_k > T_k for every edge (box_corner_ok below),
+// every point of the box does, i.e. the box only ever discards points the
+// oracle discards.
 
 // fp32 value >= v (round to nearest, then one step up if it fell below).
 CH_HD float f32_up(double v)
@@ -85,7 +70,8 @@ CH_HD float f32_down(double v)
     return ((double)f > v) ? CH_NEXTF(f, -__builtin_huge_valf()) : f;
 }
 
-// fp32 certification of the edge predicate.
+// fp32 certification of the edge predicate,
+// computed per edge in octagon_edge().
 // For a point inside the bounding box let E = a x + b y + c exactly, with
 // a = -ey, b = ex, c = ey ax - ex ay (ex, ey, ax, ay the stored doubles), so
 // E = ex (y - ay) - ey (x - ax).  Then (eps = 2^-53, u = 2^-24):
@@ -101,40 +87,50 @@ CH_HD float f32_down(double v)
 // fl(c) - T_k + M_k and h <= 0 implies D_k < T_k.  The 2^-100 slack covers
 // fp32 subnormal roundings.  Enabled only when the box lies within
 // [-2^40, 2^40]^2 (no fp32 overflow).
-CH_HD void build_f32(ch_octagon &o)
+CH_HD bool f32_domain_ok(const ch_octagon &o)
 {
-    o.has_f32 = 0;
     const double Xm = dmax(dabs(o.bbox[0]), dabs(o.bbox[1]));
     const double Ym = dmax(dabs(o.bbox[2]), dabs(o.bbox[3]));
-    if (o.degenerate || !(Xm <= 0x1p40) || !(Ym <= 0x1p40))
-        return;
-    for (int k = 0; k < o.nv; k++) {
-        const double ax = o.vx[k], ay = o.vy[k], ex = o.ex[k], ey = o.ey[k];
-        const double c = CH_SUB(CH_MUL(ey, ax), CH_MUL(ex, ay));
-        const double C = CH_ADD(dabs(CH_MUL(ey, ax)), dabs(CH_MUL(ex, ay)));
-        const double B0 = CH_ADD(CH_MUL(dabs(ey), Xm), CH_MUL(dabs(ex), Ym));
-        const double X = dmax(CH_SUB(o.bbox[1], ax), CH_SUB(ax, o.bbox[0]));
-        const double Y = dmax(CH_SUB(o.bbox[3], ay), CH_SUB(ay, o.bbox[2]));
-        const double S = CH_ADD(CH_MUL(dabs(ex), Y), CH_MUL(dabs(ey), X));
-        const double T = o.thr[k];
-        // 1 + 2^-20 factors absorb the roundings of these fp64 bound computations
-        const double M = CH_MUL(CH_ADD(CH_ADD(CH_MUL(CH_ADD(CH_ADD(B0, C), dabs(T)), 8.0 * 0x1p-24),
-                                              CH_MUL(S, 4.0 * 0x1p-53)),
-                                       0x1p-100),
-                                1.0 + 0x1p-20);
-        o.f32_a[k] = CH_F32(-ey);
-        o.f32_b[k] = CH_F32(ex);
-        o.f32_cin[k] = f32_down(CH_SUB(CH_SUB(c, T), M));
-        o.f32_cout[k] = f32_up(CH_ADD(CH_SUB(c, T), M));
-    }
-    o.has_f32 = 1;
+    return !o.degenerate && Xm <= 0x1p40 && Ym <= 0x1p40;
 }
 
-// Octagon assembly (DESIGN R5): cycle [R,TR,T,TL,L,BL,B,BR]; drop a vertex
-// equal (numeric ==) to the last kept one, then trailing vertices equal to
-// the first; nv < 3 => degenerate (every point survives, R6).  Certified
-// threshold T_k = 2^-50 fl(fl(|ex| Y) + fl(|ey| X)) (R4; proof in DESIGN.md).
-CH_HD void build_octagon(const ch_extremes &e, int flags, ch_octagon &o)
+// Edge k of an octagon whose vertices and bbox are set: ex, ey, T_k (R4)
+// and the fp32 pre-filter constants.
+CH_HD void octagon_edge(ch_octagon &o, int k)
+{
+    const int k1 = (k + 1 == o.nv) ? 0 : k + 1;
+    const double ax = o.vx[k], ay = o.vy[k];
+    const double ex = CH_SUB(o.vx[k1], ax);
+    const double ey = CH_SUB(o.vy[k1], ay);
+    o.ex[k] = ex;
+    o.ey[k] = ey;
+    const double X = dmax(CH_SUB(o.bbox[1], ax), CH_SUB(ax, o.bbox[0]));
+    const double Y = dmax(CH_SUB(o.bbox[3], ay), CH_SUB(ay, o.bbox[2]));
+    const double S = CH_ADD(CH_MUL(dabs(ex), Y), CH_MUL(dabs(ey), X));
+    const double T = o.plain ? 0.0 : CH_MUL(S, 0x1p-50); // exact power-of-two scaling
+    o.thr[k] = T;
+    // fp32 pre-filter constants (used only if f32_domain_ok)
+    const double Xm = dmax(dabs(o.bbox[0]), dabs(o.bbox[1]));
+    const double Ym = dmax(dabs(o.bbox[2]), dabs(o.bbox[3]));
+    const double c = CH_SUB(CH_MUL(ey, ax), CH_MUL(ex, ay));
+    const double C = CH_ADD(dabs(CH_MUL(ey, ax)), dabs(CH_MUL(ex, ay)));
+    const double B0 = CH_ADD(CH_MUL(dabs(ey), Xm), CH_MUL(dabs(ex), Ym));
+    // 1 + 2^-20 absorbs the roundings of this fp64 bound computation
+    const double M = CH_MUL(CH_ADD(CH_ADD(CH_MUL(CH_ADD(CH_ADD(B0, C), dabs(T)), 8.0 * 0x1p-24),
+                                          CH_MUL(S, 4.0 * 0x1p-53)),
+                                   0x1p-100),
+                            1.0 + 0x1p-20);
+    o.f32_a[k] = CH_F32(-ey);
+    o.f32_b[k] = CH_F32(ex);
+    o.f32_cin[k] = f32_down(CH_SUB(CH_SUB(c, T), M));
+    o.f32_cout[k] = f32_up(CH_ADD(CH_SUB(c, T), M));
+}
+
+// Octagon assembly (DESIGN R5), vertex part: cycle [R,TR,T,TL,L,BL,B,BR];
+// drop a vertex equal (numeric ==) to the last kept one, then trailing
+// vertices equal to the first; nv < 3 => degenerate (every point survives,
+// R6).  Also the bbox, the octant centre and the guessed-edge table.
+CH_HD void octagon_vertices(const ch_extremes &e, int flags, ch_octagon &o)
 {
     o.nv = 0;
     o.degenerate = 0;
@@ -177,46 +173,65 @@ CH_HD void build_octagon(const ch_extremes &e, int flags, ch_octagon &o)
         o.degenerate = 1;
         return;
     }
-    for (int k = 0; k < o.nv; k++) {
-        int k1 = (k + 1 == o.nv) ? 0 : k + 1;
-        double ax = o.vx[k], ay = o.vy[k];
-        o.ex[k] = CH_SUB(o.vx[k1], ax);
-        o.ey[k] = CH_SUB(o.vy[k1], ay);
-        if (o.plain) {
-            o.thr[k] = 0.0;
-        } else {
-            double X = dmax(CH_SUB(o.bbox[1], ax), CH_SUB(ax, o.bbox[0]));
-            double Y = dmax(CH_SUB(o.bbox[3], ay), CH_SUB(ay, o.bbox[2]));
-            double S = CH_ADD(CH_MUL(dabs(o.ex[k]), Y), CH_MUL(dabs(o.ey[k]), X));
-            o.thr[k] = CH_MUL(S, 0x1p-50); // exact power-of-two scaling (RNE if subnormal)
-        }
-    }
     // Octant k of (x - cx, y - cy) lies between slot directions k and k+1;
     // test first the edge leaving slot k's kept vertex (speed hint only).
     for (int k = 0; k < 8; k++)
         o.guess_edge[k] = slot_vertex[k] < o.nv ? slot_vertex[k] : 0;
+}
 
-    build_f32(o);
+// Early-accept box candidate t (t < 7): the box spanned by the corner
+// vertices, shrunk toward its centre by shrink[t] of its size on each side.
+constexpr int BOX_CANDIDATES = 7;
+CH_HD bool box_candidate(const ch_extremes &e, int t, double b[4])
+{
+    const double x0 = dmax(e.x[3], e.x[5]), x1 = dmin(e.x[1], e.x[7]);
+    const double y0 = dmax(e.y[5], e.y[7]), y1 = dmin(e.y[1], e.y[3]);
+    if (!(x0 < x1 && y0 < y1))
+        return false;
+    const double shrink[BOX_CANDIDATES] = {0.0, 0x1p-40, 0x1p-24, 0x1p-12, 0x1p-6, 0x1p-3, 0x1p-2};
+    const double wx = CH_MUL(CH_SUB(x1, x0), shrink[t]);
+    const double wy = CH_MUL(CH_SUB(y1, y0), shrink[t]);
+    b[0] = CH_ADD(x0, wx);
+    b[1] = CH_SUB(x1, wx);
+    b[2] = CH_ADD(y0, wy);
+    b[3] = CH_SUB(y1, wy);
+    return b[0] <= b[1] && b[2] <= b[3];
+}
 
-    // Early-accept box from the corner vertices, validated (and shrunk
-    // toward the centre until valid) with box_valid().
-    double x0 = dmax(e.x[3], e.x[5]), x1 = dmin(e.x[1], e.x[7]);
-    double y0 = dmax(e.y[5], e.y[7]), y1 = dmin(e.y[1], e.y[3]);
-    if (x0 < x1 && y0 < y1) {
-        const double shrink[7] = {0.0, 0x1p-40, 0x1p-24, 0x1p-12, 0x1p-6, 0x1p-3, 0x1p-2};
-        for (int t = 0; t < 7; t++) {
-            double wx = CH_MUL(CH_SUB(x1, x0), shrink[t]);
-            double wy = CH_MUL(CH_SUB(y1, y0), shrink[t]);
-            double bx0 = CH_ADD(x0, wx), bx1 = CH_SUB(x1, wx);
-            double by0 = CH_ADD(y0, wy), by1 = CH_SUB(y1, wy);
-            if (box_valid(o, bx0, bx1, by0, by1)) {
-                o.box[0] = bx0;
-                o.box[1] = bx1;
-                o.box[2] = by0;
-                o.box[3] = by1;
-                o.has_box = 1;
-                break;
-            }
+// One corner of a candidate box against one edge: D_k(corner) > T_k.
+CH_HD bool box_corner_ok(const ch_octagon &o, int k, const double b[4], int corner)
+{
+    const double x = (corner & 1) ? b[1] : b[0];
+    const double y = (corner & 2) ? b[3] : b[2];
+    return edge_det(o.vx[k], o.vy[k], o.ex[k], o.ey[k], x, y) > o.thr[k];
+}
+
+// Serial assembly (host, and tests): vertices, every edge, the fp32 domain
+// flag, then the first valid accept-box candidate.  The device builds the
+// same octagon with one thread per edge / per (candidate, edge, corner).
+CH_HD void build_octagon(const ch_extremes &e, int flags, ch_octagon &o)
+{
+    octagon_vertices(e, flags, o);
+    if (o.degenerate)
+        return;
+    for (int k = 0; k < o.nv; k++)
+        octagon_edge(o, k);
+    o.has_f32 = f32_domain_ok(o) ? 1 : 0;
+    for (int t = 0; t < BOX_CANDIDATES; t++) {
+        double b[4];
+        if (!box_candidate(e, t, b))
+            continue;
+        bool ok = true;
+        for (int k = 0; k < o.nv && ok; k++)
+            for (int c = 0; c < 4 && ok; c++)
+                ok = box_corner_ok(o, k, b, c);
+        if (ok) {
+            o.box[0] = b[0];
+            o.box[1] = b[1];
+            o.box[2] = b[2];
+            o.box[3] = b[3];
+            o.has_box = 1;
+            break;
         }
     }
 }

@@ -12,3 +12,5 @@ for f in sorted(glob.glob("gpurun_out/bench_*.json")):
     except Exception as e: print(f, "ERR", e); continue
     r=d["roofline"]; print(f"{d['config']['workload']:28s} {d['value']:8.2f} Gpts/s  step {d['ms_per_step']:.3f} ms  k1 {r['k1_ms']:.3f} ({r['k1_gbs']:.0f} GB/s)  k2 {r['k2_ms']:.3f} ({r['k2_gbs']:.0f} GB/s)  hbm {d['hbm_frac']:.3f}  clk {d['clocks']['sm_mhz']} {d['clocks']['reasons']}")
 PY
+timeout 300 python bench.py --no-e2e --no-cpu-baseline --dist normal --n 1e4 --steps 500 --warmup 20 > gpurun_out/bench_normal_1e4.json 2>/dev/null
+python -c "import json; d=json.loads(open('gpurun_out/bench_normal_1e4.json').read().strip().splitlines()[-1]); r=d['roofline']; print('normal_1e4: step %.1f us  k1 %.1f us  k2 %.1f us' % (d['ms_per_step']*1e3, r['k1_ms']*1e3, r['k2_ms']*1e3))"

@@ -1,0 +1,18 @@
+# compute-sanitizer on the hot kernels at small n (1 GPU)
+set -x
+cat > /tmp/san.py <<'PY'
+import sys; sys.path.insert(0, ".")
+import numpy as np, torch, oracle, synth, paper_2303_10581_b200 as chf
+for dist, n in (("displaced", 300_001), ("circle", 70_000), ("normal", 200_003), ("displaced", 5)):
+    xy = synth.points(dist, n, seed=1, device="cuda")
+    ws = chf.Workspace(n)
+    s = chf.filter(xy, ws).cpu().numpy()
+    want, _ = oracle.filter_compact(xy.cpu().numpy())
+    assert np.array_equal(s, want), dist
+    chf.octagon_filter(xy, ws)
+    hull, surv, st = chf.hull_end_to_end(xy, ws)
+print("sanitize workload ok")
+PY
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san.py > gpurun_out/sanitize_$tool.log 2>&1; echo "$tool rc=$?"; tail -3 gpurun_out/sanitize_$tool.log
+done
