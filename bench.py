@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
     ap.add_argument("--plain", action="store_true", help="plain fp64 predicate (T_k = 0)")
+    ap.add_argument("--storage", choices=["f64", "f32"], default="f64",
+                    help="point storage precision (f32: the paper's, widened exactly to f64)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -66,7 +68,7 @@ def workload_name(a) -> str:
     e = int(round(math.log10(n))) if n > 0 and 10 ** round(math.log10(n)) == n else None
     size = f"1e{e}" if e is not None else str(n)
     d = a.dist if a.dist != "displaced" else f"displaced_p{a.p:g}"
-    return f"{d}_{size}_fp64"
+    return f"{d}_{size}_fp{'32' if getattr(a, 'storage', 'f64') == 'f32' else '64'}"
 
 
 class ClockSampler:
@@ -173,6 +175,8 @@ def run_reference(a):
     per_step_s = 120.0 / max(a.steps + a.warmup, 1)
     m = int(min(n, max(m0, m0 * min(per_step_s, 2.0) / max(dt0, 1e-9))))
     xy = synth.points(a.dist, n, seed=a.seed, p=a.p, device=dev, lo=0, hi=m).cpu().numpy()
+    if a.storage == "f32":
+        xy = xy.astype(np.float32).astype(np.float64)   # the widened f32 workload
     for _ in range(a.warmup):
         oracle.filter_compact(xy, certified=not a.plain)
     times = []
@@ -217,7 +221,10 @@ def run_ours(a):
     lo, hi = chdist.shard_range(n_total, world, rank)
     n_local = hi - lo
     xy = synth.points(a.dist, n_total, seed=a.seed, p=a.p, device=dev, lo=lo, hi=hi)
+    if a.storage == "f32":
+        xy = xy.float()
     torch.cuda.synchronize()
+    bpp = 8.0 if a.storage == "f32" else 16.0   # bytes per point per pass
     stream = torch.cuda.current_stream()
 
     if world == 1:
@@ -305,8 +312,8 @@ def run_ours(a):
 
     # ---- roofline of the dominant kernel (algorithmic bytes) ----
     peak, peak_src = measured_peaks()
-    k1_bytes = 16.0 * n_local
-    k2_bytes = 16.0 * n_local + 8.0 * s_local
+    k1_bytes = bpp * n_local
+    k2_bytes = bpp * n_local + 8.0 * s_local
     if k2_ms >= k1_ms:
         dom, dom_bytes, dom_ms = "k2_filter_compact", k2_bytes, k2_ms
     else:
@@ -323,7 +330,7 @@ def run_ours(a):
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
-    if not a.no_e2e and a.e2e_steps > 0:
+    if not a.no_e2e and a.e2e_steps > 0 and a.storage == "f64":
         h_xy = torch.empty(n_local, 2, dtype=torch.float64, pin_memory=True)
         h_xy.copy_(xy)
         h_out = torch.empty(max(n_local, 1), dtype=torch.int64)
@@ -373,7 +380,7 @@ def run_ours(a):
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         m_cap = n_local
-        host = xy[:m_cap].cpu().numpy()
+        host = xy[:m_cap].double().cpu().numpy()
         m, dt, s = oracle_rate(host, a.cpu_seconds)
         cpu = {"value": m / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"first {m} points of the same {workload_name(a)} input (oracle: extremes + octagon + "
@@ -386,9 +393,9 @@ def run_ours(a):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(a), "n": n_total, "n_per_gpu": n_local, "dist": a.dist,
                        "seed": a.seed, "p": a.p if a.dist == "displaced" else None,
-                       "predicate": "plain" if a.plain else "certified",
-                       "parallelism": f"dp{world}", "l2": "inputs larger than L2 (16 B/pt)"
-                       if 16 * n_local > 126e6 else "inputs smaller than L2 (not flushed)"},
+                       "predicate": "plain" if a.plain else "certified", "storage": a.storage,
+                       "parallelism": f"dp{world}", "l2": f"inputs larger than L2 ({int(bpp)} B/pt)"
+                       if bpp * n_local > 126e6 else "inputs smaller than L2 (not flushed)"},
             "survivors": s_total, "survivor_ratio": s_total / n_total,
             "hbm_frac": roof["step_frac"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

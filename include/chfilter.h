@@ -172,6 +172,19 @@ ch_status ch_filter_compact(const double *d_xy, int64_t n, int64_t index_base,
                             const ch_octagon *h_oct, int64_t *d_survivors, int64_t *d_count,
                             void *d_ws, size_t ws_bytes, void *stream);
 
+/* float32 storage (the paper's precision): the same
+ * three calls on AoS float32 points (8 B/pt, 16-byte aligned base).  Each
+ * coordinate is widened to double exactly, so every result equals the
+ * float64 call on the widened array (and the oracle on it). */
+ch_status ch_extremes8_f32(const float *d_xy, int64_t n, int64_t index_base, int flags,
+                           void *d_ext_out, ch_extremes *h_ext, ch_octagon *h_oct,
+                           void *d_ws, size_t ws_bytes, void *stream);
+ch_status ch_filter_compact_f32(const float *d_xy, int64_t n, int64_t index_base,
+                                const ch_octagon *h_oct, int64_t *d_survivors, int64_t *d_count,
+                                void *d_ws, size_t ws_bytes, void *stream);
+ch_status ch_filter_f32(const float *d_xy, int64_t n, int flags, int64_t *d_survivors,
+                        int64_t *h_count, void *d_ws, size_t ws_bytes, void *stream);
+
 /* Synchronize `stream` and copy the workspace result to the host.  Returns
  * CH_ERR_NONFINITE if the last pass saw a non-finite coordinate. */
 ch_status ch_read_result(const void *d_ws, ch_result *h_res, void *stream);

@@ -37,8 +37,8 @@ def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
 
 
 def _points(xy: torch.Tensor) -> torch.Tensor:
-    if not isinstance(xy, torch.Tensor) or xy.dtype != torch.float64:
-        raise TypeError("points must be a float64 torch tensor of shape [n, 2]")
+    if not isinstance(xy, torch.Tensor) or xy.dtype not in (torch.float64, torch.float32):
+        raise TypeError("points must be a float64 (or float32) torch tensor of shape [n, 2]")
     if xy.dim() != 2 or xy.shape[1] != 2 or not xy.is_contiguous():
         raise ValueError("points must be a contiguous [n, 2] tensor (AoS x, y)")
     if not xy.is_cuda:
@@ -48,6 +48,11 @@ def _points(xy: torch.Tensor) -> torch.Tensor:
 
 def _plain(plain: bool) -> int:
     return _lib.CH_PLAIN if plain else _lib.CH_CERTIFIED
+
+
+def _fn(lib, name: str, xy: torch.Tensor):
+    """The float64 entry point, or its _f32 twin for float32 storage."""
+    return getattr(lib, name + "_f32") if xy.dtype == torch.float32 else getattr(lib, name)
 
 
 class Workspace:
@@ -83,7 +88,7 @@ def extremes8(xy: torch.Tensor, ws: Workspace | None = None, index_base: int = 0
     n = xy.shape[0]
     ws = _ws(ws, n, xy.device)
     e, o = Extremes(), Octagon()
-    _lib.check(lib.ch_extremes8(_ptr(xy), n, index_base, _plain(plain), _ptr(ext_out), ctypes.byref(e),
+    _lib.check(_fn(lib, "ch_extremes8", xy)(_ptr(xy), n, index_base, _plain(plain), _ptr(ext_out), ctypes.byref(e),
                                 ctypes.byref(o), ws.ptr, ws.nbytes, _stream(stream)), "ch_extremes8")
     return e, o
 
@@ -93,7 +98,7 @@ def extremes8_async(xy: torch.Tensor, ws: Workspace, index_base: int = 0, plain:
     """Enqueue K1 only (no synchronization)."""
     lib = _lib.load()
     xy = _points(xy)
-    _lib.check(lib.ch_extremes8(_ptr(xy), xy.shape[0], index_base, _plain(plain), _ptr(ext_out), None, None,
+    _lib.check(_fn(lib, "ch_extremes8", xy)(_ptr(xy), xy.shape[0], index_base, _plain(plain), _ptr(ext_out), None, None,
                                 ws.ptr, ws.nbytes, _stream(stream)), "ch_extremes8")
 
 
@@ -117,6 +122,8 @@ def octagon_filter(xy: torch.Tensor, ws: Workspace | None = None, oct_: Octagon 
     words (bit i%32 of word i//32).  Uses the workspace octagon unless oct_."""
     lib = _lib.load()
     xy = _points(xy)
+    if xy.dtype != torch.float64:
+        raise TypeError("octagon_filter takes float64 points")
     n = xy.shape[0]
     ws = _ws(ws, 0, xy.device)
     words = (n + 31) // 32
@@ -136,7 +143,7 @@ def filter_compact(xy: torch.Tensor, ws: Workspace, index_base: int = 0, oct_: O
     n = xy.shape[0]
     if out is None:
         out = torch.empty(max(n, 1), dtype=torch.int64, device=xy.device)
-    _lib.check(lib.ch_filter_compact(_ptr(xy), n, index_base, ctypes.byref(oct_) if oct_ is not None else None,
+    _lib.check(_fn(lib, "ch_filter_compact", xy)(_ptr(xy), n, index_base, ctypes.byref(oct_) if oct_ is not None else None,
                                      _ptr(out), _ptr(count), ws.ptr, ws.nbytes, _stream(stream)),
                "ch_filter_compact")
     return out
@@ -160,7 +167,7 @@ def filter(xy: torch.Tensor, ws: Workspace | None = None, plain: bool = False, o
     if out is None:
         out = torch.empty(max(n, 1), dtype=torch.int64, device=xy.device)
     cnt = ctypes.c_int64(0)
-    _lib.check(lib.ch_filter(_ptr(xy), n, _plain(plain), _ptr(out), ctypes.byref(cnt), ws.ptr, ws.nbytes,
+    _lib.check(_fn(lib, "ch_filter", xy)(_ptr(xy), n, _plain(plain), _ptr(out), ctypes.byref(cnt), ws.ptr, ws.nbytes,
                              _stream(stream)), "ch_filter")
     return out[: cnt.value]
 
@@ -205,6 +212,8 @@ def hull_end_to_end(xy: torch.Tensor, ws: Workspace | None = None, plain: bool =
     on the host.  Returns (hull ids np.ndarray, survivors tensor, Stats)."""
     lib = _lib.load()
     xy = _points(xy)
+    if xy.dtype != torch.float64:
+        raise TypeError("hull_end_to_end takes float64 points")
     n = xy.shape[0]
     ws = _ws(ws, n, xy.device)
     if out is None:

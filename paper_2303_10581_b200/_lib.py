@@ -54,10 +54,14 @@ SIGNATURES = {
     "ch_workspace_init": (ctypes.c_int, [P, SZ, P]),
     "ch_extremes8": (ctypes.c_int, [P, I64, I64, ctypes.c_int, P, ctypes.POINTER(Extremes),
                                     ctypes.POINTER(Octagon), P, SZ, P]),
+    "ch_extremes8_f32": (ctypes.c_int, [P, I64, I64, ctypes.c_int, P, ctypes.POINTER(Extremes),
+                                        ctypes.POINTER(Octagon), P, SZ, P]),
     "ch_combine8": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, SZ, P]),
     "ch_octagon_build": (ctypes.c_int, [ctypes.POINTER(Extremes), ctypes.c_int, ctypes.POINTER(Octagon)]),
     "ch_octagon_filter": (ctypes.c_int, [P, I64, ctypes.POINTER(Octagon), P, P, SZ, P]),
     "ch_filter_compact": (ctypes.c_int, [P, I64, I64, ctypes.POINTER(Octagon), P, P, P, SZ, P]),
+    "ch_filter_compact_f32": (ctypes.c_int, [P, I64, I64, ctypes.POINTER(Octagon), P, P, P, SZ, P]),
+    "ch_filter_f32": (ctypes.c_int, [P, I64, ctypes.c_int, P, ctypes.POINTER(I64), P, SZ, P]),
     "ch_read_result": (ctypes.c_int, [P, ctypes.POINTER(Result), P]),
     "ch_filter": (ctypes.c_int, [P, I64, ctypes.c_int, P, ctypes.POINTER(I64), P, SZ, P]),
     "ch_filter_host": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, ctypes.POINTER(I64), P, SZ, P]),

@@ -32,23 +32,38 @@ constexpr unsigned FULL = 0xffffffffu;
 
 // ----------------------------------------------------------------- layout --
 constexpr int K1_THREADS = 256;
-constexpr int K1_UNROLL = 4;                                   // LDG.256 per thread per chunk
-constexpr long long K1_CHUNK = (long long)K1_THREADS * K1_UNROLL * 2; // points per CTA iteration
+// Point storage: float64 AoS (16 B/pt, the default) or float32 AoS (8 B/pt,
+// the paper's storage precision).  Float coordinates are widened to
+// double exactly, so both run the same fp64 arithmetic.
+template <typename T> struct PtTraits;
+template <> struct PtTraits<double> {
+    using V2 = double2;
+    static constexpr int K1_UNROLL = 4;  // wide loads (2 points each) per thread per chunk
+    static constexpr int K2_STAGES = 3;  // TMA ring depth (32 KB sub-tiles)
+};
+template <> struct PtTraits<float> {
+    using V2 = float2;
+    static constexpr int K1_UNROLL = 8;
+    static constexpr int K2_STAGES = 6;  // 16 KB sub-tiles
+};
+template <typename T> constexpr long long k1_chunk() { return (long long)K1_THREADS * PtTraits<T>::K1_UNROLL * 2; }
 constexpr int K1_MAX_CTAS = 2048;
 
 constexpr int K2_CWARPS = 8;                                   // consumer (compute) warps per CTA
 constexpr int K2_CTHREADS = K2_CWARPS * 32;
-constexpr int K2_PUB_WARP = K2_CWARPS;                         // publisher warp
 constexpr int K2_PROD_WARP = K2_CWARPS + 1;                    // TMA producer warp
 constexpr int K2_THREADS = K2_CTHREADS + 64;
 constexpr int K2_NP = 8;                                       // points per consumer thread per sub-tile
 constexpr long long K2_SUB = (long long)K2_CTHREADS * K2_NP;   // 1024 points (16 KB) per sub-tile
-constexpr int K2_STAGES = 3;                                   // TMA ring depth (sub-tiles)
 constexpr int K2_MAXSUB = 16;                                  // sub-tiles per super-tile (max)
 constexpr int K2_GROUPS = K2_NP * K2_CWARPS;                   // 32-point groups per sub-tile
 constexpr int K2_ENTRIES = K2_MAXSUB * K2_GROUPS;              // ballot words per super-tile
 static_assert(K2_ENTRIES == 4 * K2_CTHREADS, "block scan: 4 entries per consumer thread");
-constexpr size_t K2_DSMEM = (size_t)K2_STAGES * K2_SUB * 16 + 4 * K2_ENTRIES * 4; // stages + bits[2] + scan[2]
+template <typename T>
+constexpr size_t k2_dsmem() // stages + bits[2] + scan[2]
+{
+    return (size_t)PtTraits<T>::K2_STAGES * K2_SUB * sizeof(typename PtTraits<T>::V2) + 4 * K2_ENTRIES * 4;
+}
 constexpr int K2_BAR_BASE = 1;                                 // named barrier ids 1..5
 
 constexpr int K4_THREADS = 256;
@@ -92,17 +107,72 @@ __device__ __forceinline__ void ld128(const double *p, double &a, double &b)
 {
     asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
 }
-// Two consecutive points (32 bytes): one LDG.256 when 32-byte aligned,
-// else two LDG.128.
-template <bool A32>
-__device__ __forceinline__ void ld2pts(const double *p, double &a, double &b, double &c, double &d)
+__device__ __forceinline__ void ld128f(const float *p, float &a, float &b, float &c, float &d)
 {
-    if (A32) {
-        ld256(p, a, b, c, d);
-    } else {
-        ld128(p, a, b);
-        ld128(p + 2, c, d);
-    }
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld64f(const float *p, float &a, float &b)
+{
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(a), "=f"(b) : "l"(p));
+}
+// Two consecutive points as doubles: one wide load (LDG.256 for double,
+// LDG.128 for float) when VEC (the pair is aligned to its size), else two.
+template <typename T, bool VEC>
+__device__ __forceinline__ void ld2pts(const T *p, double &a, double &b, double &c, double &d);
+template <>
+__device__ __forceinline__ void ld2pts<double, true>(const double *p, double &a, double &b, double &c, double &d)
+{
+    ld256(p, a, b, c, d);
+}
+template <>
+__device__ __forceinline__ void ld2pts<double, false>(const double *p, double &a, double &b, double &c, double &d)
+{
+    ld128(p, a, b);
+    ld128(p + 2, c, d);
+}
+template <>
+__device__ __forceinline__ void ld2pts<float, true>(const float *p, double &a, double &b, double &c, double &d)
+{
+    float fa, fb, fc, fd;
+    ld128f(p, fa, fb, fc, fd);
+    a = fa, b = fb, c = fc, d = fd; // exact widening
+}
+template <>
+__device__ __forceinline__ void ld2pts<float, false>(const float *p, double &a, double &b, double &c, double &d)
+{
+    float fa, fb, fc, fd;
+    ld64f(p, fa, fb);
+    ld64f(p + 2, fc, fd);
+    a = fa, b = fb, c = fc, d = fd;
+}
+// Two consecutive points in their storage type (widened at use).
+template <typename T, bool VEC>
+__device__ __forceinline__ void ld2raw(const T *p, T (&r)[4]);
+template <>
+__device__ __forceinline__ void ld2raw<double, true>(const double *p, double (&r)[4]) { ld256(p, r[0], r[1], r[2], r[3]); }
+template <>
+__device__ __forceinline__ void ld2raw<double, false>(const double *p, double (&r)[4])
+{
+    ld128(p, r[0], r[1]);
+    ld128(p + 2, r[2], r[3]);
+}
+template <>
+__device__ __forceinline__ void ld2raw<float, true>(const float *p, float (&r)[4]) { ld128f(p, r[0], r[1], r[2], r[3]); }
+template <>
+__device__ __forceinline__ void ld2raw<float, false>(const float *p, float (&r)[4])
+{
+    ld64f(p, r[0], r[1]);
+    ld64f(p + 2, r[2], r[3]);
+}
+// One point as doubles.
+__device__ __forceinline__ void ld1pt(const double *xy, long long i, double &x, double &y) { ld128(xy + 2 * i, x, y); }
+__device__ __forceinline__ void ld1pt(const float *xy, long long i, double &x, double &y)
+{
+    float fx, fy;
+    ld64f(xy + 2 * i, fx, fy);
+    x = fx, y = fy;
 }
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p)
 {
@@ -172,31 +242,55 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned
 }
 
 // ===================================================================== K1 ==
-// One pass over the points: per-thread running extremes (walking indices
-// downward, so ">=" keeps the lowest index on ties), warp shuffles, CTA
-// partials, and an atomic ticket: the last CTA combines all partials (max
-// key, then lowest index: order independent, R2), builds the octagon on the
-// device and resets the ticket.  Non-finite detection: acc += x*0 (exact 0
-// for finite x, NaN otherwise) via DFMA.
+// One pass over the points.  Each thread keeps running extremes (key, global
+// index) for the 8 slots, walking indices downward.  Per point: 2 DADD (the
+// x+y, x-y keys), 8 compares OR-ed into one predicate, and only if some key
+// reaches its running best (rare after the first few chunks) a per-lane
+// update with the exact (key, lowest index) rule.  Every K1_SHARE chunks the
+// warp shares its best per slot (so thresholds tighten 32x).  Then warp
+// shuffles, CTA partials, and an atomic ticket: the last CTA combines all
+// partials (best key, then lowest index: order independent, R2) and builds
+// the octagon.  Non-finite detection: acc += x*0 (exact 0 for finite x,
+// NaN otherwise) via DFMA.
+constexpr int K1_SHARE = 16;
 struct Best {
     double v[8];
-    unsigned c[8];
+    long long i[8];
 };
 
-__device__ __forceinline__ void k1_update(Best &b, double x, double y, unsigned code, double &acc)
+__device__ __forceinline__ void reduce_pair(int k, double &v, long long &i, double w, long long j);
+
+__device__ __forceinline__ void k1_slow_update(Best &b, double x, double y, double s, double d, long long gi)
 {
-    double s = __dadd_rn(x, y);
-    double d = __dsub_rn(x, y);
-    if (x >= b.v[0]) { b.v[0] = x; b.c[0] = code; }
-    if (s >= b.v[1]) { b.v[1] = s; b.c[1] = code; }
-    if (y >= b.v[2]) { b.v[2] = y; b.c[2] = code; }
-    if (d <= b.v[3]) { b.v[3] = d; b.c[3] = code; }
-    if (x <= b.v[4]) { b.v[4] = x; b.c[4] = code; }
-    if (s <= b.v[5]) { b.v[5] = s; b.c[5] = code; }
-    if (y <= b.v[6]) { b.v[6] = y; b.c[6] = code; }
-    if (d >= b.v[7]) { b.v[7] = d; b.c[7] = code; }
+    const double key[8] = {x, s, y, d, x, s, y, d};
+#pragma unroll
+    for (int k = 0; k < 8; k++)
+        reduce_pair(k, b.v[k], b.i[k], key[k], gi);
+}
+
+__device__ __forceinline__ void k1_update(Best &b, double x, double y, long long gi, double &acc)
+{
+    const double s = __dadd_rn(x, y);
+    const double d = __dsub_rn(x, y);
+    const bool t = (x >= b.v[0]) | (s >= b.v[1]) | (y >= b.v[2]) | (d <= b.v[3]) | (x <= b.v[4]) |
+                   (s <= b.v[5]) | (y <= b.v[6]) | (d >= b.v[7]);
+    if (t)
+        k1_slow_update(b, x, y, s, d, gi);
     acc = __fma_rn(x, 0.0, acc);
     acc = __fma_rn(y, 0.0, acc);
+}
+
+__device__ __forceinline__ void k1_warp_share(Best &b)
+{
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double w = __shfl_xor_sync(FULL, b.v[k], off);
+            const long long j = __shfl_xor_sync(FULL, b.i[k], off);
+            reduce_pair(k, b.v[k], b.i[k], w, j);
+        }
+    }
 }
 
 __device__ __forceinline__ void reduce_pair(int k, double &v, long long &i, double w, long long j)
@@ -251,7 +345,8 @@ __device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o
     __syncthreads();
 }
 
-__device__ void k1_finalize(const double *__restrict__ xy, long long index_base, int flags,
+template <typename T>
+__device__ void k1_finalize(const T *__restrict__ xy, long long index_base, int flags,
                             WsHeader *hdr, const Partial *parts, int nparts, void *ext_out)
 {
     // Called by every thread of the last CTA.
@@ -297,8 +392,8 @@ __device__ void k1_finalize(const double *__restrict__ xy, long long index_base,
             reduce_pair(k, bv, bi, s_v[w][k], s_i[w][k]);
         const long long loc = bi - index_base;
         s_e.idx[k] = bi;
-        s_e.x[k] = xy[2 * loc];
-        s_e.y[k] = xy[2 * loc + 1];
+        s_e.x[k] = (double)xy[2 * loc];
+        s_e.y[k] = (double)xy[2 * loc + 1];
     }
     __syncthreads();
     build_octagon_cta(s_e, flags, s_o);
@@ -324,32 +419,35 @@ __device__ void k1_finalize(const double *__restrict__ xy, long long index_base,
     }
 }
 
-template <bool A32>
-__global__ void __launch_bounds__(K1_THREADS, 4)
-k1_extremes8(const double *__restrict__ xy, long long n, long long index_base, int flags,
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(K1_THREADS, 3)
+k1_extremes8(const T *__restrict__ xy, long long n, long long index_base, int flags,
              WsHeader *hdr, Partial *parts, void *ext_out)
 {
+    constexpr int K1_UNROLL = PtTraits<T>::K1_UNROLL;
+    constexpr long long K1_CHUNK = k1_chunk<T>();
     const int tid = threadIdx.x;
     Best b;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         b.v[k] = chf::slot_is_max(k) ? -CH_INF : CH_INF;
-        b.c[k] = 0xffffffffu;
+        b.i[k] = LLONG_MAX;
     }
     double acc = 0.0;
     const long long nchunks = (n + K1_CHUNK - 1) / K1_CHUNK;
-    for (long long c = nchunks - 1 - blockIdx.x; c >= 0; c -= gridDim.x) {
+    int it = 0;
+    for (long long c = nchunks - 1 - blockIdx.x; c >= 0; c -= gridDim.x, it++) {
         const long long base = c * K1_CHUNK;
-        const unsigned cc = (unsigned)(c * K1_UNROLL);
+        const long long gbase = index_base + base + 2 * tid;
         if (base + K1_CHUNK <= n) {
-            double v[K1_UNROLL][4];
+            T v[K1_UNROLL][4];
 #pragma unroll
             for (int u = 0; u < K1_UNROLL; u++)
-                ld2pts<A32>(xy + 2 * (base + 2 * ((long long)u * K1_THREADS + tid)), v[u][0], v[u][1], v[u][2], v[u][3]);
+                ld2raw<T, VEC>(xy + 2 * (base + 2 * ((long long)u * K1_THREADS + tid)), v[u]);
 #pragma unroll
             for (int u = K1_UNROLL - 1; u >= 0; u--) {
-                k1_update(b, v[u][2], v[u][3], ((cc + u) << 1) | 1u, acc);
-                k1_update(b, v[u][0], v[u][1], ((cc + u) << 1), acc);
+                k1_update(b, (double)v[u][2], (double)v[u][3], gbase + 2 * u * K1_THREADS + 1, acc);
+                k1_update(b, (double)v[u][0], (double)v[u][1], gbase + 2 * u * K1_THREADS, acc);
             }
         } else {
             for (int u = K1_UNROLL - 1; u >= 0; u--) {
@@ -357,27 +455,21 @@ k1_extremes8(const double *__restrict__ xy, long long n, long long index_base, i
                 for (int h = 1; h >= 0; h--) {
                     if (p + h < n) {
                         double x, y;
-                        ld128(xy + 2 * (p + h), x, y);
-                        k1_update(b, x, y, ((cc + u) << 1) | (unsigned)h, acc);
+                        ld1pt(xy, p + h, x, y);
+                        k1_update(b, x, y, index_base + p + h, acc);
                     }
                 }
             }
         }
+        if ((it & (K1_SHARE - 1)) == 0)
+            k1_warp_share(b); // uniform: every lane of the CTA runs the same iterations
     }
-    // code -> local index
     double v[8];
     long long id[8];
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         v[k] = b.v[k];
-        if (b.c[k] == 0xffffffffu) {
-            id[k] = LLONG_MAX;
-        } else {
-            unsigned q = b.c[k] >> 1, h = b.c[k] & 1u;
-            long long c = q / K1_UNROLL;
-            unsigned u = q % K1_UNROLL;
-            id[k] = index_base + c * K1_CHUNK + 2 * ((long long)u * K1_THREADS + tid) + h;
-        }
+        id[k] = b.i[k];
     }
     __shared__ double s_v[K1_THREADS / 32][8];
     __shared__ long long s_i[K1_THREADS / 32][8];
@@ -674,20 +766,23 @@ __device__ __forceinline__ void bar_arrive(int id, int nthreads)
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+template <typename T>
 __global__ void __launch_bounds__(K2_THREADS, 2)
-k2_filter_compact(const double *__restrict__ xy, long long n, long long index_base,
+k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
                   const ch_octagon *__restrict__ oct, WsHeader *hdr,
                   unsigned long long *status, long long *__restrict__ out,
                   long long *d_count, unsigned nsuper, int subs)
 {
     extern __shared__ __align__(128) unsigned char dsm[];
-    double2 *stage = (double2 *)dsm;                                        // [K2_STAGES][K2_SUB]
-    unsigned *bits = (unsigned *)(dsm + (size_t)K2_STAGES * K2_SUB * 16);  // [2][K2_ENTRIES]
+    using V2 = typename PtTraits<T>::V2;
+    constexpr int K2_STAGES = PtTraits<T>::K2_STAGES;
+    V2 *stage = (V2 *)dsm;                                                        // [K2_STAGES][K2_SUB]
+    unsigned *bits = (unsigned *)(dsm + (size_t)K2_STAGES * K2_SUB * sizeof(V2)); // [2][K2_ENTRIES]
     int *gscan = (int *)(bits + 2 * K2_ENTRIES);                            // [2][K2_ENTRIES]
     __shared__ SOct so;
     __shared__ __align__(8) unsigned long long s_full[K2_STAGES], s_empty[K2_STAGES];
     __shared__ unsigned s_desc_super[K2_STAGES];
-    __shared__ int s_desc_j[K2_STAGES], s_desc_nsub[K2_STAGES];
+    __shared__ int s_desc_j[K2_STAGES], s_desc_nsub[K2_STAGES], s_desc_copied[K2_STAGES];
     __shared__ int s_wsum[K2_CWARPS];
     __shared__ int s_total[2];
     __shared__ unsigned s_tile[2];
@@ -739,11 +834,16 @@ k2_filter_compact(const double *__restrict__ xy, long long n, long long index_ba
                 }
                 const long long base = (long long)p_super * super_pts + (long long)p_j * K2_SUB;
                 const unsigned cnt = (unsigned)min(K2_SUB, n - base);
+                // bulk copies move multiples of 16 bytes: an odd float tail
+                // point is read from global memory by its consumer thread
+                const unsigned copied = (cnt * (unsigned)sizeof(V2)) % 16u ? cnt - 1 : cnt;
                 s_desc_super[st] = p_super;
                 s_desc_j[st] = p_j;
                 s_desc_nsub[st] = p_nsub;
-                mbar_expect_tx(&s_full[st], cnt * 16u);
-                tma_load_1d(stage + (size_t)st * K2_SUB, xy + 2 * base, cnt * 16u, &s_full[st]);
+                s_desc_copied[st] = (int)copied;
+                mbar_expect_tx(&s_full[st], copied * (unsigned)sizeof(V2));
+                if (copied > 0)
+                    tma_load_1d(stage + (size_t)st * K2_SUB, xy + 2 * base, copied * (unsigned)sizeof(V2), &s_full[st]);
                 if (++p_j == p_nsub) {
                     p_super = p_next;
                     p_next = p_super < nsuper ? atomicAdd(&hdr->k2_claim, 1u) : TILE_DONE;
@@ -794,15 +894,19 @@ k2_filter_compact(const double *__restrict__ xy, long long n, long long index_ba
                 bar_sync(K2_BAR_BASE + 4, K2_CTHREADS); // all warps done with buffer b
             }
             const long long base = (long long)sup * super_pts + (long long)j * K2_SUB;
-            const double2 *sp = stage + (size_t)st * K2_SUB;
+            const V2 *sp = stage + (size_t)st * K2_SUB;
+            const int copied = s_desc_copied[st];
             double px[K2_NP], py[K2_NP];
             unsigned valid = 0;
 #pragma unroll
             for (int u = 0; u < K2_NP; u++) {
-                double2 v = sp[u * K2_CTHREADS + tid];
-                px[u] = v.x;
-                py[u] = v.y;
-                valid |= (base + u * K2_CTHREADS + tid < n ? 1u : 0u) << u;
+                const int q = u * K2_CTHREADS + tid;
+                const V2 v = sp[q];
+                px[u] = (double)v.x; // exact widening for float storage
+                py[u] = (double)v.y;
+                if (q >= copied && base + q < n)
+                    ld1pt(xy, base + q, px[u], py[u]); // odd float tail point
+                valid |= (base + q < n ? 1u : 0u) << u;
             }
             __syncwarp();
             if (lane == 0)
@@ -1004,8 +1108,9 @@ ch_status cuda_check(const char *what)
 
 struct DevInfo {
     int sms = 0;
-    int k1_per_sm = 0;
-    int k2_per_sm = 0;
+    int k1_per_sm = 0;  // same for every instantiation (launch bounds 256 x 4)
+    int k2_per_sm_d = 0; // double points
+    int k2_per_sm_f = 0; // float points
 };
 
 DevInfo dev_info()
@@ -1016,12 +1121,19 @@ DevInfo dev_info()
     cudaGetDevice(&dev);
     if (dev != cached_dev) {
         cudaDeviceGetAttribute(&info.sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k1_per_sm, k1_extremes8<true>, K1_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k1_per_sm, k1_extremes8<double, true>, K1_THREADS, 0);
         if (info.k1_per_sm < 1)
             info.k1_per_sm = 1;
-        cudaFuncSetAttribute(k2_filter_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_DSMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k2_per_sm, k2_filter_compact, K2_THREADS, K2_DSMEM);
-        info.k2_per_sm = std::max(1, info.k2_per_sm);
+        cudaFuncSetAttribute(k2_filter_compact<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)k2_dsmem<double>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k2_per_sm_d, k2_filter_compact<double>, K2_THREADS,
+                                                      k2_dsmem<double>());
+        info.k2_per_sm_d = std::max(1, info.k2_per_sm_d);
+        cudaFuncSetAttribute(k2_filter_compact<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)k2_dsmem<float>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k2_per_sm_f, k2_filter_compact<float>, K2_THREADS,
+                                                      k2_dsmem<float>());
+        info.k2_per_sm_f = std::max(1, info.k2_per_sm_f);
         cached_dev = dev;
     }
     return info;
@@ -1038,7 +1150,8 @@ ch_status check_ws(const void *d_ws, size_t ws_bytes, long long n)
     return CH_OK;
 }
 
-ch_status check_points(const double *d_xy, long long n)
+template <typename T>
+ch_status check_points(const T *d_xy, long long n)
 {
     if (n < 0)
         return fail(CH_ERR_INVALID_ARG, "n < 0");
@@ -1060,21 +1173,24 @@ inline unsigned long long *status_of(void *d_ws)
     return (unsigned long long *)((char *)d_ws + WS_HEADER + WS_PARTIALS);
 }
 
-ch_status launch_k1(const double *d_xy, long long n, long long index_base, int flags, void *d_ext_out,
+template <typename T>
+ch_status launch_k1(const T *d_xy, long long n, long long index_base, int flags, void *d_ext_out,
                     void *d_ws, cudaStream_t st)
 {
     DevInfo di = dev_info();
+    constexpr long long K1_CHUNK = k1_chunk<T>();
     long long nchunks = (n + K1_CHUNK - 1) / K1_CHUNK;
     long long g = std::min<long long>((long long)di.sms * di.k1_per_sm, nchunks);
     g = std::min<long long>(g, K1_MAX_CTAS);
     if (g < 1)
         g = 1;
-    if (((uintptr_t)d_xy & 31u) == 0)
-        k1_extremes8<true><<<(unsigned)g, K1_THREADS, 0, st>>>(d_xy, n, index_base, flags, hdr_of(d_ws),
-                                                                parts_of(d_ws), d_ext_out);
+    // wide loads need the pair of points aligned to its size (32 B / 16 B)
+    if (((uintptr_t)d_xy & (4 * sizeof(T) - 1)) == 0)
+        k1_extremes8<T, true><<<(unsigned)g, K1_THREADS, 0, st>>>(d_xy, n, index_base, flags, hdr_of(d_ws),
+                                                                   parts_of(d_ws), d_ext_out);
     else
-        k1_extremes8<false><<<(unsigned)g, K1_THREADS, 0, st>>>(d_xy, n, index_base, flags, hdr_of(d_ws),
-                                                                 parts_of(d_ws), d_ext_out);
+        k1_extremes8<T, false><<<(unsigned)g, K1_THREADS, 0, st>>>(d_xy, n, index_base, flags, hdr_of(d_ws),
+                                                                    parts_of(d_ws), d_ext_out);
     return cuda_check("k1_extremes8");
 }
 
@@ -1095,21 +1211,32 @@ ch_status stage_octagon(const ch_octagon *h_oct, void *d_ws, cudaStream_t st, co
     return CH_OK;
 }
 
-ch_status launch_k2(const double *d_xy, long long n, long long index_base, const ch_octagon *d_oct,
+template <typename T>
+ch_status launch_k2(const T *d_xy, long long n, long long index_base, const ch_octagon *d_oct,
                     long long *d_surv, long long *d_count, void *d_ws, cudaStream_t st)
 {
     DevInfo di = dev_info();
-    long long resident = (long long)di.sms * di.k2_per_sm;
+    long long resident = (long long)di.sms * (sizeof(T) == 8 ? di.k2_per_sm_d : di.k2_per_sm_f);
     long long nsub_total = (n + K2_SUB - 1) / K2_SUB;
     // aim for >= 8 super-tiles per CTA (load balance), <= K2_MAXSUB sub-tiles each
     long long subs = (nsub_total + resident * 8 - 1) / (resident * 8);
     subs = std::max<long long>(1, std::min<long long>(subs, K2_MAXSUB));
     long long nsuper = (nsub_total + subs - 1) / subs;
     long long grid = std::max<long long>(1, std::min<long long>(resident, nsuper));
-    k2_filter_compact<<<(unsigned)grid, K2_THREADS, K2_DSMEM, st>>>(
+    k2_filter_compact<T><<<(unsigned)grid, K2_THREADS, k2_dsmem<T>(), st>>>(
         d_xy, n, index_base, d_oct, hdr_of(d_ws), status_of(d_ws), d_surv, d_count, (unsigned)nsuper, (int)subs);
     return cuda_check("k2_filter_compact");
 }
+
+template <typename T>
+ch_status extremes8_impl(const T *d_xy, int64_t n, int64_t index_base, int flags, void *d_ext_out,
+                         ch_extremes *h_ext, ch_octagon *h_oct, void *d_ws, size_t ws_bytes, void *stream);
+template <typename T>
+ch_status filter_compact_impl(const T *d_xy, int64_t n, int64_t index_base, const ch_octagon *h_oct,
+                              int64_t *d_survivors, int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
+template <typename T>
+ch_status filter_impl(const T *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *h_count, void *d_ws,
+                      size_t ws_bytes, void *stream);
 
 } // namespace
 
@@ -1174,8 +1301,12 @@ ch_status ch_read_result(const void *d_ws, ch_result *h_res, void *stream)
     return CH_OK;
 }
 
-ch_status ch_extremes8(const double *d_xy, int64_t n, int64_t index_base, int flags, void *d_ext_out,
-                       ch_extremes *h_ext, ch_octagon *h_oct, void *d_ws, size_t ws_bytes, void *stream)
+} // extern "C"
+
+namespace {
+template <typename T>
+ch_status extremes8_impl(const T *d_xy, int64_t n, int64_t index_base, int flags, void *d_ext_out,
+                         ch_extremes *h_ext, ch_octagon *h_oct, void *d_ws, size_t ws_bytes, void *stream)
 {
     ch_status s = check_points(d_xy, n);
     if (s != CH_OK)
@@ -1195,6 +1326,55 @@ ch_status ch_extremes8(const double *d_xy, int64_t n, int64_t index_base, int fl
         return ch_read_result(d_ws, &r, stream);
     }
     return CH_OK;
+}
+
+template <typename T>
+ch_status filter_compact_impl(const T *d_xy, int64_t n, int64_t index_base, const ch_octagon *h_oct,
+                              int64_t *d_survivors, int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream)
+{
+    ch_status s = check_points(d_xy, n);
+    if (s != CH_OK)
+        return s;
+    if (!d_survivors)
+        return fail(CH_ERR_INVALID_ARG, "d_survivors is NULL");
+    if ((s = check_ws(d_ws, ws_bytes, n)) != CH_OK)
+        return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const ch_octagon *d_oct;
+    if ((s = stage_octagon(h_oct, d_ws, st, &d_oct)) != CH_OK)
+        return s;
+    return launch_k2(d_xy, n, index_base, d_oct, (long long *)d_survivors, (long long *)d_count, d_ws, st);
+}
+
+template <typename T>
+ch_status filter_impl(const T *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *h_count, void *d_ws,
+                      size_t ws_bytes, void *stream)
+{
+    ch_status s = extremes8_impl(d_xy, n, 0, flags, nullptr, nullptr, nullptr, d_ws, ws_bytes, stream);
+    if (s != CH_OK)
+        return s;
+    if ((s = filter_compact_impl(d_xy, n, 0, nullptr, d_survivors, nullptr, d_ws, ws_bytes, stream)) != CH_OK)
+        return s;
+    ch_result r;
+    s = ch_read_result(d_ws, &r, stream);
+    if (h_count)
+        *h_count = r.count;
+    return s;
+}
+} // namespace
+
+extern "C" {
+
+ch_status ch_extremes8(const double *d_xy, int64_t n, int64_t index_base, int flags, void *d_ext_out,
+                       ch_extremes *h_ext, ch_octagon *h_oct, void *d_ws, size_t ws_bytes, void *stream)
+{
+    return extremes8_impl(d_xy, n, index_base, flags, d_ext_out, h_ext, h_oct, d_ws, ws_bytes, stream);
+}
+
+ch_status ch_extremes8_f32(const float *d_xy, int64_t n, int64_t index_base, int flags, void *d_ext_out,
+                           ch_extremes *h_ext, ch_octagon *h_oct, void *d_ws, size_t ws_bytes, void *stream)
+{
+    return extremes8_impl(d_xy, n, index_base, flags, d_ext_out, h_ext, h_oct, d_ws, ws_bytes, stream);
 }
 
 ch_status ch_combine8(const void *d_ext_all, int world, int flags, void *d_ws, size_t ws_bytes, void *stream)
@@ -1232,33 +1412,25 @@ ch_status ch_octagon_filter(const double *d_xy, int64_t n, const ch_octagon *h_o
 ch_status ch_filter_compact(const double *d_xy, int64_t n, int64_t index_base, const ch_octagon *h_oct,
                             int64_t *d_survivors, int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream)
 {
-    ch_status s = check_points(d_xy, n);
-    if (s != CH_OK)
-        return s;
-    if (!d_survivors)
-        return fail(CH_ERR_INVALID_ARG, "d_survivors is NULL");
-    if ((s = check_ws(d_ws, ws_bytes, n)) != CH_OK)
-        return s;
-    cudaStream_t st = (cudaStream_t)stream;
-    const ch_octagon *d_oct;
-    if ((s = stage_octagon(h_oct, d_ws, st, &d_oct)) != CH_OK)
-        return s;
-    return launch_k2(d_xy, n, index_base, d_oct, (long long *)d_survivors, (long long *)d_count, d_ws, st);
+    return filter_compact_impl(d_xy, n, index_base, h_oct, d_survivors, d_count, d_ws, ws_bytes, stream);
+}
+
+ch_status ch_filter_compact_f32(const float *d_xy, int64_t n, int64_t index_base, const ch_octagon *h_oct,
+                                int64_t *d_survivors, int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream)
+{
+    return filter_compact_impl(d_xy, n, index_base, h_oct, d_survivors, d_count, d_ws, ws_bytes, stream);
 }
 
 ch_status ch_filter(const double *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *h_count,
                     void *d_ws, size_t ws_bytes, void *stream)
 {
-    ch_status s = ch_extremes8(d_xy, n, 0, flags, nullptr, nullptr, nullptr, d_ws, ws_bytes, stream);
-    if (s != CH_OK)
-        return s;
-    if ((s = ch_filter_compact(d_xy, n, 0, nullptr, d_survivors, nullptr, d_ws, ws_bytes, stream)) != CH_OK)
-        return s;
-    ch_result r;
-    s = ch_read_result(d_ws, &r, stream);
-    if (h_count)
-        *h_count = r.count;
-    return s;
+    return filter_impl(d_xy, n, flags, d_survivors, h_count, d_ws, ws_bytes, stream);
+}
+
+ch_status ch_filter_f32(const float *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *h_count,
+                        void *d_ws, size_t ws_bytes, void *stream)
+{
+    return filter_impl(d_xy, n, flags, d_survivors, h_count, d_ws, ws_bytes, stream);
 }
 
 ch_status ch_filter_host(const double *h_xy, int64_t n, int flags, double *d_xy_staging, int64_t *d_survivors,

@@ -2,15 +2,14 @@
 set -x
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
 B="python bench.py --no-e2e --no-cpu-baseline"
-for N in 1e9 1e8; do for D in normal circle displaced; do
-  timeout 300 $B --dist $D --n $N --steps ${STEPS:-30} --warmup 3 > gpurun_out/bench_${D}_${N}.json 2>gpurun_out/bench_${D}_${N}.err; echo "bench $D $N rc=$?"
-done; done
+for S in ${STORAGES:-f64 f32}; do for N in 1e9 1e8; do for D in normal circle displaced; do
+  timeout 300 $B --storage $S --dist $D --n $N --steps ${STEPS:-50} --warmup 3 > gpurun_out/bench_${D}_${N}_${S}.json 2>gpurun_out/bench_${D}_${N}_${S}.err; echo "bench $S $D $N rc=$?"
+done; done; done
+timeout 300 python bench.py --no-e2e --no-cpu-baseline --dist normal --n 1e4 --steps 500 --warmup 20 > gpurun_out/bench_normal_1e4_f64.json 2>/dev/null
 python - <<'PY'
 import json,glob
-for f in sorted(glob.glob("gpurun_out/bench_*.json")):
+for f in sorted(glob.glob("gpurun_out/bench_*_f*.json")):
     try: d=json.loads(open(f).read().strip().splitlines()[-1])
     except Exception as e: print(f, "ERR", e); continue
-    r=d["roofline"]; print(f"{d['config']['workload']:28s} {d['value']:8.2f} Gpts/s  step {d['ms_per_step']:.3f} ms  k1 {r['k1_ms']:.3f} ({r['k1_gbs']:.0f} GB/s)  k2 {r['k2_ms']:.3f} ({r['k2_gbs']:.0f} GB/s)  hbm {d['hbm_frac']:.3f}  clk {d['clocks']['sm_mhz']} {d['clocks']['reasons']}")
+    r=d["roofline"]; print(f"{d['config']['workload']:28s} {d['value']:8.2f} Gpts/s  step {d['ms_per_step']*1e3:9.1f} us  k1 {r['k1_ms']:.3f} ({r['k1_gbs']:.0f} GB/s)  k2 {r['k2_ms']:.3f} ({r['k2_gbs']:.0f} GB/s)  hbm {d['hbm_frac']:.3f}  clk {d['clocks']['sm_mhz']} {d['clocks']['reasons']}")
 PY
-timeout 300 python bench.py --no-e2e --no-cpu-baseline --dist normal --n 1e4 --steps 500 --warmup 20 > gpurun_out/bench_normal_1e4.json 2>/dev/null
-python -c "import json; d=json.loads(open('gpurun_out/bench_normal_1e4.json').read().strip().splitlines()[-1]); r=d['roofline']; print('normal_1e4: step %.1f us  k1 %.1f us  k2 %.1f us' % (d['ms_per_step']*1e3, r['k1_ms']*1e3, r['k2_ms']*1e3))"

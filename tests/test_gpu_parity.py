@@ -308,3 +308,36 @@ def test_parity_extreme_scales(scale):
     _, oc = chf.extremes8(torch.tensor(xy, device=DEV))
     assert oc.has_f32 == (1 if scale < 2.0 ** 40 / 0.3 else 0)
     check_against_oracle(torch.tensor(xy, device=DEV), name=f"scale-{scale}")
+
+
+# ------------------------------------------------ float32 storage (f2) ------
+@pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
+@pytest.mark.parametrize("n", [1, 2, 3, 2047, 2048, 2049, 65_537, 1_000_001, 10_000_000])
+def test_parity_f32_storage(dist, n):
+    """float32 points: every result equals the float64 path on the exactly
+    widened coordinates, i.e. the oracle on xy.astype(float64)."""
+    xy32 = synth.points(dist, n, seed=n % 5, device=DEV).float()
+    xy = xy32.double().cpu().numpy()
+    ws = chf.Workspace(n)
+    e, o = chf.extremes8(xy32, ws)
+    surv = chf.filter(xy32, ws).cpu().numpy()
+    want_s, want_idx = oracle.filter_compact(xy)
+    assert np.array_equal(np.array(e.idx[:]), want_idx)
+    wo = oracle.octagon(xy, want_idx)
+    od = chf.octagon_dict(o)
+    for f in ("vx", "vy", "ex", "ey", "thr"):
+        assert np.array_equal(od[f].view(np.int64), wo[f].view(np.int64)), f
+    assert np.array_equal(surv, want_s)
+
+
+def test_f32_ties_degenerate_and_alignment():
+    rng = np.random.default_rng(3)
+    for xy in (rng.integers(-3, 4, size=(50_001, 2)).astype(np.float32),
+               np.full((777, 2), 1.5, np.float32), np.stack([np.arange(5000.0)] * 2, 1).astype(np.float32)):
+        t = torch.tensor(xy, device=DEV)
+        want, _ = oracle.filter_compact(xy.astype(np.float64))
+        assert np.array_equal(chf.filter(t).cpu().numpy(), want)
+    big = synth.points("normal", 1001, seed=0, device=DEV).float()
+    with pytest.raises(chf.CHError) as ei:
+        chf.filter(big[1:])          # 8-byte aligned only
+    assert ei.value.status == 4
