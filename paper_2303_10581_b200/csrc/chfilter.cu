@@ -38,13 +38,15 @@ constexpr int K1_THREADS = 256;
 template <typename T> struct PtTraits;
 template <> struct PtTraits<double> {
     using V2 = double2;
-    static constexpr int K1_UNROLL = 4;  // wide loads (2 points each) per thread per chunk
-    static constexpr int K2_STAGES = 3;  // TMA ring depth (32 KB sub-tiles)
+    static constexpr int K1_UNROLL = 4; // wide loads (2 points each) per thread per chunk
+    static constexpr int K2_NP = 8;     // points per consumer thread per sub-tile (32 KB)
+    static constexpr int K2_STAGES = 3; // TMA ring depth (sub-tiles)
 };
 template <> struct PtTraits<float> {
     using V2 = float2;
     static constexpr int K1_UNROLL = 8;
-    static constexpr int K2_STAGES = 6;  // 16 KB sub-tiles
+    static constexpr int K2_NP = 16;
+    static constexpr int K2_STAGES = 3;
 };
 template <typename T> constexpr long long k1_chunk() { return (long long)K1_THREADS * PtTraits<T>::K1_UNROLL * 2; }
 constexpr int K1_MAX_CTAS = 2048;
@@ -53,16 +55,14 @@ constexpr int K2_CWARPS = 8;                                   // consumer (comp
 constexpr int K2_CTHREADS = K2_CWARPS * 32;
 constexpr int K2_PROD_WARP = K2_CWARPS + 1;                    // TMA producer warp
 constexpr int K2_THREADS = K2_CTHREADS + 64;
-constexpr int K2_NP = 8;                                       // points per consumer thread per sub-tile
-constexpr long long K2_SUB = (long long)K2_CTHREADS * K2_NP;   // 1024 points (16 KB) per sub-tile
-constexpr int K2_MAXSUB = 16;                                  // sub-tiles per super-tile (max)
-constexpr int K2_GROUPS = K2_NP * K2_CWARPS;                   // 32-point groups per sub-tile
-constexpr int K2_ENTRIES = K2_MAXSUB * K2_GROUPS;              // ballot words per super-tile
-static_assert(K2_ENTRIES == 4 * K2_CTHREADS, "block scan: 4 entries per consumer thread");
+constexpr int K2_ENTRIES = 4 * K2_CTHREADS;                    // ballot words per super-tile (block scan: 4/thread)
+template <typename T> constexpr long long k2_sub() { return (long long)K2_CTHREADS * PtTraits<T>::K2_NP; }
+template <typename T> constexpr int k2_groups() { return PtTraits<T>::K2_NP * K2_CWARPS; } // 32-point groups / sub-tile
+template <typename T> constexpr int k2_maxsub() { return K2_ENTRIES / k2_groups<T>(); }   // sub-tiles / super-tile
 template <typename T>
 constexpr size_t k2_dsmem() // stages + bits[2] + scan[2]
 {
-    return (size_t)PtTraits<T>::K2_STAGES * K2_SUB * sizeof(typename PtTraits<T>::V2) + 4 * K2_ENTRIES * 4;
+    return (size_t)PtTraits<T>::K2_STAGES * k2_sub<T>() * sizeof(typename PtTraits<T>::V2) + 4 * K2_ENTRIES * 4;
 }
 constexpr int K2_BAR_BASE = 1;                                 // named barrier ids 1..5
 
@@ -94,7 +94,7 @@ static_assert(sizeof(WsHeader) <= 4096, "header too large");
 constexpr size_t WS_HEADER = 4096;
 constexpr size_t WS_PARTIALS = (size_t)K1_MAX_CTAS * sizeof(Partial);
 
-inline long long ntiles_of(long long n) { return (n + K2_SUB - 1) / K2_SUB; } // >= super-tiles
+inline long long ntiles_of(long long n) { return (n + k2_sub<double>() - 1) / k2_sub<double>(); } // >= super-tiles
 
 // ------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ void ld256(const double *p, double &a, double &b, double &c, double &d)
@@ -166,6 +166,9 @@ __device__ __forceinline__ void ld2raw<float, false>(const float *p, float (&r)[
     ld64f(p, r[0], r[1]);
     ld64f(p + 2, r[2], r[3]);
 }
+// One point in its storage type.
+__device__ __forceinline__ void ld1raw(const double *xy, long long i, double &x, double &y) { ld128(xy + 2 * i, x, y); }
+__device__ __forceinline__ void ld1raw(const float *xy, long long i, float &x, float &y) { ld64f(xy + 2 * i, x, y); }
 // One point as doubles.
 __device__ __forceinline__ void ld1pt(const double *xy, long long i, double &x, double &y) { ld128(xy + 2 * i, x, y); }
 __device__ __forceinline__ void ld1pt(const float *xy, long long i, double &x, double &y)
@@ -568,6 +571,7 @@ struct SOct {
     SEdge e[8];
     FEdge f[8];
     double box[4];
+    float boxf[4]; // float bounds with x >= boxf[0] <=> (double)x >= box[0], etc.
     double cx, cy;
     int nv, degenerate, has_f32;
     int guess[8];
@@ -593,6 +597,10 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.box[1] = o->box[1];
         s.box[2] = o->box[2];
         s.box[3] = o->box[3];
+        s.boxf[0] = chf::f32_up(o->box[0]);
+        s.boxf[1] = chf::f32_down(o->box[1]);
+        s.boxf[2] = chf::f32_up(o->box[2]);
+        s.boxf[3] = chf::f32_down(o->box[3]);
         s.cx = o->cx;
         s.cy = o->cy;
         s.nv = o->nv;
@@ -640,15 +648,19 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
 // points 2' did not settle skips 2' for the next 15 sub-tiles.  Without
 // has_f32 (caller-supplied octagon) stage 3 runs on every edge of every
 // undecided point.
-template <int NP>
-__device__ __forceinline__ unsigned classify(const SOct &s, const double (&px)[NP], const double (&py)[NP],
+template <typename C, int NP>
+__device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], const C (&py)[NP],
                                              unsigned valid, int &guess_mode)
 {
     static_assert(NP <= 32, "one mask bit per point");
     unsigned und = 0;
 #pragma unroll
     for (int i = 0; i < NP; i++) {
-        bool inbox = px[i] >= s.box[0] && px[i] <= s.box[1] && py[i] >= s.box[2] && py[i] <= s.box[3];
+        bool inbox;
+        if constexpr (sizeof(C) == 4) // float storage: the same test on float bounds
+            inbox = px[i] >= s.boxf[0] && px[i] <= s.boxf[1] && py[i] >= s.boxf[2] && py[i] <= s.boxf[3];
+        else
+            inbox = px[i] >= s.box[0] && px[i] <= s.box[1] && py[i] >= s.box[2] && py[i] <= s.box[3];
         und |= (inbox ? 0u : 1u) << i;
     }
     und &= valid;
@@ -660,12 +672,12 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const double (&px)[N
         // 2'. the guessed edge of the point's octant: D_g <= T_g => kept
 #pragma unroll
         for (int i = 0; i < NP; i++) {
-            double dx = __dsub_rn(px[i], s.cx), dy = __dsub_rn(py[i], s.cy);
+            double dx = __dsub_rn((double)px[i], s.cx), dy = __dsub_rn((double)py[i], s.cy);
             bool c = fabs(dx) >= fabs(dy);
             int oct = dy >= 0.0 ? (dx >= 0.0 ? (c ? 0 : 1) : (c ? 3 : 2))
                                 : (dx < 0.0 ? (c ? 4 : 5) : (c ? 7 : 6));
             const SEdge &e = s.e[s.guess[oct]];
-            double D = chf::edge_det(e.ax, e.ay, e.ex, e.ey, px[i], py[i]);
+            double D = chf::edge_det(e.ax, e.ay, e.ex, e.ey, (double)px[i], (double)py[i]);
             keep |= (D > e.thr ? 0u : 1u) << i;
         }
         keep &= und;
@@ -679,31 +691,35 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const double (&px)[N
         // fp32 certification on every edge: OR the sign bits of g_k (any
         // g_k < 0 or -0 => not certified inside) and of h_k (any h_k <= -0
         // => certified outside).  Proof at chf::octagon_edge.
-        float xf[NP], yf[NP];
-        unsigned sg[NP], sh[NP];
+        unsigned in = 0, out = 0;
+        constexpr int CH = NP < 8 ? NP : 8; // points per pass (bounds register use)
 #pragma unroll
-        for (int i = 0; i < NP; i++) {
-            xf[i] = __double2float_rn(px[i]);
-            yf[i] = __double2float_rn(py[i]);
-            sg[i] = 0u;
-            sh[i] = 0u;
-        }
+        for (int c0 = 0; c0 < NP; c0 += CH) {
+            float xf[CH], yf[CH];
+            unsigned sg[CH], sh[CH];
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-            if (k < nv) {
-                const FEdge f = s.f[k];
+            for (int i = 0; i < CH; i++) {
+                xf[i] = (float)px[c0 + i]; // exact for float storage
+                yf[i] = (float)py[c0 + i];
+                sg[i] = 0u;
+                sh[i] = 0u;
+            }
 #pragma unroll
-                for (int i = 0; i < NP; i++) {
-                    sg[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cin)));
-                    sh[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cout)));
+            for (int k = 0; k < 8; k++) {
+                if (k < nv) {
+                    const FEdge f = s.f[k];
+#pragma unroll
+                    for (int i = 0; i < CH; i++) {
+                        sg[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cin)));
+                        sh[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cout)));
+                    }
                 }
             }
-        }
-        unsigned in = 0, out = 0;
 #pragma unroll
-        for (int i = 0; i < NP; i++) {
-            in |= ((~sg[i]) >> 31) << i;
-            out |= (sh[i] >> 31) << i;
+            for (int i = 0; i < CH; i++) {
+                in |= ((~sg[i]) >> 31) << (c0 + i);
+                out |= (sh[i] >> 31) << (c0 + i);
+            }
         }
         keep |= und & out;
         und &= ~(in | out); // certified inside => discarded
@@ -716,7 +732,7 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const double (&px)[N
 #pragma unroll
             for (int i = 0; i < NP; i++) {
                 if ((und >> i) & 1u) {
-                    const double D = chf::edge_det(ax, ay, ex, ey, px[i], py[i]);
+                    const double D = chf::edge_det(ax, ay, ex, ey, (double)px[i], (double)py[i]);
                     disc &= ~((D > thr ? 0u : 1u) << i);
                 }
             }
@@ -728,7 +744,7 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const double (&px)[N
         const double ax = s.e[k].ax, ay = s.e[k].ay, ex = s.e[k].ex, ey = s.e[k].ey, thr = s.e[k].thr;
 #pragma unroll
         for (int i = 0; i < NP; i++) {
-            double D = chf::edge_det(ax, ay, ex, ey, px[i], py[i]);
+            double D = chf::edge_det(ax, ay, ex, ey, (double)px[i], (double)py[i]);
             disc &= ~((D > thr ? 0u : 1u) << i);
         }
     }
@@ -776,6 +792,9 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
     extern __shared__ __align__(128) unsigned char dsm[];
     using V2 = typename PtTraits<T>::V2;
     constexpr int K2_STAGES = PtTraits<T>::K2_STAGES;
+    constexpr int K2_NP = PtTraits<T>::K2_NP;
+    constexpr long long K2_SUB = k2_sub<T>();
+    constexpr int K2_GROUPS = k2_groups<T>();
     V2 *stage = (V2 *)dsm;                                                        // [K2_STAGES][K2_SUB]
     unsigned *bits = (unsigned *)(dsm + (size_t)K2_STAGES * K2_SUB * sizeof(V2)); // [2][K2_ENTRIES]
     int *gscan = (int *)(bits + 2 * K2_ENTRIES);                            // [2][K2_ENTRIES]
@@ -896,22 +915,28 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
             const long long base = (long long)sup * super_pts + (long long)j * K2_SUB;
             const V2 *sp = stage + (size_t)st * K2_SUB;
             const int copied = s_desc_copied[st];
-            double px[K2_NP], py[K2_NP];
-            unsigned valid = 0;
+            T px[K2_NP], py[K2_NP]; // storage precision; widened exactly where fp64 is needed
+            unsigned valid = (1u << K2_NP) - 1u;
 #pragma unroll
             for (int u = 0; u < K2_NP; u++) {
-                const int q = u * K2_CTHREADS + tid;
-                const V2 v = sp[q];
-                px[u] = (double)v.x; // exact widening for float storage
-                py[u] = (double)v.y;
-                if (q >= copied && base + q < n)
-                    ld1pt(xy, base + q, px[u], py[u]); // odd float tail point
-                valid |= (base + q < n ? 1u : 0u) << u;
+                const V2 v = sp[u * K2_CTHREADS + tid];
+                px[u] = v.x;
+                py[u] = v.y;
+            }
+            if (copied < (int)K2_SUB) { // the partial last sub-tile (uniform branch)
+                valid = 0;
+#pragma unroll
+                for (int u = 0; u < K2_NP; u++) {
+                    const int q = u * K2_CTHREADS + tid;
+                    if (q >= copied && base + q < n)
+                        ld1raw(xy, base + q, px[u], py[u]); // odd float tail point
+                    valid |= (base + q < n ? 1u : 0u) << u;
+                }
             }
             __syncwarp();
             if (lane == 0)
                 mbar_arrive(&s_empty[st]); // this warp is done with stage st
-            const unsigned keep = so.degenerate ? valid : classify<K2_NP>(so, px, py, valid, guess_mode);
+            const unsigned keep = so.degenerate ? valid : classify<T, K2_NP>(so, px, py, valid, guess_mode);
             unsigned *bw = bits + b * K2_ENTRIES + j * K2_GROUPS;
 #pragma unroll
             for (int u = 0; u < K2_NP; u++) {
@@ -1217,10 +1242,11 @@ ch_status launch_k2(const T *d_xy, long long n, long long index_base, const ch_o
 {
     DevInfo di = dev_info();
     long long resident = (long long)di.sms * (sizeof(T) == 8 ? di.k2_per_sm_d : di.k2_per_sm_f);
+    constexpr long long K2_SUB = k2_sub<T>();
     long long nsub_total = (n + K2_SUB - 1) / K2_SUB;
-    // aim for >= 8 super-tiles per CTA (load balance), <= K2_MAXSUB sub-tiles each
+    // aim for >= 8 super-tiles per CTA (load balance), <= k2_maxsub sub-tiles each
     long long subs = (nsub_total + resident * 8 - 1) / (resident * 8);
-    subs = std::max<long long>(1, std::min<long long>(subs, K2_MAXSUB));
+    subs = std::max<long long>(1, std::min<long long>(subs, (long long)k2_maxsub<T>()));
     long long nsuper = (nsub_total + subs - 1) / subs;
     long long grid = std::max<long long>(1, std::min<long long>(resident, nsuper));
     k2_filter_compact<T><<<(unsigned)grid, K2_THREADS, k2_dsmem<T>(), st>>>(
