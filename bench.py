@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--dist", choices=["normal", "circle", "displaced"], default="normal")
-    ap.add_argument("--n", type=float, default=1e9, help="points (total for strong scaling, per GPU for weak)")
+    ap.add_argument("--points", "--n", dest="n", type=float, default=1e9,
+                    help="points (total for strong scaling, per GPU for weak)")
     ap.add_argument("--p", type=float, default=0.1)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
@@ -212,10 +213,26 @@ def run_ours(a):
     rank, world, local = env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU path)")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # CH_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo collectives -- only
+    # to exercise the N > 1 code path on a 1-GPU box; never a measurement.
+    share = os.environ.get("CH_BENCH_SHARE_GPU") == "1"
+    gpu = 0 if share else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def reduce_host(v, op):
+        """All-reduce a python scalar over ranks (device tensor for NCCL)."""
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64 if isinstance(v, float) else torch.int64,
+                         device="cpu" if share else dev)
+        dist.all_reduce(t, op=op)
+        return t.item()
     n_arg = int(a.n)
     n_total = n_arg if a.scaling == "strong" else n_arg * world
     lo, hi = chdist.shard_range(n_total, world, rank)
@@ -299,12 +316,8 @@ def run_ours(a):
     res = chf.read_result(ws)
     s_local = int(res.count)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        st = torch.tensor([s_local], dtype=torch.int64, device=dev)
-        dist.all_reduce(st)
-        s_total = int(st.item())
+        total_ms = float(reduce_host(float(total_ms), dist.ReduceOp.MAX))
+        s_total = int(reduce_host(int(s_local), dist.ReduceOp.SUM))
     else:
         s_total = s_local
     ms_step = total_ms / K
@@ -368,9 +381,7 @@ def run_ours(a):
                 d2h = e2e_step()
             e_e.record(stream)
             torch.cuda.synchronize()
-            t = torch.tensor([e_s.elapsed_time(e_e) / a.e2e_steps], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+            e2e_ms = float(reduce_host(float(e_s.elapsed_time(e_e) / a.e2e_steps), dist.ReduceOp.MAX))
         e2e = {"value": n_total / (e2e_ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": 16 * n_local, "d2h_bytes_per_step": int(d2h),
                "api": "ch_filter_host (C ABI, pinned host input)" if world == 1 else "DistFilter + host copies"}

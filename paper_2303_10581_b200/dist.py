@@ -54,9 +54,11 @@ def empty_record(device) -> torch.Tensor:
 def _all_gather_flat(out: torch.Tensor, inp: torch.Tensor, group=None) -> torch.Tensor:
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, inp, group=group)   # one NCCL all-gather, in place
-    else:  # gloo (CPU tests)
-        parts = list(out.chunk(dist.get_world_size(group)))
-        dist.all_gather(parts, inp, group=group)
+    else:  # gloo (CPU tests, and single-GPU multi-rank tests: staged through host memory)
+        hin = inp.cpu()
+        parts = list(torch.empty(out.numel(), dtype=out.dtype).chunk(dist.get_world_size(group)))
+        dist.all_gather(parts, hin, group=group)
+        out.copy_(torch.cat(parts))
     return out
 
 

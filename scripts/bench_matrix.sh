@@ -3,9 +3,9 @@ set -x
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
 B="python bench.py --no-e2e --no-cpu-baseline"
 for S in ${STORAGES:-f64 f32}; do for N in 1e9 1e8; do for D in normal circle displaced; do
-  timeout 300 $B --storage $S --dist $D --n $N --steps ${STEPS:-50} --warmup 3 > gpurun_out/bench_${D}_${N}_${S}.json 2>gpurun_out/bench_${D}_${N}_${S}.err; echo "bench $S $D $N rc=$?"
+  timeout 300 $B --storage $S --dist $D --points $N --steps ${STEPS:-50} --warmup 3 > gpurun_out/bench_${D}_${N}_${S}.json 2>gpurun_out/bench_${D}_${N}_${S}.err; echo "bench $S $D $N rc=$?"
 done; done; done
-timeout 300 python bench.py --no-e2e --no-cpu-baseline --dist normal --n 1e4 --steps 500 --warmup 20 > gpurun_out/bench_normal_1e4_f64.json 2>/dev/null
+timeout 300 python bench.py --no-e2e --no-cpu-baseline --dist normal --points 1e4 --steps 500 --warmup 20 > gpurun_out/bench_normal_1e4_f64.json 2>/dev/null
 python - <<'PY'
 import json,glob
 for f in sorted(glob.glob("gpurun_out/bench_*_f*.json")):

@@ -341,3 +341,57 @@ def test_f32_ties_degenerate_and_alignment():
     with pytest.raises(chf.CHError) as ei:
         chf.filter(big[1:])          # 8-byte aligned only
     assert ei.value.status == 4
+
+
+def _dist_worker(rank, world, port, n, dist_name, storage, q):
+    import os
+    import torch.distributed as tdist
+    from paper_2303_10581_b200 import dist as chdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = chdist.shard_range(n, world, rank)
+        xy = synth.points(dist_name, n, seed=4, device="cuda", lo=lo, hi=hi)
+        if storage == "f32":
+            xy = xy.float()
+        df = chdist.DistFilter(n, xy)
+        df.step()
+        loc, off, total = df.result()
+        q.put((rank, lo, hi, off, total, loc.cpu().numpy()))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+def test_distfilter_multirank_single_gpu(world, storage):
+    """The whole DistFilter step (K1 with index_base, extremes exchange, K3,
+    K2, count exchange) with `world` ranks sharing cuda:0 over gloo: the
+    concatenated survivors equal the oracle on the full array."""
+    import socket
+    import torch.multiprocessing as mp
+    n = 1_000_003
+    s0 = socket.socket(); s0.bind(("127.0.0.1", 0)); port = s0.getsockname()[1]; s0.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, n, "displaced", storage, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for p_ in procs:
+        p_.join(timeout=60)
+    for r in res:
+        assert len(r) == 6, r[1]
+    full = synth.points("displaced", n, seed=4, device="cuda")
+    if storage == "f32":
+        full = full.float()
+    want, _ = oracle.filter_compact(full.double().cpu().numpy())
+    got = np.concatenate([r[5] for r in res])
+    assert np.array_equal(got, want)
+    assert all(r[4] == len(want) for r in res)
+    offs = [r[3] for r in res]
+    assert offs == sorted(offs) and offs[0] == 0
