@@ -40,7 +40,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--impl", choices=["ours", "reference", "cub"], default="ours",
+                    help="ours | reference (the CPU oracle arm) | cub (the paper's Variant #4 rebuilt "
+                         "with CUB on this GPU, SURVEY f4: an in-box prior-art bar, not a driver arm)")
     ap.add_argument("--dist", choices=["normal", "circle", "displaced"], default="normal")
     ap.add_argument("--points", "--n", dest="n", type=float, default=1e9,
                     help="points (total for strong scaling, per GPU for weak)")
@@ -419,10 +421,61 @@ def run_ours(a):
     return 0
 
 
+def run_cub(a):
+    """the paper's CUB Variant #4 (8 ArgMin/ArgMax reductions,
+    a flag kernel, DeviceSelect::Flagged) on the same GPU, same input."""
+    import ctypes
+    import paper_2303_10581_b200 as chf
+    import synth
+    sys.path.insert(0, os.path.join(ROOT, "baselines"))
+    import build as bbuild  # baselines/build.py
+    lib = ctypes.CDLL(bbuild.build())
+    lib.chb_cub_temp_bytes.restype = ctypes.c_size_t
+    lib.chb_cub_temp_bytes.argtypes = [ctypes.c_int64]
+    lib.chb_cub_filter.restype = ctypes.c_int
+    lib.chb_cub_filter.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    dev = torch.device("cuda", 0)
+    n = int(a.n)
+    xy = synth.points(a.dist, n, seed=a.seed, p=a.p, device=dev)
+    out = torch.empty(n, dtype=torch.int64, device=dev)
+    tb = int(lib.chb_cub_temp_bytes(n))
+    tmp = torch.empty(tb, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    cnt = ctypes.c_int64(0)
+
+    def step():
+        rc = lib.chb_cub_filter(ctypes.c_void_p(xy.data_ptr()), n, ctypes.c_void_p(out.data_ptr()), ctypes.byref(cnt),
+                                ctypes.c_void_p(tmp.data_ptr()), tb, ctypes.c_void_p(stream.cuda_stream))
+        assert rc == 0, rc
+
+    for _ in range(a.warmup):
+        step()
+    mine = chf.filter(xy)                       # same survivors as the product path
+    assert cnt.value == mine.shape[0] and torch.equal(out[: cnt.value], mine)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    print(json.dumps({"impl": "cub", "metric": METRIC, "value": n / (ms / 1e3) / 1e9, "unit": UNIT, "n_gpus": 1,
+                      "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+                      "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": workload_name(a), "n": n, "survivors": int(cnt.value),
+                                 "variant": "paper Variant #4 cub-flagged (P:237-242), rebuilt with CUB"}}),
+          flush=True)
+    return 0
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         return run_reference(a)
+    if a.impl == "cub":
+        return run_cub(a)
     return run_ours(a)
 
 

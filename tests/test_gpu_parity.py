@@ -395,3 +395,30 @@ def test_distfilter_multirank_single_gpu(world, storage):
     assert all(r[4] == len(want) for r in res)
     offs = [r[3] for r in res]
     assert offs == sorted(offs) and offs[0] == 0
+
+
+def test_cub_variant_baseline_same_survivors():
+    """the CUB Variant #4 rebuild finds the same survivors."""
+    import ctypes
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baselines"))
+    import build as bbuild
+    lib = ctypes.CDLL(bbuild.build())
+    lib.chb_cub_temp_bytes.restype = ctypes.c_size_t
+    lib.chb_cub_temp_bytes.argtypes = [ctypes.c_int64]
+    lib.chb_cub_filter.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    for dist in ("normal", "displaced", "circle"):
+        n = 1_000_003
+        xy = synth.points(dist, n, seed=2, device=DEV)
+        out = torch.empty(n, dtype=torch.int64, device=DEV)
+        tb = int(lib.chb_cub_temp_bytes(n))
+        tmp = torch.empty(tb, dtype=torch.uint8, device=DEV)
+        cnt = ctypes.c_int64(0)
+        rc = lib.chb_cub_filter(ctypes.c_void_p(xy.data_ptr()), n, ctypes.c_void_p(out.data_ptr()), ctypes.byref(cnt),
+                                ctypes.c_void_p(tmp.data_ptr()), tb,
+                                ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert rc == 0
+        want, _ = oracle.filter_compact(xy.cpu().numpy())
+        assert np.array_equal(out[: cnt.value].cpu().numpy(), want), dist
