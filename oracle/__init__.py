@@ -76,6 +76,8 @@ def _load():
         lib.oracle_compact.restype = I64
         lib.oracle_filter_compact.argtypes = [P, I64, ctypes.c_int, P, ctypes.POINTER(_Octagon), P, P]
         lib.oracle_filter_compact.restype = ctypes.c_int
+        lib.oracle_filter_compact_exact.argtypes = [P, I64, P, P, P]
+        lib.oracle_filter_compact_exact.restype = ctypes.c_int
         lib.oracle_orient_sign.argtypes = [ctypes.c_double] * 6
         lib.oracle_orient_sign.restype = ctypes.c_int
         lib.oracle_hull.argtypes = [P, P, I64, P]
@@ -156,6 +158,22 @@ def filter_compact(xy, certified: bool = True):
     cnt = np.zeros(1, dtype=np.int64)
     o = _Octagon()
     st = _load().oracle_filter_compact(_p(a), n, int(certified), _p(idx8), ctypes.byref(o), _p(surv), _p(cnt))
+    if st == EMPTY:
+        raise ValueError("EmptySet")
+    if st == NONFINITE:
+        raise ValueError("NonFinite")
+    return surv[: cnt[0]].copy(), idx8
+
+
+def filter_compact_exact(xy):
+    """f3: survivors of the exact strict predicate (discard iff the exact
+    orientation is > 0 on every octagon edge).  Returns (survivors, idx8)."""
+    a = _xy(xy)
+    n = a.shape[0]
+    surv = np.zeros(max(n, 1), dtype=np.int64)
+    idx8 = np.zeros(8, dtype=np.int64)
+    cnt = np.zeros(1, dtype=np.int64)
+    st = _load().oracle_filter_compact_exact(_p(a), n, _p(idx8), _p(surv), _p(cnt))
     if st == EMPTY:
         raise ValueError("EmptySet")
     if st == NONFINITE:

@@ -274,6 +274,45 @@ int oracle_orient_sign(double ax, double ay, double bx, double by, double cx, do
 }
 
 /* ------------------------------------------------------------------------ */
+/* f3  The exact strict predicate: point p is   */
+/* discarded iff orient(v_k, v_{k+1}, p) > 0 exactly on every edge of the     */
+/* octagon (the same vertex cycle, R5).  Maximal hull-safe discard.          */
+/* ------------------------------------------------------------------------ */
+int oracle_orient_sign(double ax, double ay, double bx, double by, double cx, double cy);
+
+int oracle_discard_exact(const oracle_octagon *o, double x, double y)
+{
+    if (o->degenerate)
+        return 0;
+    for (int k = 0; k < o->nv; k++) {
+        int k1 = (k + 1) % o->nv;
+        if (oracle_orient_sign(o->vx[k], o->vy[k], o->vx[k1], o->vy[k1], x, y) <= 0)
+            return 0;
+    }
+    return 1;
+}
+
+int oracle_filter_compact_exact(const double *xy, int64_t n, int64_t idx8_out[8], int64_t *survivors,
+                                int64_t *count)
+{
+    int st = oracle_admit(xy, n);
+    if (st != OR_OK)
+        return st;
+    int64_t idx8[8];
+    oracle_extremes8(xy, n, idx8);
+    oracle_octagon oct;
+    oracle_octagon_build(xy, idx8, 1, &oct);
+    int64_t c = 0;
+    for (int64_t i = 0; i < n; i++)
+        if (!oracle_discard_exact(&oct, xy[2 * i], xy[2 * i + 1]))
+            survivors[c++] = i;
+    *count = c;
+    if (idx8_out)
+        memcpy(idx8_out, idx8, sizeof(idx8));
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* a8  Hull of the candidates ("connected to any existing convex   */
 /* hull implementation").  Andrew's monotone    */
 /* chain with the exact sign above: sort by (x, y, index), drop duplicate    */

@@ -352,3 +352,31 @@ def test_hull_idempotent():
     xy = synth.points("displaced", 3000, seed=6).numpy()
     h = oracle.hull(xy)
     assert list(oracle.hull(xy, h)) == list(h)
+
+
+# -------------------------------------------------- f3: exact predicate ----
+@pytest.mark.parametrize("dist", ["normal", "displaced", "circle"])
+def test_exact_predicate_matches_rational_definition(dist):
+    """f3: discard iff the exact orientation (Fraction) is > 0
+    on every octagon edge; the certified survivors are a superset."""
+    rng = np.random.default_rng(31)
+    base = synth.points(dist, 3000, seed=31).numpy()
+    o = oracle.octagon(base)
+    V = list(zip(o["vx"], o["vy"]))
+    adv = near_edge_points(rng, V, 3000, ulps=3)
+    xy = np.concatenate([base, adv])
+    assert list(oracle.octagon(xy)["vidx"]) == list(o["vidx"])
+    surv_x, _ = oracle.filter_compact_exact(xy)
+    keep_x = np.zeros(len(xy), bool)
+    keep_x[surv_x] = True
+    for i in range(len(xy)):
+        assert keep_x[i] == (not strictly_inside_exact(V, xy[i])), i
+    surv_c, _ = oracle.filter_compact(xy)
+    assert set(surv_x.tolist()) <= set(surv_c.tolist())
+    assert list(oracle.hull(xy, surv_x)) == list(oracle.hull(xy))
+
+
+def test_exact_predicate_golden():
+    for ex in load_golden():
+        surv, _ = oracle.filter_compact_exact(ex["points"])
+        assert list(surv) == ex["survivors"], ex["name"]
