@@ -49,7 +49,9 @@ def parse():
     ap.add_argument("--p", type=float, default=0.1)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
-    ap.add_argument("--plain", action="store_true", help="plain fp64 predicate (T_k = 0)")
+    ap.add_argument("--predicate", choices=["certified", "plain", "exact"], default="certified",
+                    help="certified (default, DESIGN R4) | plain (T_k = 0) | exact (f3)")
+    ap.add_argument("--plain", action="store_true", help="alias of --predicate plain")
     ap.add_argument("--storage", choices=["f64", "f32"], default="f64",
                     help="point storage precision (f32: the paper's, widened exactly to f64)")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -173,7 +175,9 @@ def run_reference(a):
     m0 = min(n, 1 << 20)
     probe = synth.points(a.dist, n, seed=a.seed, p=a.p, device=dev, lo=0, hi=m0).cpu().numpy()
     t0 = time.perf_counter()
-    oracle.filter_compact(probe, certified=not a.plain)
+    ofc = (lambda v: oracle.filter_compact_exact(v)) if a.predicate == "exact" else \
+        (lambda v: oracle.filter_compact(v, certified=a.predicate != "plain"))
+    ofc(probe)
     dt0 = time.perf_counter() - t0
     per_step_s = 120.0 / max(a.steps + a.warmup, 1)
     m = int(min(n, max(m0, m0 * min(per_step_s, 2.0) / max(dt0, 1e-9))))
@@ -181,12 +185,12 @@ def run_reference(a):
     if a.storage == "f32":
         xy = xy.astype(np.float32).astype(np.float64)   # the widened f32 workload
     for _ in range(a.warmup):
-        oracle.filter_compact(xy, certified=not a.plain)
+        ofc(xy)
     times = []
     s = 0
     for _ in range(a.steps):
         t0 = time.perf_counter()
-        surv, _ = oracle.filter_compact(xy, certified=not a.plain)
+        surv, _ = ofc(xy)
         times.append(time.perf_counter() - t0)
         s = len(surv)
     ms = 1e3 * float(np.mean(times))
@@ -406,7 +410,7 @@ def run_ours(a):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(a), "n": n_total, "n_per_gpu": n_local, "dist": a.dist,
                        "seed": a.seed, "p": a.p if a.dist == "displaced" else None,
-                       "predicate": "plain" if a.plain else "certified", "storage": a.storage,
+                       "predicate": a.predicate, "storage": a.storage,
                        "parallelism": f"dp{world}", "l2": f"inputs larger than L2 ({int(bpp)} B/pt)"
                        if bpp * n_local > 126e6 else "inputs smaller than L2 (not flushed)"},
             "survivors": s_total, "survivor_ratio": s_total / n_total,
@@ -472,6 +476,10 @@ def run_cub(a):
 
 def main():
     a = parse()
+    if a.plain:
+        a.predicate = "plain"
+    # the binding's predicate argument: False (certified), True (plain), "exact"
+    a.plain = {"certified": False, "plain": True, "exact": "exact"}[a.predicate]
     if a.impl == "reference":
         return run_reference(a)
     if a.impl == "cub":

@@ -61,6 +61,10 @@ typedef enum {
 /* Predicate switch (DESIGN R4).  Default: certified thresholds T_k. */
 #define CH_CERTIFIED 0
 #define CH_PLAIN 1 /* T_k = 0: the plain fp64 test (not hull-safe adversarially) */
+#define CH_EXACT 2 /* f3: discard iff the EXACT orientation is > 0 on
+                      every edge -- the maximal hull-safe discard.  Certified T_k and
+                      Shewchuk's per-point bound decide all but a thin band, which is
+                      evaluated with exact expansion arithmetic on the device. */
 
 /* The eight extremes, slot order R, TR, T, TL, L, BL, B, BR:
  *   R = argmax x, TR = argmax fl(x+y), T = argmax y, TL = argmin fl(x-y),
@@ -106,7 +110,7 @@ typedef struct {
     double cx, cy;
     float f32_a[8], f32_b[8], f32_cin[8], f32_cout[8];
     int32_t has_f32;
-    int32_t pad_;
+    int32_t exact;     /* 1 if built with CH_EXACT                       */
 } ch_octagon;
 
 /* Result of the last filter call on a workspace (device-resident copy in the

@@ -47,7 +47,13 @@ def _points(xy: torch.Tensor) -> torch.Tensor:
 
 
 def _plain(plain: bool) -> int:
-    return _lib.CH_PLAIN if plain else _lib.CH_CERTIFIED
+    """Predicate flags: True / "plain" -> CH_PLAIN, "exact" -> CH_EXACT,
+    False / "certified" -> CH_CERTIFIED (DESIGN R4, f3)."""
+    if plain == "exact":
+        return _lib.CH_EXACT
+    if plain is True or plain == "plain":
+        return _lib.CH_PLAIN
+    return _lib.CH_CERTIFIED
 
 
 def _fn(lib, name: str, xy: torch.Tensor):

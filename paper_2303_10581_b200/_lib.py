@@ -18,7 +18,7 @@ SZ = ctypes.c_size_t
 
 CH_OK, CH_ERR_INVALID_ARG, CH_ERR_EMPTY, CH_ERR_NONFINITE = 0, 1, 2, 3
 CH_ERR_MISALIGNED, CH_ERR_WORKSPACE, CH_ERR_CUDA = 4, 5, 6
-CH_CERTIFIED, CH_PLAIN = 0, 1
+CH_CERTIFIED, CH_PLAIN, CH_EXACT = 0, 1, 2
 
 
 class Extremes(ctypes.Structure):
@@ -32,7 +32,7 @@ class Octagon(ctypes.Structure):
         ("bbox", DBL * 4), ("box", DBL * 4), ("has_box", I32), ("plain", I32),
         ("guess_edge", I32 * 8), ("cx", DBL), ("cy", DBL),
         ("f32_a", ctypes.c_float * 8), ("f32_b", ctypes.c_float * 8), ("f32_cin", ctypes.c_float * 8),
-        ("f32_cout", ctypes.c_float * 8), ("has_f32", I32), ("pad_", I32),
+        ("f32_cout", ctypes.c_float * 8), ("has_f32", I32), ("exact", I32),
     ]
 
 

@@ -23,6 +23,7 @@
 
 #include "../../include/chfilter.h"
 #include "octagon.cuh"
+#include "exact.cuh"
 
 extern "C" int64_t ch_internal_hull(const double *pts, const int64_t *ids, int64_t m, int64_t *hull);
 
@@ -562,7 +563,7 @@ __global__ void __launch_bounds__(256) k3_combine8(const ch_extremes *__restrict
 
 // ========================================================= octagon test ==
 struct __align__(16) SEdge {
-    double ax, ay, ex, ey, thr, pad;
+    double ax, ay, ex, ey, thr, bx, by, pad;
 };
 struct __align__(16) FEdge {
     float a, b, cin, cout;
@@ -573,7 +574,7 @@ struct SOct {
     double box[4];
     float boxf[4]; // float bounds with x >= boxf[0] <=> (double)x >= box[0], etc.
     double cx, cy;
-    int nv, degenerate, has_f32;
+    int nv, degenerate, has_f32, exact;
     int guess[8];
 };
 
@@ -586,6 +587,9 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.e[t].ex = o->ex[t];
         s.e[t].ey = o->ey[t];
         s.e[t].thr = o->thr[t];
+        const int t1 = (t + 1 < o->nv) ? t + 1 : 0;
+        s.e[t].bx = o->vx[t1];
+        s.e[t].by = o->vy[t1];
         s.e[t].pad = 0.0;
         s.guess[t] = o->guess_edge[t];
         s.f[t].a = o->f32_a[t];
@@ -606,7 +610,28 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.nv = o->nv;
         s.degenerate = o->degenerate;
         s.has_f32 = o->has_f32;
+        s.exact = o->exact;
     }
+}
+
+// One edge in fp64: true if the point is certainly "inside" for this edge.
+// Certified / plain modes: D_k > T_k (the definition, R4).  Exact mode (f3):
+// the exact orientation is > 0 -- decided by Shewchuk's per-point bound
+// (3 + 16 eps) eps (|l| + |r|) on the same D_k, else by exact expansion
+// arithmetic (chf::orient_sign_exact_stage).
+__device__ __forceinline__ bool edge_inside(const SEdge &e, int exact, double x, double y)
+{
+    const double dy = __dsub_rn(y, e.ay), dx = __dsub_rn(x, e.ax);
+    const double l = __dmul_rn(e.ex, dy), r = __dmul_rn(e.ey, dx);
+    const double D = __dsub_rn(l, r);
+    if (!exact)
+        return D > e.thr;
+    const double eb = __dmul_rn((3.0 + 16.0 * 0x1p-53) * 0x1p-53, __dadd_rn(fabs(l), fabs(r)));
+    if (D > eb)
+        return true;
+    if (-D > eb)
+        return false;
+    return chf::orient_sign_exact_stage(e.ax, e.ay, e.bx, e.by, x, y) > 0;
 }
 
 // Survivor test, bit-identical to "not (forall k: D_k > T_k)" (R4): the
@@ -626,9 +651,7 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
         int off = (t & 1) ? ((t + 1) >> 1) : -(t >> 1);
         int k = g + off;
         k = k < 0 ? k + nv : (k >= nv ? k - nv : k);
-        const SEdge &e = s.e[k];
-        double D = chf::edge_det(e.ax, e.ay, e.ex, e.ey, x, y);
-        if (!(D > e.thr))
+        if (!edge_inside(s.e[k], s.exact, x, y))
             return true;
     }
     return false;
@@ -678,7 +701,8 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
                                 : (dx < 0.0 ? (c ? 4 : 5) : (c ? 7 : 6));
             const SEdge &e = s.e[s.guess[oct]];
             double D = chf::edge_det(e.ax, e.ay, e.ex, e.ey, (double)px[i], (double)py[i]);
-            keep |= (D > e.thr ? 0u : 1u) << i;
+            // exact mode: only D < -T_k proves the exact orientation negative
+            keep |= ((s.exact ? D < -e.thr : !(D > e.thr)) ? 1u : 0u) << i;
         }
         keep &= und;
         und &= ~keep;
@@ -728,24 +752,29 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
         // fp64 on every edge for the (rare) points inside the uncertainty band
         unsigned disc = und;
         for (int k = 0; k < nv; k++) {
-            const double ax = s.e[k].ax, ay = s.e[k].ay, ex = s.e[k].ex, ey = s.e[k].ey, thr = s.e[k].thr;
 #pragma unroll
-            for (int i = 0; i < NP; i++) {
-                if ((und >> i) & 1u) {
-                    const double D = chf::edge_det(ax, ay, ex, ey, (double)px[i], (double)py[i]);
-                    disc &= ~((D > thr ? 0u : 1u) << i);
-                }
-            }
+            for (int i = 0; i < NP; i++)
+                if ((disc >> i) & 1u)
+                    disc &= ~((edge_inside(s.e[k], s.exact, (double)px[i], (double)py[i]) ? 0u : 1u) << i);
         }
         return keep | (und & ~disc);
     }
     unsigned disc = und;
-    for (int k = 0; k < nv; k++) {
-        const double ax = s.e[k].ax, ay = s.e[k].ay, ex = s.e[k].ex, ey = s.e[k].ey, thr = s.e[k].thr;
+    if (!s.exact) {
+        for (int k = 0; k < nv; k++) {
+            const double ax = s.e[k].ax, ay = s.e[k].ay, ex = s.e[k].ex, ey = s.e[k].ey, thr = s.e[k].thr;
 #pragma unroll
-        for (int i = 0; i < NP; i++) {
-            double D = chf::edge_det(ax, ay, ex, ey, (double)px[i], (double)py[i]);
-            disc &= ~((D > thr ? 0u : 1u) << i);
+            for (int i = 0; i < NP; i++) {
+                double D = chf::edge_det(ax, ay, ex, ey, (double)px[i], (double)py[i]);
+                disc &= ~((D > thr ? 0u : 1u) << i);
+            }
+        }
+    } else {
+        for (int k = 0; k < nv; k++) {
+#pragma unroll
+            for (int i = 0; i < NP; i++)
+                if ((disc >> i) & 1u)
+                    disc &= ~((edge_inside(s.e[k], 1, (double)px[i], (double)py[i]) ? 0u : 1u) << i);
         }
     }
     return keep | (und & ~disc);

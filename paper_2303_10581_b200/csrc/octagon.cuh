@@ -123,7 +123,9 @@ CH_HD void octagon_edge(ch_octagon &o, int k)
     o.f32_a[k] = CH_F32(-ey);
     o.f32_b[k] = CH_F32(ex);
     o.f32_cin[k] = f32_down(CH_SUB(CH_SUB(c, T), M));
-    o.f32_cout[k] = f32_up(CH_ADD(CH_SUB(c, T), M));
+    // keep-certificate: h <= 0 proves D_k < T_k; in exact mode it must prove
+    // D_k < -T_k (then the exact orientation is negative, R4's bound)
+    o.f32_cout[k] = f32_up(CH_ADD(CH_SUB(c, o.exact ? -T : T), M));
 }
 
 // Octagon assembly (DESIGN R5), vertex part: cycle [R,TR,T,TL,L,BL,B,BR];
@@ -136,6 +138,7 @@ CH_HD void octagon_vertices(const ch_extremes &e, int flags, ch_octagon &o)
     o.degenerate = 0;
     o.has_box = 0;
     o.plain = (flags & CH_PLAIN) ? 1 : 0;
+    o.exact = (!o.plain && (flags & CH_EXACT)) ? 1 : 0;
     int slot_vertex[8];
     for (int k = 0; k < 8; k++) {
         o.vidx[k] = -1;
@@ -144,7 +147,6 @@ CH_HD void octagon_vertices(const ch_extremes &e, int flags, ch_octagon &o)
         o.f32_a[k] = o.f32_b[k] = o.f32_cin[k] = o.f32_cout[k] = 0.0f;
     }
     o.has_f32 = 0;
-    o.pad_ = 0;
     for (int k = 0; k < 8; k++) {
         double x = e.x[k], y = e.y[k];
         if (!(o.nv > 0 && x == o.vx[o.nv - 1] && y == o.vy[o.nv - 1])) {

@@ -422,3 +422,41 @@ def test_cub_variant_baseline_same_survivors():
         assert rc == 0
         want, _ = oracle.filter_compact(xy.cpu().numpy())
         assert np.array_equal(out[: cnt.value].cpu().numpy(), want), dist
+
+
+# --------------------------------------------- f3: the exact predicate ------
+@pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
+def test_parity_exact_predicate(dist):
+    """f3: CH_EXACT survivors equal the oracle's exact strict predicate,
+    including near-edge points in the certified band (exact evaluation on
+    the device) and fp32-band points."""
+    rng = np.random.default_rng(41)
+    base = synth.points(dist, 200_000, seed=41).numpy()
+    o = oracle.octagon(base)
+    V = list(zip(o["vx"], o["vy"]))
+    adv = near_edge_points(rng, V, 50_000, ulps=3)
+    band = _edge_band_points(rng, o, [10.0 ** -e for e in range(6, 17)], per=200)
+    xy = np.concatenate([base, adv, band])
+    d = torch.tensor(xy, device=DEV)
+    want, want_idx = oracle.filter_compact_exact(xy)
+    got = chf.filter(d, plain="exact").cpu().numpy()
+    assert np.array_equal(got, want)
+    cert, _ = oracle.filter_compact(xy)
+    assert len(want) <= len(cert)
+    ws = chf.Workspace(len(xy))
+    e, oc = chf.extremes8(d, ws, plain="exact")
+    assert oc.exact == 1 and np.array_equal(np.array(e.idx[:]), want_idx)
+    # the bit-vector kernel (K4) agrees too
+    bits = chf.octagon_filter(d, ws).cpu().numpy().view(np.uint32)
+    keep = ((bits[:, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(-1)[: len(xy)]
+    assert np.array_equal(np.flatnonzero(keep), want)
+
+
+def test_parity_exact_predicate_sizes_and_f32():
+    for n in (1, 7, 4097, 333_333):
+        xy = synth.points("displaced", n, seed=n, device=DEV)
+        want, _ = oracle.filter_compact_exact(xy.cpu().numpy())
+        assert np.array_equal(chf.filter(xy, plain="exact").cpu().numpy(), want)
+        x32 = xy.float()
+        want32, _ = oracle.filter_compact_exact(x32.double().cpu().numpy())
+        assert np.array_equal(chf.filter(x32, plain="exact").cpu().numpy(), want32)
