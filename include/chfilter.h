@@ -219,10 +219,23 @@ ch_status ch_gather_points(const double *d_xy, int64_t index_base, const int64_t
 ch_status ch_hull_points(const double *h_pts, const int64_t *h_ids, int64_t m,
                          int64_t *h_hull, int64_t *h_n_hull);
 
+/* f1: Algorithm 1 line 4 on the device (future work P:432):
+ * the exact strict hull of the m survivors d_surv (indices into d_xy), same
+ * canonical form as ch_hull_points (DESIGN R8).  Two stable radix sorts by
+ * (x, y), per-chunk exact monotone chains, a tree of exact bridge merges.
+ * Scratch: ch_hull_gpu_temp_bytes(m) bytes at d_tmp.  Hull ids go to h_hull
+ * (host, capacity m); synchronizes `stream`. */
+size_t ch_hull_gpu_temp_bytes(int64_t m);
+ch_status ch_hull_gpu(const double *d_xy, const int64_t *d_surv, int64_t m, int64_t *h_hull,
+                      int64_t *h_n_hull, void *d_tmp, size_t tmp_bytes, void *stream);
+
+#define CH_HULL_HOST 4 /* flag for ch_hull_end_to_end: gather + host monotone chain */
+
 /* Algorithm 1 complete: ch_filter on device-resident d_xy, then
- * the survivors' coordinates are gathered on the device, copied to the host,
- * and the exact hull is computed there.  Stage times go to h_stats
- * (nullable).  h_hull capacity >= number of survivors (<= n). */
+ * the exact hull of the survivors -- on the device (ch_hull_gpu, default)
+ * or, with flags & CH_HULL_HOST, gathered to the host and computed there
+ * (ch_hull_points).  Stage times go to h_stats (nullable).  h_hull capacity
+ * >= number of survivors (<= n). */
 ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *d_survivors,
                              int64_t *h_n_survivors, int64_t *h_hull, int64_t *h_n_hull,
                              ch_stats *h_stats, void *d_ws, size_t ws_bytes, void *stream);

@@ -212,10 +212,26 @@ def hull_points(pts: np.ndarray, ids: np.ndarray) -> np.ndarray:
     return out[: h.value].copy()
 
 
+def hull_gpu(xy: torch.Tensor, surv: torch.Tensor, stream=None) -> np.ndarray:
+    """f1: exact strict hull of the survivors `surv` (int64 device indices
+    into xy) computed on the device; returns the hull ids (host)."""
+    lib = _lib.load()
+    xy = _points(xy)
+    m = int(surv.shape[0])
+    tb = int(lib.ch_hull_gpu_temp_bytes(m))
+    tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=xy.device)
+    out = np.zeros(max(m, 1), dtype=np.int64)
+    h = ctypes.c_int64(0)
+    _lib.check(lib.ch_hull_gpu(_ptr(xy), _ptr(surv), m, out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(h),
+                               _ptr(tmp), tb, _stream(stream)), "ch_hull_gpu")
+    return out[: h.value].copy()
+
+
 def hull_end_to_end(xy: torch.Tensor, ws: Workspace | None = None, plain: bool = False,
-                    out: torch.Tensor | None = None, stream=None):
-    """Algorithm 1: filter on the GPU, exact hull of the survivors
-    on the host.  Returns (hull ids np.ndarray, survivors tensor, Stats)."""
+                    out: torch.Tensor | None = None, stream=None, host_hull: bool = False):
+    """Algorithm 1: filter on the GPU, then the exact hull of the
+    survivors on the device (default, f1) or on the host (host_hull=True).
+    Returns (hull ids np.ndarray, survivors tensor, Stats)."""
     lib = _lib.load()
     xy = _points(xy)
     if xy.dtype != torch.float64:
@@ -226,7 +242,8 @@ def hull_end_to_end(xy: torch.Tensor, ws: Workspace | None = None, plain: bool =
         out = torch.empty(max(n, 1), dtype=torch.int64, device=xy.device)
     hull = np.zeros(max(n, 1), dtype=np.int64)
     ns, nh, st = ctypes.c_int64(0), ctypes.c_int64(0), Stats()
-    _lib.check(lib.ch_hull_end_to_end(_ptr(xy), n, _plain(plain), _ptr(out), ctypes.byref(ns),
+    flags = _plain(plain) | (_lib.CH_HULL_HOST if host_hull else 0)
+    _lib.check(lib.ch_hull_end_to_end(_ptr(xy), n, flags, _ptr(out), ctypes.byref(ns),
                                       hull.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nh), ctypes.byref(st),
                                       ws.ptr, ws.nbytes, _stream(stream)), "ch_hull_end_to_end")
     return hull[: nh.value].copy(), out[: ns.value], st

@@ -19,6 +19,7 @@ SZ = ctypes.c_size_t
 CH_OK, CH_ERR_INVALID_ARG, CH_ERR_EMPTY, CH_ERR_NONFINITE = 0, 1, 2, 3
 CH_ERR_MISALIGNED, CH_ERR_WORKSPACE, CH_ERR_CUDA = 4, 5, 6
 CH_CERTIFIED, CH_PLAIN, CH_EXACT = 0, 1, 2
+CH_HULL_HOST = 4
 
 
 class Extremes(ctypes.Structure):
@@ -67,6 +68,8 @@ SIGNATURES = {
     "ch_filter_host": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, ctypes.POINTER(I64), P, SZ, P]),
     "ch_gather_points": (ctypes.c_int, [P, I64, P, I64, P, P]),
     "ch_hull_points": (ctypes.c_int, [P, P, I64, P, ctypes.POINTER(I64)]),
+    "ch_hull_gpu_temp_bytes": (SZ, [I64]),
+    "ch_hull_gpu": (ctypes.c_int, [P, P, I64, P, ctypes.POINTER(I64), P, SZ, P]),
     "ch_hull_end_to_end": (ctypes.c_int, [P, I64, ctypes.c_int, P, ctypes.POINTER(I64), P,
                                           ctypes.POINTER(I64), ctypes.POINTER(Stats), P, SZ, P]),
 }

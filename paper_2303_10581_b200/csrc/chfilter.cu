@@ -118,36 +118,6 @@ __device__ __forceinline__ void ld64f(const float *p, float &a, float &b)
 {
     asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(a), "=f"(b) : "l"(p));
 }
-// Two consecutive points as doubles: one wide load (LDG.256 for double,
-// LDG.128 for float) when VEC (the pair is aligned to its size), else two.
-template <typename T, bool VEC>
-__device__ __forceinline__ void ld2pts(const T *p, double &a, double &b, double &c, double &d);
-template <>
-__device__ __forceinline__ void ld2pts<double, true>(const double *p, double &a, double &b, double &c, double &d)
-{
-    ld256(p, a, b, c, d);
-}
-template <>
-__device__ __forceinline__ void ld2pts<double, false>(const double *p, double &a, double &b, double &c, double &d)
-{
-    ld128(p, a, b);
-    ld128(p + 2, c, d);
-}
-template <>
-__device__ __forceinline__ void ld2pts<float, true>(const float *p, double &a, double &b, double &c, double &d)
-{
-    float fa, fb, fc, fd;
-    ld128f(p, fa, fb, fc, fd);
-    a = fa, b = fb, c = fc, d = fd; // exact widening
-}
-template <>
-__device__ __forceinline__ void ld2pts<float, false>(const float *p, double &a, double &b, double &c, double &d)
-{
-    float fa, fb, fc, fd;
-    ld64f(p, fa, fb);
-    ld64f(p + 2, fc, fd);
-    a = fa, b = fb, c = fc, d = fd;
-}
 // Two consecutive points in their storage type (widened at use).
 template <typename T, bool VEC>
 __device__ __forceinline__ void ld2raw(const T *p, T (&r)[4]);
@@ -1547,7 +1517,7 @@ ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *
     cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
     int64_t cnt = 0;
-    ch_status s = ch_filter(d_xy, n, flags, d_survivors, &cnt, d_ws, ws_bytes, stream);
+    ch_status s = ch_filter(d_xy, n, flags & 3, d_survivors, &cnt, d_ws, ws_bytes, stream);
     cudaEventRecord(e1, st);
     if (s != CH_OK) {
         cudaEventDestroy(e0);
@@ -1561,6 +1531,21 @@ ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *
     cudaEventDestroy(e1);
 
     auto t0 = std::chrono::steady_clock::now();
+    auto t1 = t0;
+    int64_t h = 0;
+    if (!(flags & CH_HULL_HOST)) {
+        // f1: the hull on the device; only the hull ids come back
+        const size_t tb = ch_hull_gpu_temp_bytes(cnt);
+        void *d_tmp = nullptr;
+        if (cudaMallocAsync(&d_tmp, tb, st) != cudaSuccess)
+            return fail(CH_ERR_CUDA, "cudaMallocAsync for the device hull failed");
+        s = ch_hull_gpu(d_xy, d_survivors, cnt, h_hull, &h, d_tmp, tb, stream);
+        cudaFreeAsync(d_tmp, st);
+        cudaStreamSynchronize(st);
+        if (s != CH_OK)
+            return fail(s, "ch_hull_gpu failed");
+        t1 = std::chrono::steady_clock::now();
+    } else {
     std::vector<double> pts((size_t)cnt * 2);
     std::vector<int64_t> ids((size_t)cnt);
     if (cnt > 0) {
@@ -1576,8 +1561,9 @@ ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *
         if ((s = cuda_check("hull gather")) != CH_OK)
             return s;
     }
-    auto t1 = std::chrono::steady_clock::now();
-    int64_t h = ch_internal_hull(pts.data(), ids.data(), cnt, h_hull);
+    t1 = std::chrono::steady_clock::now();
+    h = ch_internal_hull(pts.data(), ids.data(), cnt, h_hull);
+    }
     auto t2 = std::chrono::steady_clock::now();
     *h_n_hull = h;
     if (h_n_survivors)

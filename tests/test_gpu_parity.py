@@ -460,3 +460,49 @@ def test_parity_exact_predicate_sizes_and_f32():
         x32 = xy.float()
         want32, _ = oracle.filter_compact_exact(x32.double().cpu().numpy())
         assert np.array_equal(chf.filter(x32, plain="exact").cpu().numpy(), want32)
+
+
+# ------------------------------------------------------ f1: device hull ------
+def _hull_sets():
+    rng = np.random.default_rng(51)
+    yield "single", np.array([[2.0, 3.0]])
+    yield "two", np.array([[1.0, 2.0], [3.0, 4.0]])
+    yield "same", np.full((1000, 2), 0.5)
+    yield "collinear", np.stack([np.arange(3000.0), 2 * np.arange(3000.0)], 1)
+    yield "vertical", np.stack([np.zeros(2000), rng.random(2000)], 1)
+    for trial in range(4):
+        yield f"grid{trial}", rng.integers(-20, 21, size=(int(rng.integers(1, 60000)), 2)).astype(np.float64)
+    for n in (1000, 70_001, 1_000_003):
+        th = rng.random(n) * 2 * np.pi
+        yield f"circle{n}", np.stack([np.cos(th), np.sin(th)], 1) * 0.25
+    yield "random", rng.random((300_000, 2))
+    yield "signed_zero", np.array([[0.0, 0.0], [-0.0, 0.0], [1.0, 0.0], [0.0, -0.0], [0.0, 1.0], [-0.0, -0.0]])
+
+
+def test_device_hull_matches_oracle():
+    """The device hull (every point a candidate) equals the oracle hull."""
+    for name, xy in _hull_sets():
+        d = torch.tensor(xy, device=DEV)
+        ids = torch.arange(len(xy), dtype=torch.int64, device=DEV)
+        got = chf.hull_gpu(d, ids)
+        assert np.array_equal(got, oracle.hull(xy)), name
+
+
+@pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
+def test_device_hull_end_to_end(dist):
+    n = 2_000_003
+    xy_d = synth.points(dist, n, seed=52, device=DEV)
+    xy = xy_d.cpu().numpy()
+    hull, surv, st = chf.hull_end_to_end(xy_d)
+    hull_h, surv_h, st_h = chf.hull_end_to_end(xy_d, host_hull=True)
+    want_hull, want_s, _ = oracle.hull_end_to_end(xy)
+    assert np.array_equal(surv.cpu().numpy(), want_s)
+    assert np.array_equal(hull, want_hull)
+    assert np.array_equal(hull_h, want_hull)
+
+
+def test_device_hull_golden():
+    for ex in load_golden():
+        d = torch.tensor(ex["points"], device=DEV)
+        s = torch.tensor(ex["survivors"], dtype=torch.int64, device=DEV)
+        assert list(chf.hull_gpu(d, s)) == ex["hull"], ex["name"]
