@@ -532,14 +532,15 @@ __global__ void __launch_bounds__(256) k3_combine8(const ch_extremes *__restrict
 }
 
 // ========================================================= octagon test ==
-struct __align__(16) SEdge {
-    double ax, ay, ex, ey, thr, bx, by, pad;
+struct __align__(16) SEdge { // 48 B: lanes indexing different edges hit distinct banks
+    double ax, ay, ex, ey, thr, pad;
 };
 struct __align__(16) FEdge {
     float a, b, cin, cout;
 };
 struct SOct {
     SEdge e[8];
+    double2 eb[8]; // edge end points (exact mode only)
     FEdge f[8];
     double box[4];
     float boxf[4]; // float bounds with x >= boxf[0] <=> (double)x >= box[0], etc.
@@ -558,8 +559,7 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.e[t].ey = o->ey[t];
         s.e[t].thr = o->thr[t];
         const int t1 = (t + 1 < o->nv) ? t + 1 : 0;
-        s.e[t].bx = o->vx[t1];
-        s.e[t].by = o->vy[t1];
+        s.eb[t] = make_double2(o->vx[t1], o->vy[t1]);
         s.e[t].pad = 0.0;
         s.guess[t] = o->guess_edge[t];
         s.f[t].a = o->f32_a[t];
@@ -589,7 +589,7 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
 // the exact orientation is > 0 -- decided by Shewchuk's per-point bound
 // (3 + 16 eps) eps (|l| + |r|) on the same D_k, else by exact expansion
 // arithmetic (chf::orient_sign_exact_stage).
-__device__ __forceinline__ bool edge_inside(const SEdge &e, int exact, double x, double y)
+__device__ __forceinline__ bool edge_inside(const SEdge &e, const double2 &b, int exact, double x, double y)
 {
     const double dy = __dsub_rn(y, e.ay), dx = __dsub_rn(x, e.ax);
     const double l = __dmul_rn(e.ex, dy), r = __dmul_rn(e.ey, dx);
@@ -601,7 +601,7 @@ __device__ __forceinline__ bool edge_inside(const SEdge &e, int exact, double x,
         return true;
     if (-D > eb)
         return false;
-    return chf::orient_sign_exact_stage(e.ax, e.ay, e.bx, e.by, x, y) > 0;
+    return chf::orient_sign_exact_stage(e.ax, e.ay, b.x, b.y, x, y) > 0;
 }
 
 // Survivor test, bit-identical to "not (forall k: D_k > T_k)" (R4): the
@@ -621,7 +621,7 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
         int off = (t & 1) ? ((t + 1) >> 1) : -(t >> 1);
         int k = g + off;
         k = k < 0 ? k + nv : (k >= nv ? k - nv : k);
-        if (!edge_inside(s.e[k], s.exact, x, y))
+        if (!edge_inside(s.e[k], s.eb[k], s.exact, x, y))
             return true;
     }
     return false;
@@ -632,9 +632,9 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
 // skipped when no lane of the warp needs it (warp-uniform branches):
 //  1. the certified accept box (4 DSETP): inside => discarded (proof at
 //     chf::box_corner_ok);
-//  2. (has_f32) the fp32 pre-filter on every edge (proof at chf::octagon_edge):
-//     g_k >= 0 on every edge certifies discard, h_k <= 0 on some edge
-//     certifies keep; then
+//  2. (has_f32) the fp32 pre-filter (proof at chf::octagon_edge): g_k >= 0 on
+//     every edge certifies discard; then h_k <= 0 certifies keep, tried on
+//     the octant-guessed edge first and on every edge only if needed; then
 //  3. fp64 D_k on every edge for the points left in the uncertainty band.
 // Before stage 2, adaptively: 2'. the guessed edge of the point's octant
 // (D_g <= T_g => kept, the oracle's exists-k condition); a warp whose
@@ -686,34 +686,74 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
         // g_k < 0 or -0 => not certified inside) and of h_k (any h_k <= -0
         // => certified outside).  Proof at chf::octagon_edge.
         unsigned in = 0, out = 0;
-        constexpr int CH = NP < 8 ? NP : 8; // points per pass (bounds register use)
+        constexpr int CH = NP < 4 ? NP : 4; // points per pass (bounds register use)
+        const float cxf = (float)s.cx, cyf = (float)s.cy;
 #pragma unroll
         for (int c0 = 0; c0 < NP; c0 += CH) {
             float xf[CH], yf[CH];
-            unsigned sg[CH], sh[CH];
+            unsigned sg[CH];
 #pragma unroll
             for (int i = 0; i < CH; i++) {
                 xf[i] = (float)px[c0 + i]; // exact for float storage
                 yf[i] = (float)py[c0 + i];
                 sg[i] = 0u;
-                sh[i] = 0u;
             }
+            // A. inside certificate on every edge: all g_k >= 0
+            if (nv == 8) {
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                if (k < nv) {
+                for (int k = 0; k < 8; k++) {
                     const FEdge f = s.f[k];
 #pragma unroll
-                    for (int i = 0; i < CH; i++) {
+                    for (int i = 0; i < CH; i++)
                         sg[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cin)));
-                        sh[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cout)));
-                    }
+                }
+            } else {
+                for (int k = 0; k < nv; k++) {
+                    const FEdge f = s.f[k];
+#pragma unroll
+                    for (int i = 0; i < CH; i++)
+                        sg[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cin)));
                 }
             }
+            unsigned inc = 0;
 #pragma unroll
-            for (int i = 0; i < CH; i++) {
-                in |= ((~sg[i]) >> 31) << (c0 + i);
-                out |= (sh[i] >> 31) << (c0 + i);
+            for (int i = 0; i < CH; i++)
+                inc |= ((~sg[i]) >> 31) << i;
+            unsigned undc = ((und >> c0) & ((1u << CH) - 1u)) & ~inc;
+            unsigned outc = 0;
+            if (__any_sync(FULL, undc)) {
+                // B. keep certificate on the octant-guessed edge: h_g <= 0
+#pragma unroll
+                for (int i = 0; i < CH; i++) {
+                    const float dx = xf[i] - cxf, dy = yf[i] - cyf;
+                    const bool c = fabsf(dx) >= fabsf(dy);
+                    const int oct = dy >= 0.0f ? (dx >= 0.0f ? (c ? 0 : 1) : (c ? 3 : 2))
+                                               : (dx < 0.0f ? (c ? 4 : 5) : (c ? 7 : 6));
+                    const FEdge f = s.f[s.guess[oct]];
+                    const float h = __fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cout));
+                    outc |= (__float_as_uint(h) >> 31) << i;
+                }
+                outc &= undc;
+                if (__any_sync(FULL, undc & ~outc)) {
+                    // C. keep certificate on any edge: some h_k <= 0
+                    unsigned sh[CH];
+#pragma unroll
+                    for (int i = 0; i < CH; i++)
+                        sh[i] = 0u;
+                    for (int k = 0; k < nv; k++) {
+                        const FEdge f = s.f[k];
+#pragma unroll
+                        for (int i = 0; i < CH; i++)
+                            sh[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cout)));
+                    }
+#pragma unroll
+                    for (int i = 0; i < CH; i++)
+                        outc |= (sh[i] >> 31) << i;
+                    outc &= undc;
+                }
             }
+            in |= inc << c0;
+            out |= outc << c0;
         }
         keep |= und & out;
         und &= ~(in | out); // certified inside => discarded
@@ -725,7 +765,7 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
 #pragma unroll
             for (int i = 0; i < NP; i++)
                 if ((disc >> i) & 1u)
-                    disc &= ~((edge_inside(s.e[k], s.exact, (double)px[i], (double)py[i]) ? 0u : 1u) << i);
+                    disc &= ~((edge_inside(s.e[k], s.eb[k], s.exact, (double)px[i], (double)py[i]) ? 0u : 1u) << i);
         }
         return keep | (und & ~disc);
     }
@@ -744,7 +784,7 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
 #pragma unroll
             for (int i = 0; i < NP; i++)
                 if ((disc >> i) & 1u)
-                    disc &= ~((edge_inside(s.e[k], 1, (double)px[i], (double)py[i]) ? 0u : 1u) << i);
+                    disc &= ~((edge_inside(s.e[k], s.eb[k], 1, (double)px[i], (double)py[i]) ? 0u : 1u) << i);
         }
     }
     return keep | (und & ~disc);
