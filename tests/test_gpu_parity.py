@@ -506,3 +506,33 @@ def test_device_hull_golden():
         d = torch.tensor(ex["points"], device=DEV)
         s = torch.tensor(ex["survivors"], dtype=torch.int64, device=DEV)
         assert list(chf.hull_gpu(d, s)) == ex["hull"], ex["name"]
+
+
+def test_parity_beyond_2pow31_points_sampled():
+    """X5: more than 2^31 points (int64 indices throughout).
+    Extremes against the oracle over all points, every survivor re-checked,
+    the survivors beyond index 2^31 checked against the oracle exactly, and
+    a random sample's decisions compared one by one."""
+    n = (1 << 31) + 12_345
+    free = torch.cuda.mem_get_info()[0]
+    if free < 70e9:
+        pytest.skip("needs ~70 GB of device memory")
+    xy_d = synth.points("displaced", n, seed=7, p=0.02, device=DEV)
+    ws = chf.Workspace(n)
+    e, o = chf.extremes8(xy_d, ws)
+    surv = chf.filter(xy_d, ws).cpu().numpy()
+    xy = xy_d.cpu().numpy()
+    del xy_d
+    torch.cuda.empty_cache()
+    idx8 = oracle.extremes8(xy)
+    assert np.array_equal(np.array(e.idx[:]), idx8)
+    wo = oracle.octagon(xy, idx8)
+    assert np.all(np.diff(surv) > 0) and surv[-1] < n
+    assert np.all(oracle.flags(xy[surv], oct_=wo) == 1)
+    tail0 = (1 << 31) - 1000
+    keep_tail = oracle.flags(xy[tail0:], oct_=wo)
+    assert np.array_equal(np.flatnonzero(keep_tail) + tail0, surv[surv >= tail0])
+    rng = np.random.default_rng(1)
+    sample = np.sort(rng.choice(n, 1_000_000, replace=False))
+    keep_s = oracle.flags(xy[sample], oct_=wo).astype(bool)
+    assert np.array_equal(np.isin(sample, surv), keep_s)
