@@ -194,9 +194,19 @@ ch_status ch_filter_f32(const float *d_xy, int64_t n, int flags, int64_t *d_surv
 ch_status ch_read_result(const void *d_ws, ch_result *h_res, void *stream);
 
 /* One filter step on device-resident input: ch_extremes8 + ch_filter_compact
- * (two kernels, no host round trip in between) + ch_read_result. */
+ * (two kernels, no host round trip in between; one kernel, K5, for n <= 4096)
+ * + ch_read_result. */
 ch_status ch_filter(const double *d_xy, int64_t n, int flags, int64_t *d_survivors,
                     int64_t *h_count, void *d_ws, size_t ws_bytes, void *stream);
+
+/* The same step without synchronizing: the count goes to *d_count (device,
+ * nullable) and to the workspace result.  For n <= 4096 (the latency-bound
+ * C1 case) the whole step runs as ONE single-CTA kernel (K5); above, K1 + K2.
+ * _f32: float32 storage. */
+ch_status ch_filter_async(const double *d_xy, int64_t n, int flags, int64_t *d_survivors,
+                          int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
+ch_status ch_filter_async_f32(const float *d_xy, int64_t n, int flags, int64_t *d_survivors,
+                              int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
 
 /* The same step end to end from HOST memory: copies h_xy (pinned for full
  * speed) into d_xy_staging (capacity n points), filters, and copies the

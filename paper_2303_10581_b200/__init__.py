@@ -178,6 +178,16 @@ def filter(xy: torch.Tensor, ws: Workspace | None = None, plain: bool = False, o
     return out[: cnt.value]
 
 
+def filter_async(xy: torch.Tensor, ws: Workspace, out: torch.Tensor, count: torch.Tensor | None = None,
+                 plain: bool = False, stream=None):
+    """One filter step without synchronizing (K5 for n <= 4096, else K1 + K2);
+    the count goes to `count` (device int64[1]) and the workspace result."""
+    lib = _lib.load()
+    xy = _points(xy)
+    _lib.check(_fn(lib, "ch_filter_async", xy)(_ptr(xy), xy.shape[0], _plain(plain), _ptr(out), _ptr(count),
+                                                ws.ptr, ws.nbytes, _stream(stream)), "ch_filter_async")
+
+
 def filter_host(h_xy: torch.Tensor, ws: Workspace, d_staging: torch.Tensor, d_out: torch.Tensor,
                 h_out: torch.Tensor, plain: bool = False, stream=None) -> int:
     """End-to-end step from host memory (H2D copy, filter, D2H survivors)."""

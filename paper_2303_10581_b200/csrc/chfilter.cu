@@ -1116,6 +1116,166 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
     }
 }
 
+// ===================================================================== K5 ==
+// Small inputs (n <= KS_MAX_N, the latency-bound C1 case): the whole step in
+// ONE CTA and one launch -- extremes (per-thread runs, block reduction),
+// octagon (build_octagon_cta), octagon test and a block-wide stable
+// compaction -- so no grid combine, no look-back, no second launch.  Same
+// results as K1 + K2 (same functions, same order of decisions).
+constexpr int KS_THREADS = 512;
+constexpr int KS_BATCH = 8;
+constexpr long long KS_MAX_N = 4096;  // measured crossover vs K1 + K2 (profiles/r01_small_n.txt)
+
+template <typename T>
+__global__ void __launch_bounds__(KS_THREADS, 1)
+k5_small_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hdr, long long *__restrict__ out,
+                long long *d_count)
+{
+    constexpr int B = KS_BATCH;                 // points per thread per batch
+    constexpr long long BP = (long long)B * KS_THREADS;
+    constexpr int NW = KS_THREADS / 32;
+    __shared__ double s_v[NW][8];
+    __shared__ long long s_i[NW][8];
+    constexpr int GPL = B * NW / 32;            // scan groups per lane
+    static_assert(B * NW % 32 == 0, "K5 group count");
+    __shared__ int s_cnt[B * NW], s_pre[B * NW], s_tot;
+    __shared__ ch_extremes s_e;
+    __shared__ ch_octagon s_o;
+    __shared__ SOct so;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long nb = (n + BP - 1) / BP;
+    // ---- extremes: batches high -> low, points loaded first, then walked
+    //      downward (">=" ties keep the lowest index) ----
+    Best bst;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        bst.v[k] = chf::slot_is_max(k) ? -CH_INF : CH_INF;
+        bst.i[k] = LLONG_MAX;
+    }
+    double acc = 0.0;
+    for (long long bi = nb - 1; bi >= 0; bi--) {
+        double px[B], py[B];
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            const long long i = bi * BP + (long long)j * KS_THREADS + tid;
+            px[j] = py[j] = 0.0;
+            if (i < n)
+                ld1pt(xy, i, px[j], py[j]);
+        }
+#pragma unroll
+        for (int j = B - 1; j >= 0; j--) {
+            const long long i = bi * BP + (long long)j * KS_THREADS + tid;
+            if (i < n)
+                k1_update(bst, px[j], py[j], i, acc);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        double v = bst.v[k];
+        long long id = bst.i[k];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double w = __shfl_xor_sync(FULL, v, off);
+            const long long j = __shfl_xor_sync(FULL, id, off);
+            reduce_pair(k, v, id, w, j);
+        }
+        if (lane == 0) {
+            s_v[warp][k] = v;
+            s_i[warp][k] = id;
+        }
+    }
+    const int nf = __syncthreads_or(acc != acc);
+    if (tid < 8) {
+        const int k = tid;
+        double bv = s_v[0][k];
+        long long bi = s_i[0][k];
+        for (int w = 1; w < NW; w++)
+            reduce_pair(k, bv, bi, s_v[w][k], s_i[w][k]);
+        s_e.idx[k] = bi;
+        s_e.x[k] = (double)xy[2 * bi];
+        s_e.y[k] = (double)xy[2 * bi + 1];
+    }
+    __syncthreads();
+    build_octagon_cta(s_e, flags, s_o);
+    load_soct(so, &s_o);
+    __syncthreads();
+    // ---- octagon test + stable compaction: per batch, groups (j, warp) of
+    //      32 consecutive points, block scan of their popcounts ----
+    long long base_out = 0;
+    for (long long bi = 0; bi < nb; bi++) {
+        double px[B], py[B];
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            const long long i = bi * BP + (long long)j * KS_THREADS + tid;
+            px[j] = py[j] = 0.0;
+            if (i < n)
+                ld1pt(xy, i, px[j], py[j]);
+        }
+        unsigned m[B];
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            const long long i = bi * BP + (long long)j * KS_THREADS + tid;
+            const bool k = i < n && (so.degenerate || keep_point(so, px[j], py[j]));
+            m[j] = __ballot_sync(FULL, k);
+            if (lane == 0)
+                s_cnt[j * NW + warp] = __popc(m[j]);
+        }
+        __syncthreads();
+        // exclusive prefix of the B * NW group counts (index order: j, warp),
+        // one warp scan: lane l owns groups [GPL*l, GPL*l + GPL)
+        if (warp == 0) {
+            int c[GPL], run = 0;
+#pragma unroll
+            for (int t = 0; t < GPL; t++) {
+                c[t] = s_cnt[lane * GPL + t];
+                run += c[t];
+            }
+            int inc = run;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int v = __shfl_up_sync(FULL, inc, off);
+                if (lane >= off)
+                    inc += v;
+            }
+            int ex = inc - run;
+#pragma unroll
+            for (int t = 0; t < GPL; t++) {
+                s_pre[lane * GPL + t] = ex;
+                ex += c[t];
+            }
+            if (lane == 31)
+                s_tot = inc;
+        }
+        __syncthreads();
+        const int tot = s_tot;
+        const unsigned lt = lanemask_lt();
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            const int pre = s_pre[j * NW + warp];
+            if ((m[j] >> lane) & 1u)
+                out[base_out + pre + __popc(m[j] & lt)] = bi * BP + (long long)j * KS_THREADS + tid;
+        }
+        base_out += tot;
+        __syncthreads();
+    }
+    // ---- publish (the same workspace fields K1/K2 write) ----
+    const unsigned *src = (const unsigned *)&s_o;
+    unsigned *dst = (unsigned *)&hdr->oct;
+    for (int q = tid; q < (int)(sizeof(ch_octagon) / 4); q += KS_THREADS)
+        dst[q] = src[q];
+    const unsigned *se = (const unsigned *)&s_e;
+    unsigned *de = (unsigned *)&hdr->ext;
+    for (int q = tid; q < (int)(sizeof(ch_extremes) / 4); q += KS_THREADS)
+        de[q] = se[q];
+    if (tid == 0) {
+        hdr->result.count = base_out;
+        hdr->result.nonfinite = nf;
+        hdr->result.degenerate = s_o.degenerate;
+        if (d_count)
+            *d_count = base_out;
+    }
+}
+
 // ===================================================================== K4 ==
 __global__ void __launch_bounds__(K4_THREADS)
 k4_octagon_bits(const double *__restrict__ xy, long long n, const ch_octagon *__restrict__ oct,
@@ -1302,6 +1462,9 @@ ch_status filter_compact_impl(const T *d_xy, int64_t n, int64_t index_base, cons
 template <typename T>
 ch_status filter_impl(const T *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *h_count, void *d_ws,
                       size_t ws_bytes, void *stream);
+template <typename T>
+ch_status filter_async_impl(const T *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *d_count, void *d_ws,
+                            size_t ws_bytes, void *stream);
 
 } // namespace
 
@@ -1411,14 +1574,35 @@ ch_status filter_compact_impl(const T *d_xy, int64_t n, int64_t index_base, cons
     return launch_k2(d_xy, n, index_base, d_oct, (long long *)d_survivors, (long long *)d_count, d_ws, st);
 }
 
+// One step, asynchronous: K5 (one CTA, one launch) for small n, else K1 + K2.
+template <typename T>
+ch_status filter_async_impl(const T *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *d_count, void *d_ws,
+                            size_t ws_bytes, void *stream)
+{
+    if (n <= KS_MAX_N) {
+        ch_status s = check_points(d_xy, n);
+        if (s != CH_OK)
+            return s;
+        if (!d_survivors)
+            return fail(CH_ERR_INVALID_ARG, "d_survivors is NULL");
+        if ((s = check_ws(d_ws, ws_bytes, n)) != CH_OK)
+            return s;
+        k5_small_filter<T><<<1, KS_THREADS, 0, (cudaStream_t)stream>>>(d_xy, n, flags, hdr_of(d_ws),
+                                                                       (long long *)d_survivors, (long long *)d_count);
+        return cuda_check("k5_small_filter");
+    }
+    ch_status s = extremes8_impl(d_xy, n, 0, flags, nullptr, nullptr, nullptr, d_ws, ws_bytes, stream);
+    if (s != CH_OK)
+        return s;
+    return filter_compact_impl(d_xy, n, 0, nullptr, d_survivors, d_count, d_ws, ws_bytes, stream);
+}
+
 template <typename T>
 ch_status filter_impl(const T *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *h_count, void *d_ws,
                       size_t ws_bytes, void *stream)
 {
-    ch_status s = extremes8_impl(d_xy, n, 0, flags, nullptr, nullptr, nullptr, d_ws, ws_bytes, stream);
+    ch_status s = filter_async_impl(d_xy, n, flags, d_survivors, (int64_t *)nullptr, d_ws, ws_bytes, stream);
     if (s != CH_OK)
-        return s;
-    if ((s = filter_compact_impl(d_xy, n, 0, nullptr, d_survivors, nullptr, d_ws, ws_bytes, stream)) != CH_OK)
         return s;
     ch_result r;
     s = ch_read_result(d_ws, &r, stream);
@@ -1490,6 +1674,18 @@ ch_status ch_filter(const double *d_xy, int64_t n, int flags, int64_t *d_survivo
                     void *d_ws, size_t ws_bytes, void *stream)
 {
     return filter_impl(d_xy, n, flags, d_survivors, h_count, d_ws, ws_bytes, stream);
+}
+
+ch_status ch_filter_async(const double *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *d_count,
+                          void *d_ws, size_t ws_bytes, void *stream)
+{
+    return filter_async_impl(d_xy, n, flags, d_survivors, d_count, d_ws, ws_bytes, stream);
+}
+
+ch_status ch_filter_async_f32(const float *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *d_count,
+                              void *d_ws, size_t ws_bytes, void *stream)
+{
+    return filter_async_impl(d_xy, n, flags, d_survivors, d_count, d_ws, ws_bytes, stream);
 }
 
 ch_status ch_filter_f32(const float *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *h_count,

@@ -536,3 +536,28 @@ def test_parity_beyond_2pow31_points_sampled():
     sample = np.sort(rng.choice(n, 1_000_000, replace=False))
     keep_s = oracle.flags(xy[sample], oct_=wo).astype(bool)
     assert np.array_equal(np.isin(sample, surv), keep_s)
+
+
+@pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
+def test_small_n_single_kernel_equals_two_kernels(dist):
+    """K5 (one CTA, n <= 4096) against K1 + K2 and the oracle, f64 and f32,
+    all predicate modes."""
+    for n in (1, 5, 1023, 1024, 1025, 4095, 4096):
+        for storage in ("f64", "f32"):
+            xy_d = synth.points(dist, n, seed=n, device=DEV)
+            if storage == "f32":
+                xy_d = xy_d.float()
+            xy = xy_d.double().cpu().numpy()
+            for mode in (False, True, "exact"):
+                ws = chf.Workspace(n)
+                k5 = chf.filter(xy_d, ws, plain=mode).cpu().numpy()          # K5
+                ws2 = chf.Workspace(n)
+                chf.extremes8_async(xy_d, ws2, plain=mode)
+                out = chf.filter_compact(xy_d, ws2)                          # K1 + K2
+                k12 = out[: chf.read_result(ws2).count].cpu().numpy()
+                if mode == "exact":
+                    want, _ = oracle.filter_compact_exact(xy)
+                else:
+                    want, _ = oracle.filter_compact(xy, certified=not mode)
+                assert np.array_equal(k5, want), (dist, n, storage, mode)
+                assert np.array_equal(k12, want), (dist, n, storage, mode)
