@@ -425,6 +425,8 @@ def run_ours(a):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * K, "clocks": clk.summary(),
             "exchange_ms": ex_ms if world > 1 else 0.0,
+            "ctas_per_sm": {"k1": chf._lib.load().ch_occupancy(0),
+                            "k2": chf._lib.load().ch_occupancy(2 if a.storage == "f32" else 1)},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -132,6 +132,13 @@ int ch_abi_version(void);
 const char *ch_status_str(ch_status s);
 const char *ch_last_error(void); /* thread-local, valid until the next call */
 
+/* Diagnostics: resident CTAs per SM the streaming kernels launch with, from
+ * the CUDA occupancy API on the current device (kernel 0 = K1, 1 = K2 on
+ * float64 points, 2 = K2 on float32 points).  K1 runs 3 and K2 2 per SM by
+ * design; a smaller number means a resource regression.
+ * Returns < 0 for an unknown kernel or a CUDA error. */
+int ch_occupancy(int kernel);
+
 /* Bytes of workspace needed for inputs of up to n points. */
 size_t ch_workspace_bytes(int64_t n);
 /* Zero-fill a workspace (once, before first use).  Async on `stream`. */

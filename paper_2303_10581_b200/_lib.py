@@ -51,6 +51,7 @@ SIGNATURES = {
     "ch_abi_version": (ctypes.c_int, []),
     "ch_status_str": (ctypes.c_char_p, [ctypes.c_int]),
     "ch_last_error": (ctypes.c_char_p, []),
+    "ch_occupancy": (ctypes.c_int, [ctypes.c_int]),
     "ch_workspace_bytes": (SZ, [I64]),
     "ch_workspace_init": (ctypes.c_int, [P, SZ, P]),
     "ch_extremes8": (ctypes.c_int, [P, I64, I64, ctypes.c_int, P, ctypes.POINTER(Extremes),

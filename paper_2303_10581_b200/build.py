@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [nvcc(), *ARCH, *NVFLAGS, "-shared", "-o", tmp,
+    extra = os.environ.get("CH_NVCC_EXTRA", "").split()  # developer experiments only
+    cmd = [nvcc(), *ARCH, *NVFLAGS, *extra, "-shared", "-o", tmp,
            *[os.path.join(CSRC, s) for s in SOURCES], "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

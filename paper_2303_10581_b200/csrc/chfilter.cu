@@ -540,8 +540,8 @@ struct __align__(16) FEdge {
 };
 struct SOct {
     SEdge e[8];
-    double2 eb[8]; // edge end points (exact mode only)
     FEdge f[8];
+    FEdge fg[8];   // f[guess[oct]] by the code (dy<0)<<2 | (dx<0)<<1 | (|dx|<|dy|)
     double box[4];
     float boxf[4]; // float bounds with x >= boxf[0] <=> (double)x >= box[0], etc.
     double cx, cy;
@@ -558,14 +558,19 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.e[t].ex = o->ex[t];
         s.e[t].ey = o->ey[t];
         s.e[t].thr = o->thr[t];
-        const int t1 = (t + 1 < o->nv) ? t + 1 : 0;
-        s.eb[t] = make_double2(o->vx[t1], o->vy[t1]);
         s.e[t].pad = 0.0;
         s.guess[t] = o->guess_edge[t];
         s.f[t].a = o->f32_a[t];
         s.f[t].b = o->f32_b[t];
         s.f[t].cin = o->f32_cin[t];
         s.f[t].cout = o->f32_cout[t];
+        // code bits (sy, sx, |dx| < |dy|) -> octant of the 2' stage
+        const int oct_of_code[8] = {0, 1, 3, 2, 7, 6, 4, 5};
+        const int g = o->guess_edge[oct_of_code[t]];
+        s.fg[t].a = o->f32_a[g];
+        s.fg[t].b = o->f32_b[g];
+        s.fg[t].cin = o->f32_cin[g];
+        s.fg[t].cout = o->f32_cout[g];
     } else if (t == 8) {
         s.box[0] = o->box[0];
         s.box[1] = o->box[1];
@@ -584,13 +589,22 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
     }
 }
 
+// The exact expansion stage, out of line: it is cold (exact mode, points
+// within a few ulps of an edge), and inlining it into the unrolled loops
+// made most of K2's code.
+__device__ __noinline__ int exact_stage(double ax, double ay, double bx, double by, double x, double y)
+{
+    return chf::orient_sign_exact_stage(ax, ay, bx, by, x, y);
+}
+
 // One edge in fp64: true if the point is certainly "inside" for this edge.
 // Certified / plain modes: D_k > T_k (the definition, R4).  Exact mode (f3):
 // the exact orientation is > 0 -- decided by Shewchuk's per-point bound
 // (3 + 16 eps) eps (|l| + |r|) on the same D_k, else by exact expansion
 // arithmetic (chf::orient_sign_exact_stage).
-__device__ __forceinline__ bool edge_inside(const SEdge &e, const double2 &b, int exact, double x, double y)
+__device__ __forceinline__ bool edge_inside(const SOct &s, int k, int exact, double x, double y)
 {
+    const SEdge &e = s.e[k];
     const double dy = __dsub_rn(y, e.ay), dx = __dsub_rn(x, e.ax);
     const double l = __dmul_rn(e.ex, dy), r = __dmul_rn(e.ey, dx);
     const double D = __dsub_rn(l, r);
@@ -601,7 +615,8 @@ __device__ __forceinline__ bool edge_inside(const SEdge &e, const double2 &b, in
         return true;
     if (-D > eb)
         return false;
-    return chf::orient_sign_exact_stage(e.ax, e.ay, b.x, b.y, x, y) > 0;
+    const int k1 = k + 1 < s.nv ? k + 1 : 0; // the edge's end point: the next vertex
+    return exact_stage(e.ax, e.ay, s.e[k1].ax, s.e[k1].ay, x, y) > 0;
 }
 
 // Survivor test, bit-identical to "not (forall k: D_k > T_k)" (R4): the
@@ -621,7 +636,7 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
         int off = (t & 1) ? ((t + 1) >> 1) : -(t >> 1);
         int k = g + off;
         k = k < 0 ? k + nv : (k >= nv ? k - nv : k);
-        if (!edge_inside(s.e[k], s.eb[k], s.exact, x, y))
+        if (!edge_inside(s, k, s.exact, x, y))
             return true;
     }
     return false;
@@ -632,15 +647,15 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
 // skipped when no lane of the warp needs it (warp-uniform branches):
 //  1. the certified accept box (4 DSETP): inside => discarded (proof at
 //     chf::box_corner_ok);
-//  2. (has_f32) the fp32 pre-filter (proof at chf::octagon_edge): g_k >= 0 on
-//     every edge certifies discard; then h_k <= 0 certifies keep, tried on
-//     the octant-guessed edge first and on every edge only if needed; then
+//  2. (has_f32) the fp32 pre-filter (proof at chf::octagon_edge): h_g <= 0
+//     on the octant-guessed edge certifies keep; then g_k >= 0 on every edge
+//     certifies discard; then h_k <= 0 on some edge certifies keep (these
+//     two with two points per FFMA2);
 //  3. fp64 D_k on every edge for the points left in the uncertainty band.
-// Before stage 2, adaptively: 2'. the guessed edge of the point's octant
-// (D_g <= T_g => kept, the oracle's exists-k condition); a warp whose
-// points 2' did not settle skips 2' for the next 15 sub-tiles.  Without
-// has_f32 (caller-supplied octagon) stage 3 runs on every edge of every
-// undecided point.
+// Without has_f32 (caller-supplied octagon), instead of stage 2, adaptively:
+// 2'. the guessed edge in fp64 (D_g <= T_g => kept, the oracle's exists-k
+// condition; a warp whose points 2' did not settle skips 2' for the next 15
+// sub-tiles), then stage 3 on every edge of every undecided point.
 template <typename C, int NP>
 __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], const C (&py)[NP],
                                              unsigned valid, int &guess_mode)
@@ -661,7 +676,9 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
         return 0u;
     const int nv = s.nv;
     unsigned keep = 0;
-    if (guess_mode <= 0) {
+    // With has_f32 the fp32 guessed-edge keep certificate (B) replaces 2'
+    // (measured faster for both storages, profiles/r01_k2_stage_order.txt).
+    if (!s.has_f32 && guess_mode <= 0) {
         // 2'. the guessed edge of the point's octant: D_g <= T_g => kept
 #pragma unroll
         for (int i = 0; i < NP; i++) {
@@ -682,74 +699,105 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
     }
     guess_mode--;
     if (s.has_f32) {
-        // fp32 certification on every edge: OR the sign bits of g_k (any
-        // g_k < 0 or -0 => not certified inside) and of h_k (any h_k <= -0
-        // => certified outside).  Proof at chf::octagon_edge.
+        // fp32 certification (proof at chf::octagon_edge), chunk by chunk:
+        //  B. keep certificate on the octant-guessed edge: h_g <= -0;
+        //  A. inside certificate on every edge: all g_k >= +0 (the sign bits
+        //     of the g_k OR-ed);
+        //  C. keep certificate on any edge: some h_k <= -0.
+        // Two points per FFMA2 in A and C (fma.rn.f32x2: each half is one
+        // correctly rounded fma, bit-identical to the scalar __fmaf_rn chain).
         unsigned in = 0, out = 0;
-        constexpr int CH = NP < 4 ? NP : 4; // points per pass (bounds register use)
-        const float cxf = (float)s.cx, cyf = (float)s.cy;
+        constexpr int CH = sizeof(C) == 4 ? 4 : 8; // points per pass (bounds register use)
+        static_assert(CH % 2 == 0, "points are processed in pairs");
+        const float2 mc = make_float2(-(float)s.cx, -(float)s.cy);
 #pragma unroll
         for (int c0 = 0; c0 < NP; c0 += CH) {
-            float xf[CH], yf[CH];
+            unsigned undc = (und >> c0) & ((1u << CH) - 1u);
+            if (!__any_sync(FULL, undc))
+                continue;
+            float2 X[CH / 2], Y[CH / 2];
             unsigned sg[CH];
 #pragma unroll
-            for (int i = 0; i < CH; i++) {
-                xf[i] = (float)px[c0 + i]; // exact for float storage
-                yf[i] = (float)py[c0 + i];
-                sg[i] = 0u;
+            for (int q = 0; q < CH / 2; q++) {
+                X[q] = make_float2((float)px[c0 + 2 * q], (float)px[c0 + 2 * q + 1]); // exact for float storage
+                Y[q] = make_float2((float)py[c0 + 2 * q], (float)py[c0 + 2 * q + 1]);
             }
-            // A. inside certificate on every edge: all g_k >= 0
-            if (nv == 8) {
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    const FEdge f = s.f[k];
-#pragma unroll
-                    for (int i = 0; i < CH; i++)
-                        sg[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cin)));
-                }
-            } else {
-                for (int k = 0; k < nv; k++) {
-                    const FEdge f = s.f[k];
-#pragma unroll
-                    for (int i = 0; i < CH; i++)
-                        sg[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cin)));
-                }
-            }
-            unsigned inc = 0;
-#pragma unroll
-            for (int i = 0; i < CH; i++)
-                inc |= ((~sg[i]) >> 31) << i;
-            unsigned undc = ((und >> c0) & ((1u << CH) - 1u)) & ~inc;
+            // B. the octant-guessed edge (any edge is sound for "keep")
             unsigned outc = 0;
-            if (__any_sync(FULL, undc)) {
-                // B. keep certificate on the octant-guessed edge: h_g <= 0
 #pragma unroll
-                for (int i = 0; i < CH; i++) {
-                    const float dx = xf[i] - cxf, dy = yf[i] - cyf;
-                    const bool c = fabsf(dx) >= fabsf(dy);
-                    const int oct = dy >= 0.0f ? (dx >= 0.0f ? (c ? 0 : 1) : (c ? 3 : 2))
-                                               : (dx < 0.0f ? (c ? 4 : 5) : (c ? 7 : 6));
-                    const FEdge f = s.f[s.guess[oct]];
-                    const float h = __fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cout));
-                    outc |= (__float_as_uint(h) >> 31) << i;
+            for (int q = 0; q < CH / 2; q++) {
+                const float2 dx = __fadd2_rn(X[q], make_float2(mc.x, mc.x));
+                const float2 dy = __fadd2_rn(Y[q], make_float2(mc.y, mc.y));
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const unsigned ux = __float_as_uint(h ? dx.y : dx.x), uy = __float_as_uint(h ? dy.y : dy.x);
+                    const unsigned code = ((uy >> 31) << 2) | ((ux >> 31) << 1) |
+                                          ((ux & 0x7fffffffu) < (uy & 0x7fffffffu) ? 1u : 0u);
+                    const FEdge f = s.fg[code];
+                    const float x = h ? X[q].y : X[q].x, y = h ? Y[q].y : Y[q].x;
+                    const float hv = __fmaf_rn(f.a, x, __fmaf_rn(f.b, y, f.cout));
+                    outc |= (__float_as_uint(hv) >> 31) << (2 * q + h);
                 }
-                outc &= undc;
-                if (__any_sync(FULL, undc & ~outc)) {
-                    // C. keep certificate on any edge: some h_k <= 0
-                    unsigned sh[CH];
+            }
+            outc &= undc;
+            undc &= ~outc;
+            unsigned inc = 0;
+            if (__any_sync(FULL, undc)) {
+                // A. inside certificate on every edge
 #pragma unroll
-                    for (int i = 0; i < CH; i++)
-                        sh[i] = 0u;
-                    for (int k = 0; k < nv; k++) {
-                        const FEdge f = s.f[k];
+                for (int i = 0; i < CH; i++)
+                    sg[i] = 0u;
+                auto edge_in = [&](const FEdge &f) {
+                    const float2 a = make_float2(f.a, f.a), b = make_float2(f.b, f.b),
+                                 c = make_float2(f.cin, f.cin);
 #pragma unroll
-                        for (int i = 0; i < CH; i++)
-                            sh[i] |= __float_as_uint(__fmaf_rn(f.a, xf[i], __fmaf_rn(f.b, yf[i], f.cout)));
+                    for (int q = 0; q < CH / 2; q++) {
+                        const float2 g = __ffma2_rn(a, X[q], __ffma2_rn(b, Y[q], c));
+                        sg[2 * q] |= __float_as_uint(g.x);
+                        sg[2 * q + 1] |= __float_as_uint(g.y);
                     }
+                };
+                if (nv == 8) {
+#pragma unroll
+                    for (int k = 0; k < 8; k++)
+                        edge_in(s.f[k]);
+                } else {
+                    for (int k = 0; k < nv; k++)
+                        edge_in(s.f[k]);
+                }
+#pragma unroll
+                for (int i = 0; i < CH; i++)
+                    inc |= ((~sg[i]) >> 31) << i;
+                inc &= undc;
+                undc &= ~inc;
+                if (__any_sync(FULL, undc)) {
+                    // C. keep certificate on any edge
 #pragma unroll
                     for (int i = 0; i < CH; i++)
-                        outc |= (sh[i] >> 31) << i;
-                    outc &= undc;
+                        sg[i] = 0u;
+                    auto edge_out = [&](const FEdge &f) {
+                        const float2 a = make_float2(f.a, f.a), b = make_float2(f.b, f.b),
+                                     c = make_float2(f.cout, f.cout);
+#pragma unroll
+                        for (int q = 0; q < CH / 2; q++) {
+                            const float2 h = __ffma2_rn(a, X[q], __ffma2_rn(b, Y[q], c));
+                            sg[2 * q] |= __float_as_uint(h.x);
+                            sg[2 * q + 1] |= __float_as_uint(h.y);
+                        }
+                    };
+                    if (nv == 8) {
+#pragma unroll
+                        for (int k = 0; k < 8; k++)
+                            edge_out(s.f[k]);
+                    } else {
+                        for (int k = 0; k < nv; k++)
+                            edge_out(s.f[k]);
+                    }
+                    unsigned o2 = 0;
+#pragma unroll
+                    for (int i = 0; i < CH; i++)
+                        o2 |= (sg[i] >> 31) << i;
+                    outc |= o2 & undc;
                 }
             }
             in |= inc << c0;
@@ -765,7 +813,7 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
 #pragma unroll
             for (int i = 0; i < NP; i++)
                 if ((disc >> i) & 1u)
-                    disc &= ~((edge_inside(s.e[k], s.eb[k], s.exact, (double)px[i], (double)py[i]) ? 0u : 1u) << i);
+                    disc &= ~((edge_inside(s, k, s.exact, (double)px[i], (double)py[i]) ? 0u : 1u) << i);
         }
         return keep | (und & ~disc);
     }
@@ -784,7 +832,7 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
 #pragma unroll
             for (int i = 0; i < NP; i++)
                 if ((disc >> i) & 1u)
-                    disc &= ~((edge_inside(s.e[k], s.eb[k], 1, (double)px[i], (double)py[i]) ? 0u : 1u) << i);
+                    disc &= ~((edge_inside(s, k, 1, (double)px[i], (double)py[i]) ? 0u : 1u) << i);
         }
     }
     return keep | (und & ~disc);
@@ -919,22 +967,31 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
         // Survivors of the super-tile held in buffer bb, written by every
         // consumer warp for its own 32-point groups, once the publisher has
         // resolved the super-tile's global offset.
+        // Group e of a super-tile holds its points [32 e, 32 e + 32) (e =
+        // (j * K2_NP + u) * K2_CWARPS + warp), so warp w writes the contiguous
+        // groups [w E / 8, (w + 1) E / 8), four per step, branch-free.
         auto write_survivors = [&](int bb) {
             bar_sync(K2_BAR_BASE + 2 + bb, K2_CTHREADS + 32); // offset of buffer bb is known
             if (s_total[bb] > 0) {
-                const long long sbase = (long long)s_tile[bb] * super_pts + index_base;
-                const long long excl = s_excl[bb];
-                const unsigned *bw = bits + bb * K2_ENTRIES;
-                const int *sc = gscan + bb * K2_ENTRIES;
-                const int E = s_nsub[bb] * K2_GROUPS;
-                for (int e = warp; e < E; e += K2_CWARPS) {
-                    const unsigned m = bw[e];
-                    if (m == 0u)
+                const int E = s_nsub[bb] * K2_GROUPS, per = E / K2_CWARPS, e0 = warp * per;
+                long long *ob = out + s_excl[bb];
+                long long v = (long long)s_tile[bb] * super_pts + index_base + 32LL * e0 + lane;
+                const uint4 *bw = (const uint4 *)(bits + bb * K2_ENTRIES + e0);
+                const int4 *sc = (const int4 *)(gscan + bb * K2_ENTRIES + e0);
+                const unsigned lb = 1u << lane;
+                for (int q = 0; q < per / 4; q++, v += 128) {
+                    const uint4 m = bw[q];
+                    if ((m.x | m.y | m.z | m.w) == 0u)
                         continue;
-                    const int u = (e / K2_CWARPS) % K2_NP, jj = e / K2_GROUPS;
-                    if ((m >> lane) & 1u)
-                        out[excl + sc[e] + __popc(m & lt)] =
-                            sbase + (long long)jj * K2_SUB + u * K2_CTHREADS + 32 * warp + lane;
+                    const int4 c = sc[q];
+                    if (m.x & lb)
+                        ob[c.x + __popc(m.x & lt)] = v;
+                    if (m.y & lb)
+                        ob[c.y + __popc(m.y & lt)] = v + 32;
+                    if (m.z & lb)
+                        ob[c.z + __popc(m.z & lt)] = v + 64;
+                    if (m.w & lb)
+                        ob[c.w + __popc(m.w & lt)] = v + 96;
                 }
             }
         };
@@ -1472,6 +1529,19 @@ ch_status filter_async_impl(const T *d_xy, int64_t n, int flags, int64_t *d_surv
 extern "C" {
 
 int ch_abi_version(void) { return CH_ABI_VERSION; }
+
+int ch_occupancy(int kernel)
+{
+    const DevInfo d = dev_info();
+    if (cudaGetLastError() != cudaSuccess)
+        return -1;
+    switch (kernel) {
+    case 0: return d.k1_per_sm;
+    case 1: return d.k2_per_sm_d;
+    case 2: return d.k2_per_sm_f;
+    default: return -1;
+    }
+}
 
 const char *ch_status_str(ch_status s)
 {

@@ -37,6 +37,17 @@ def check_against_oracle(xy_d, plain=False, ws=None, name=""):
     return surv, ws
 
 
+def test_kernels_launch_at_design_occupancy():
+    """K1 3 CTAs/SM, K2 2 CTAs/SM: a few bytes more of
+    static shared memory or registers silently halve K2's residency."""
+    lib = chf._lib.load()
+    torch.zeros(1, device=DEV)
+    assert lib.ch_occupancy(0) >= 3
+    assert lib.ch_occupancy(1) == 2
+    assert lib.ch_occupancy(2) == 2
+    assert lib.ch_occupancy(7) < 0
+
+
 # ------------------------------------------------------------- golden -------
 @pytest.mark.parametrize("ex", load_golden(), ids=[g["name"] for g in load_golden()])
 def test_golden_on_gpu(ex):
