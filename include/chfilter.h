@@ -245,6 +245,13 @@ ch_status ch_hull_points(const double *h_pts, const int64_t *h_ids, int64_t m,
 size_t ch_hull_gpu_temp_bytes(int64_t m);
 ch_status ch_hull_gpu(const double *d_xy, const int64_t *d_surv, int64_t m, int64_t *h_hull,
                       int64_t *h_n_hull, void *d_tmp, size_t tmp_bytes, void *stream);
+/* The same hull kept on the device ("avoiding unnecessary data copying
+ * between the device and host"): ids to d_hull (device, capacity m), the
+ * count to *d_n_hull (device int64).  Fully asynchronous on `stream`; d_tmp
+ * (ch_hull_gpu_temp_bytes(m)) must stay untouched until the stream reaches
+ * this point.  m == 0 writes a zero count. */
+ch_status ch_hull_gpu_async(const double *d_xy, const int64_t *d_surv, int64_t m, int64_t *d_hull,
+                            int64_t *d_n_hull, void *d_tmp, size_t tmp_bytes, void *stream);
 
 #define CH_HULL_HOST 4 /* flag for ch_hull_end_to_end: gather + host monotone chain */
 
@@ -252,7 +259,10 @@ ch_status ch_hull_gpu(const double *d_xy, const int64_t *d_surv, int64_t m, int6
  * the exact hull of the survivors -- on the device (ch_hull_gpu, default)
  * or, with flags & CH_HULL_HOST, gathered to the host and computed there
  * (ch_hull_points).  Stage times go to h_stats (nullable).  h_hull capacity
- * >= number of survivors (<= n). */
+ * >= number of survivors (<= n).  Device-hull scratch: when ws_bytes >=
+ * ch_hull_workspace_bytes(n) it is the tail of d_ws (no allocation);
+ * otherwise it is taken with cudaMallocAsync for the call. */
+size_t ch_hull_workspace_bytes(int64_t n); /* filter workspace + device-hull scratch */
 ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *d_survivors,
                              int64_t *h_n_survivors, int64_t *h_hull, int64_t *h_n_hull,
                              ch_stats *h_stats, void *d_ws, size_t ws_bytes, void *stream);

@@ -62,12 +62,15 @@ def _fn(lib, name: str, xy: torch.Tensor):
 
 
 class Workspace:
-    """Caller-owned scratch of ch_workspace_bytes(n) bytes, zero-filled once."""
+    """Caller-owned scratch of ch_workspace_bytes(n) bytes, zero-filled once.
+    hull=True sizes it for ch_hull_end_to_end's device hull too
+    (ch_hull_workspace_bytes), so that call allocates nothing."""
 
-    def __init__(self, n: int, device=None, stream=None):
+    def __init__(self, n: int, device=None, stream=None, hull: bool = False):
         lib = _lib.load()
         self.capacity = int(n)
-        self.nbytes = int(lib.ch_workspace_bytes(self.capacity))
+        self.hull = bool(hull)
+        self.nbytes = int(lib.ch_hull_workspace_bytes(self.capacity) if hull else lib.ch_workspace_bytes(self.capacity))
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.buf = torch.zeros(self.nbytes, dtype=torch.uint8, device=dev)
 
@@ -237,26 +240,46 @@ def hull_gpu(xy: torch.Tensor, surv: torch.Tensor, stream=None) -> np.ndarray:
     return out[: h.value].copy()
 
 
+def hull_gpu_async(xy: torch.Tensor, surv: torch.Tensor, tmp: torch.Tensor | None = None, stream=None):
+    """f1 without host round trip: (hull ids, count) as device int64 tensors
+    (the ids valid up to the count).  `tmp`: uint8 device scratch of
+    ch_hull_gpu_temp_bytes(len(surv)) bytes (allocated if None)."""
+    lib = _lib.load()
+    xy = _points(xy)
+    m = int(surv.shape[0])
+    tb = int(lib.ch_hull_gpu_temp_bytes(m))
+    if tmp is None or tmp.numel() < tb:
+        tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=xy.device)
+    ids = torch.empty(max(m, 1), dtype=torch.int64, device=xy.device)
+    cnt = torch.empty(1, dtype=torch.int64, device=xy.device)
+    _lib.check(lib.ch_hull_gpu_async(_ptr(xy), _ptr(surv), m, _ptr(ids), _ptr(cnt), _ptr(tmp), tb, _stream(stream)),
+               "ch_hull_gpu_async")
+    return ids, cnt
+
+
 def hull_end_to_end(xy: torch.Tensor, ws: Workspace | None = None, plain: bool = False,
                     out: torch.Tensor | None = None, stream=None, host_hull: bool = False):
     """Algorithm 1: filter on the GPU, then the exact hull of the
     survivors on the device (default, f1) or on the host (host_hull=True).
-    Returns (hull ids np.ndarray, survivors tensor, Stats)."""
+    Returns (hull ids np.ndarray, survivors tensor, Stats).  A workspace made
+    with Workspace(n, hull=True) also holds the device hull's scratch."""
     lib = _lib.load()
     xy = _points(xy)
     if xy.dtype != torch.float64:
         raise TypeError("hull_end_to_end takes float64 points")
     n = xy.shape[0]
-    ws = _ws(ws, n, xy.device)
+    ws = ws.ensure(n) if ws is not None else Workspace(max(n, 1), device=xy.device, hull=not host_hull)
     if out is None:
         out = torch.empty(max(n, 1), dtype=torch.int64, device=xy.device)
-    hull = np.zeros(max(n, 1), dtype=np.int64)
+    # pinned (page-locked, cached by torch) so the hull ids come back at full PCIe speed
+    hull_t = torch.empty(max(n, 1), dtype=torch.int64, pin_memory=True)
+    hull = hull_t.numpy()
     ns, nh, st = ctypes.c_int64(0), ctypes.c_int64(0), Stats()
     flags = _plain(plain) | (_lib.CH_HULL_HOST if host_hull else 0)
     _lib.check(lib.ch_hull_end_to_end(_ptr(xy), n, flags, _ptr(out), ctypes.byref(ns),
                                       hull.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nh), ctypes.byref(st),
                                       ws.ptr, ws.nbytes, _stream(stream)), "ch_hull_end_to_end")
-    return hull[: nh.value].copy(), out[: ns.value], st
+    return hull[: nh.value], out[: ns.value], st  # a view of the pinned buffer (no 0.8 GB copy)
 
 
 def orient_sign(a, b, c) -> int:

@@ -1811,6 +1811,13 @@ ch_status ch_hull_points(const double *h_pts, const int64_t *h_ids, int64_t m, i
     return CH_OK;
 }
 
+static size_t ws_tail_offset(int64_t n) { return (ch_workspace_bytes(n) + 255) & ~(size_t)255; }
+
+size_t ch_hull_workspace_bytes(int64_t n)
+{
+    return ws_tail_offset(n) + ch_hull_gpu_temp_bytes(n < 1 ? 1 : n);
+}
+
 ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *h_n_survivors,
                              int64_t *h_hull, int64_t *h_n_hull, ch_stats *h_stats, void *d_ws, size_t ws_bytes,
                              void *stream)
@@ -1841,12 +1848,15 @@ ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *
     int64_t h = 0;
     if (!(flags & CH_HULL_HOST)) {
         // f1: the hull on the device; only the hull ids come back
-        const size_t tb = ch_hull_gpu_temp_bytes(cnt);
-        void *d_tmp = nullptr;
-        if (cudaMallocAsync(&d_tmp, tb, st) != cudaSuccess)
+        // scratch: the workspace tail when the caller sized it for the hull
+        const size_t off = ws_tail_offset(n), tb = ch_hull_gpu_temp_bytes(cnt);
+        const bool tail = ws_bytes >= off + tb;
+        void *d_tmp = tail ? (void *)((char *)d_ws + off) : nullptr;
+        if (!tail && cudaMallocAsync(&d_tmp, tb, st) != cudaSuccess)
             return fail(CH_ERR_CUDA, "cudaMallocAsync for the device hull failed");
         s = ch_hull_gpu(d_xy, d_survivors, cnt, h_hull, &h, d_tmp, tb, stream);
-        cudaFreeAsync(d_tmp, st);
+        if (!tail)
+            cudaFreeAsync(d_tmp, st);
         cudaStreamSynchronize(st);
         if (s != CH_OK)
             return fail(s, "ch_hull_gpu failed");

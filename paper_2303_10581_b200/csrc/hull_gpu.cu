@@ -161,12 +161,25 @@ __global__ void k_merge_copy(long long m_cap, long long nchunks, long long w, co
     }
 }
 
-__global__ void k_assemble(long long m, const long long *__restrict__ low, long long nl, const long long *__restrict__ up,
-                           long long nu, const long long *__restrict__ val, long long *__restrict__ out)
+// lower[0 .. nl-1) then upper[0 .. nu-1) (each excludes its last point,
+// which is the other's first); upper positions are in reversed order.  The
+// chain lengths are read on the device, so nothing waits for the host.
+__global__ void k_assemble(long long m, const long long *__restrict__ low, const long long *__restrict__ d_nl,
+                           const long long *__restrict__ up, const long long *__restrict__ d_nu,
+                           const long long *__restrict__ val, long long *__restrict__ out, long long *__restrict__ d_nh)
 {
-    // lower[0 .. nl-1) then upper[0 .. nu-1) (each excludes its last point,
-    // which is the other's first); upper positions are in reversed order
+    const long long nl = *d_nl, nu = *d_nu;
+    if (nl <= 1) {
+        // a single distinct point: the lowest id among all survivors
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            out[0] = val[low[0]];
+            *d_nh = 1;
+        }
+        return;
+    }
     const long long a = nl - 1, total = a + (nu - 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        *d_nh = total;
     for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x)
         out[g] = g < a ? val[low[g]] : val[m - 1 - up[g - a]];
 }
@@ -180,9 +193,10 @@ int grid_for(long long work, int threads)
 } // namespace
 
 // One chain (lower: rev = 0, upper: rev = 1) of the m sorted points P; the
-// result positions are in pos_a (returned pointer) with length *h.
+// result positions are in the returned buffer (pos_a or pos_b), the length in
+// the returned device word (len_a[0] or len_b[0]).  Asynchronous.
 static long long *chain_gpu(const double2 *P, long long m, int rev, long long *pos_a, long long *pos_b, long long *len_a,
-                            long long *len_b, long long *bi, long long *bj, long long *h, cudaStream_t st)
+                            long long *len_b, long long *bi, long long *bj, const long long **d_len, cudaStream_t st)
 {
     const long long nchunks = (m + HG_CHUNK - 1) / HG_CHUNK;
     const long long m_cap = nchunks * HG_CHUNK;
@@ -196,105 +210,116 @@ static long long *chain_gpu(const double2 *P, long long m, int rev, long long *p
         std::swap(pos_a, pos_b);
         std::swap(len_a, len_b);
     }
-    cudaMemcpyAsync(h, len_a, sizeof(long long), cudaMemcpyDeviceToHost, st);
+    *d_len = len_a;
     return pos_a;
 }
 
+// Scratch layout of ch_hull_gpu_async for m survivors (all 256-B aligned).
+struct HullTmp {
+    size_t sort_tmp = 0, total = 0;
+    size_t o_k0, o_k1, o_v0, o_v1, o_P, o_pa, o_pb, o_pc, o_pd, o_la, o_lb, o_lc, o_ld, o_bi, o_bj, o_out;
+    explicit HullTmp(long long m)
+    {
+        if (m < 1)
+            m = 1;
+        const size_t nchunks = (size_t)((m + HG_CHUNK - 1) / HG_CHUNK), cap = nchunks * HG_CHUNK;
+        cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
+        cub::DoubleBuffer<long long> vb(nullptr, nullptr);
+        cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, kb, vb, (int64_t)m);
+        size_t p = 0;
+        auto take = [&](size_t b) { const size_t o = p; p += (b + 255) & ~(size_t)255; return o; };
+        take(sort_tmp);
+        o_k0 = take((size_t)m * 8); o_k1 = take((size_t)m * 8);
+        o_v0 = take((size_t)m * 8); o_v1 = take((size_t)m * 8);
+        o_P = take((size_t)m * 16);
+        o_pa = take(cap * 8); o_pb = take(cap * 8); o_pc = take(cap * 8); o_pd = take(cap * 8);
+        o_la = take(nchunks * 8 + 8); o_lb = take(nchunks * 8 + 8);
+        o_lc = take(nchunks * 8 + 8); o_ld = take(nchunks * 8 + 8);
+        o_bi = take(nchunks * 8 + 8); o_bj = take(nchunks * 8 + 8);
+        o_out = take((size_t)m * 8 + 8);
+        total = p;
+    }
+};
+
 extern "C" {
 
-// Device scratch for ch_hull_gpu on m survivors.
+// Device scratch for ch_hull_gpu / ch_hull_gpu_async on m survivors.
 size_t ch_hull_gpu_temp_bytes(int64_t m)
 {
-    if (m < 1)
-        m = 1;
-    const size_t nchunks = (size_t)((m + HG_CHUNK - 1) / HG_CHUNK);
-    const size_t cap = nchunks * HG_CHUNK;
-    size_t sort_tmp = 0;
-    cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
-    cub::DoubleBuffer<long long> vb(nullptr, nullptr);
-    cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, kb, vb, (int64_t)m);
-    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    return al(sort_tmp) + 4 * al((size_t)m * 8)   // keys x2, vals x2
-           + al((size_t)m * 16)                     // sorted points
-           + 4 * al(cap * 8)                        // chain positions: 2 per chain
-           + 4 * al(nchunks * 8 + 8)                // lengths x2, bridges x2
-           + al((size_t)m * 8 + 8);                 // assembled hull
+    return HullTmp(m).total;
 }
 
-// Exact strict hull of the m survivors d_surv (indices into d_xy) on the
-// device; hull ids are written to h_hull (host, capacity m) and the count to
-// *h_n_hull.  Synchronizes `stream`.
+// The device hull, asynchronous: hull ids to d_hull (device, capacity m), the
+// count to *d_n_hull (device).  No host synchronization.
+ch_status ch_hull_gpu_async(const double *d_xy, const int64_t *d_surv, int64_t m, int64_t *d_hull, int64_t *d_n_hull,
+                            void *d_tmp, size_t tmp_bytes, void *stream)
+{
+    cudaStream_t st = (cudaStream_t)stream;
+    if (m < 0 || !d_n_hull || (m > 0 && (!d_xy || !d_surv || !d_hull || !d_tmp)))
+        return CH_ERR_INVALID_ARG;
+    if (m == 0)
+        return cudaMemsetAsync(d_n_hull, 0, sizeof(int64_t), st) == cudaSuccess ? CH_OK : CH_ERR_CUDA;
+    const HullTmp L(m);
+    if (tmp_bytes < L.total)
+        return CH_ERR_WORKSPACE;
+    char *b = (char *)d_tmp;
+    auto *k0 = (unsigned long long *)(b + L.o_k0), *k1 = (unsigned long long *)(b + L.o_k1);
+    auto *v0 = (long long *)(b + L.o_v0), *v1 = (long long *)(b + L.o_v1);
+    auto *P = (double2 *)(b + L.o_P);
+    auto *pa = (long long *)(b + L.o_pa), *pb = (long long *)(b + L.o_pb);
+    auto *pc = (long long *)(b + L.o_pc), *pd = (long long *)(b + L.o_pd);
+    auto *la = (long long *)(b + L.o_la), *lb = (long long *)(b + L.o_lb);
+    auto *lc = (long long *)(b + L.o_lc), *ld = (long long *)(b + L.o_ld);
+    auto *bi = (long long *)(b + L.o_bi), *bj = (long long *)(b + L.o_bj);
+
+    const int g = grid_for(m, 256);
+    k_ykeys<<<g, 256, 0, st>>>(d_xy, (const long long *)d_surv, m, k0, v0);
+    cub::DoubleBuffer<unsigned long long> kb(k0, k1);
+    cub::DoubleBuffer<long long> vb(v0, v1);
+    size_t tb = L.sort_tmp;
+    if (cub::DeviceRadixSort::SortPairs(d_tmp, tb, kb, vb, (int64_t)m, 0, 64, st) != cudaSuccess)
+        return CH_ERR_CUDA;
+    // x keys in the y-sorted order, then a stable sort by x
+    k_xkeys<<<g, 256, 0, st>>>(d_xy, vb.Current(), m, kb.Alternate());
+    kb.selector ^= 1;
+    tb = L.sort_tmp;
+    if (cub::DeviceRadixSort::SortPairs(d_tmp, tb, kb, vb, (int64_t)m, 0, 64, st) != cudaSuccess)
+        return CH_ERR_CUDA;
+    const long long *val = vb.Current();
+    k_points<<<g, 256, 0, st>>>(d_xy, val, m, P);
+
+    const long long *d_hl, *d_hu;
+    const long long *low = chain_gpu(P, m, 0, pa, pb, la, lb, bi, bj, &d_hl, st);
+    const long long *up = chain_gpu(P, m, 1, pc, pd, lc, ld, bi, bj, &d_hu, st);
+    k_assemble<<<grid_for(m, 256), 256, 0, st>>>(m, low, d_hl, up, d_hu, val, (long long *)d_hull,
+                                                 (long long *)d_n_hull);
+    return cudaGetLastError() == cudaSuccess ? CH_OK : CH_ERR_CUDA;
+}
+
+// The device hull with the ids copied to h_hull (host, capacity m).
+// Synchronizes `stream`.
 ch_status ch_hull_gpu(const double *d_xy, const int64_t *d_surv, int64_t m, int64_t *h_hull, int64_t *h_n_hull,
                       void *d_tmp, size_t tmp_bytes, void *stream)
 {
     cudaStream_t st = (cudaStream_t)stream;
     if (!h_n_hull || (m > 0 && (!d_xy || !d_surv || !h_hull || !d_tmp)))
         return CH_ERR_INVALID_ARG;
-    if (m == 0) {
+    if (m <= 0) {
         *h_n_hull = 0;
-        return CH_OK;
+        return m == 0 ? CH_OK : CH_ERR_INVALID_ARG;
     }
-    if (tmp_bytes < ch_hull_gpu_temp_bytes(m))
+    const HullTmp L(m);
+    if (tmp_bytes < L.total)
         return CH_ERR_WORKSPACE;
-    const long long nchunks = (m + HG_CHUNK - 1) / HG_CHUNK;
-    const size_t cap = (size_t)nchunks * HG_CHUNK;
-    size_t sort_tmp = 0;
-    {
-        cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
-        cub::DoubleBuffer<long long> vb(nullptr, nullptr);
-        cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, kb, vb, (int64_t)m);
-    }
-    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    char *p = (char *)d_tmp;
-    void *tmp = p; p += al(sort_tmp);
-    auto *k0 = (unsigned long long *)p; p += al((size_t)m * 8);
-    auto *k1 = (unsigned long long *)p; p += al((size_t)m * 8);
-    auto *v0 = (long long *)p; p += al((size_t)m * 8);
-    auto *v1 = (long long *)p; p += al((size_t)m * 8);
-    auto *P = (double2 *)p; p += al((size_t)m * 16);
-    auto *pa = (long long *)p; p += al(cap * 8);
-    auto *pb = (long long *)p; p += al(cap * 8);
-    auto *pc = (long long *)p; p += al(cap * 8);
-    auto *pd = (long long *)p; p += al(cap * 8);
-    auto *la = (long long *)p; p += al((size_t)nchunks * 8 + 8);
-    auto *lb = (long long *)p; p += al((size_t)nchunks * 8 + 8);
-    auto *bi = (long long *)p; p += al((size_t)nchunks * 8 + 8);
-    auto *bj = (long long *)p; p += al((size_t)nchunks * 8 + 8);
-    auto *out = (long long *)p;
-
-    const int g = grid_for(m, 256);
-    k_ykeys<<<g, 256, 0, st>>>(d_xy, (const long long *)d_surv, m, k0, v0);
-    cub::DoubleBuffer<unsigned long long> kb(k0, k1);
-    cub::DoubleBuffer<long long> vb(v0, v1);
-    size_t tb = sort_tmp;
-    if (cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, (int64_t)m, 0, 64, st) != cudaSuccess)
-        return CH_ERR_CUDA;
-    // x keys in the y-sorted order, then a stable sort by x
-    k_xkeys<<<g, 256, 0, st>>>(d_xy, vb.Current(), m, kb.Alternate());
-    kb.selector ^= 1;
-    tb = sort_tmp;
-    if (cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, (int64_t)m, 0, 64, st) != cudaSuccess)
-        return CH_ERR_CUDA;
-    const long long *val = vb.Current();
-    k_points<<<g, 256, 0, st>>>(d_xy, val, m, P);
-
-    long long hl = 0, hu = 0;
-    long long *low_keep = chain_gpu(P, m, 0, pa, pb, la, lb, bi, bj, &hl, st);
-    cudaStreamSynchronize(st); // hl is read below; la/lb/bi/bj are reused
-    long long *up = chain_gpu(P, m, 1, pc, pd, la, lb, bi, bj, &hu, st);
+    int64_t *d_out = (int64_t *)((char *)d_tmp + L.o_out);
+    int64_t *d_nh = d_out + m; // the word after the ids (o_out holds m + 1 words)
+    ch_status s = ch_hull_gpu_async(d_xy, d_surv, m, d_out, d_nh, d_tmp, tmp_bytes, stream);
+    if (s != CH_OK)
+        return s;
+    int64_t nh = 0;
+    cudaMemcpyAsync(&nh, d_nh, sizeof(nh), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    if (cudaGetLastError() != cudaSuccess)
-        return CH_ERR_CUDA;
-    long long nh;
-    if (hl <= 1) {
-        // a single distinct point: the lowest id among all survivors
-        nh = 1;
-        k_assemble<<<1, 1, 0, st>>>(m, low_keep, 2, up, 1, val, out); // out[0] = val[low[0]]
-    } else {
-        nh = (hl - 1) + (hu - 1);
-        k_assemble<<<grid_for(nh, 256), 256, 0, st>>>(m, low_keep, hl, up, hu, val, out);
-    }
-    cudaMemcpyAsync(h_hull, out, (size_t)nh * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h_hull, d_out, (size_t)nh * 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     if (cudaGetLastError() != cudaSuccess)
         return CH_ERR_CUDA;

@@ -33,13 +33,25 @@ def main():
         n = int(nf)
         for dist in a.dists:
             xy = synth.points(dist, n, seed=0, device="cuda")
-            ws = chf.Workspace(n)
+            ws = chf.Workspace(n, hull=True)
             hull, surv, st = chf.hull_end_to_end(xy, ws)           # warm-up (allocator, modules)
             t0 = time.perf_counter()
             hull, surv, st = chf.hull_end_to_end(xy, ws)
             wall_dev = (time.perf_counter() - t0) * 1e3
             row = {"workload": f"{dist}_{n:.0e}", "n": n, "survivors": int(st.n_survivors), "hull": int(st.n_hull),
                    "ms_filter": st.ms_filter, "ms_hull_device": st.ms_hull + st.ms_gather, "ms_total_device": wall_dev}
+            # the hull kept on the device (ch_hull_gpu_async), CUDA events
+            tmp = torch.empty(int(chf._lib.load().ch_hull_gpu_temp_bytes(surv.shape[0])), dtype=torch.uint8,
+                              device="cuda")
+            chf.hull_gpu_async(xy, surv, tmp)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            hd, hc = chf.hull_gpu_async(xy, surv, tmp)
+            e1.record()
+            torch.cuda.synchronize()
+            row["ms_hull_on_device"] = e0.elapsed_time(e1)
+            assert int(hc.item()) == len(hull)
+            del tmp, hd
             if st.n_survivors <= a.host_max:
                 t0 = time.perf_counter()
                 hull_h, _, sth = chf.hull_end_to_end(xy, ws, host_hull=True)
@@ -52,10 +64,14 @@ def main():
             del xy, ws, surv
             torch.cuda.empty_cache()
     lines = ["# hull stage (a8 / f1), 1x B200: filter (K1+K2) and hull timed separately; device hull vs host chain",
-             f"{'workload':16s} {'survivors':>11s} {'hull':>10s} {'filter ms':>10s} {'dev hull ms':>12s} {'host hull ms':>13s}  equal"]
+             "# dev hull ms: ch_hull_end_to_end's hull stage incl. the id copy to pinned host memory; "
+             "on-device ms: ch_hull_gpu_async (ids stay on the device), CUDA events",
+             f"{'workload':16s} {'survivors':>11s} {'hull':>10s} {'filter ms':>10s} {'dev hull ms':>12s} "
+             f"{'on-device ms':>13s} {'host hull ms':>13s}  equal"]
     for r in rows:
         lines.append(f"{r['workload']:16s} {r['survivors']:11d} {r['hull']:10d} {r['ms_filter']:10.3f} "
-                     f"{r['ms_hull_device']:12.2f} {r.get('ms_hull_host', float('nan')):13.2f}  {r.get('device_equals_host', '-')}")
+                     f"{r['ms_hull_device']:12.2f} {r['ms_hull_on_device']:13.2f} "
+                     f"{r.get('ms_hull_host', float('nan')):13.2f}  {r.get('device_equals_host', '-')}")
     open(a.out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 

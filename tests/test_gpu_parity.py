@@ -512,6 +512,32 @@ def test_device_hull_end_to_end(dist):
     assert np.array_equal(hull_h, want_hull)
 
 
+def test_device_hull_async_on_device():
+    """ch_hull_gpu_async: ids and count stay on the device, same hull; m = 0
+    gives a zero count."""
+    for name, xy in list(_hull_sets())[-4:]:
+        d = torch.tensor(xy, device=DEV)
+        ids = torch.arange(len(xy), dtype=torch.int64, device=DEV)
+        h, c = chf.hull_gpu_async(d, ids)
+        assert h.is_cuda and c.is_cuda
+        assert np.array_equal(h[: int(c.item())].cpu().numpy(), oracle.hull(xy)), name
+    d = torch.zeros((4, 2), dtype=torch.float64, device=DEV)
+    h, c = chf.hull_gpu_async(d, torch.empty(0, dtype=torch.int64, device=DEV))
+    assert int(c.item()) == 0
+
+
+def test_hull_end_to_end_workspace_tail_and_malloc_paths():
+    """The device-hull scratch from the workspace tail (Workspace(n, hull=True))
+    and from cudaMallocAsync (plain workspace) give the same result."""
+    n = 300_001
+    xy_d = synth.points("displaced", n, seed=11, device=DEV)
+    a, sa, _ = chf.hull_end_to_end(xy_d, chf.Workspace(n, hull=True))
+    b, sb, _ = chf.hull_end_to_end(xy_d, chf.Workspace(n))
+    want, want_s, _ = oracle.hull_end_to_end(xy_d.cpu().numpy())
+    assert np.array_equal(a, want) and np.array_equal(b, want)
+    assert np.array_equal(sa.cpu().numpy(), want_s) and np.array_equal(sb.cpu().numpy(), want_s)
+
+
 def test_device_hull_golden():
     for ex in load_golden():
         d = torch.tensor(ex["points"], device=DEV)
