@@ -31,6 +31,10 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef CH_CERT_H
+#define CH_CERT_H 8 // points per consume_cert pass
+#endif
+
 // ----------------------------------------------------------------- layout --
 constexpr int K1_THREADS = 256;
 // Point storage: float64 AoS (16 B/pt, the default) or float32 AoS (8 B/pt,
@@ -535,13 +539,11 @@ __global__ void __launch_bounds__(256) k3_combine8(const ch_extremes *__restrict
 struct __align__(16) SEdge { // 48 B: lanes indexing different edges hit distinct banks
     double ax, ay, ex, ey, thr, pad;
 };
-struct __align__(16) FEdge {
-    float a, b, cin, cout;
-};
 struct SOct {
     SEdge e[8];
-    FEdge f[8];
-    FEdge fg[8];   // f[guess[oct]] by the code (dy<0)<<2 | (dx<0)<<1 | (|dx|<|dy|)
+    float4 fab[8]; // {a, a, b, b}: edge k's fp32 coefficients as FFMA2 operand pairs
+    float4 fc[8];  // {cin, cin, cout, cout}
+    float2 bxlo, bxhi; // float storage: (-boxf[0], -boxf[2]), (boxf[1], boxf[3])
     double box[4];
     float boxf[4]; // float bounds with x >= boxf[0] <=> (double)x >= box[0], etc.
     double cx, cy;
@@ -560,17 +562,8 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.e[t].thr = o->thr[t];
         s.e[t].pad = 0.0;
         s.guess[t] = o->guess_edge[t];
-        s.f[t].a = o->f32_a[t];
-        s.f[t].b = o->f32_b[t];
-        s.f[t].cin = o->f32_cin[t];
-        s.f[t].cout = o->f32_cout[t];
-        // code bits (sy, sx, |dx| < |dy|) -> octant of the 2' stage
-        const int oct_of_code[8] = {0, 1, 3, 2, 7, 6, 4, 5};
-        const int g = o->guess_edge[oct_of_code[t]];
-        s.fg[t].a = o->f32_a[g];
-        s.fg[t].b = o->f32_b[g];
-        s.fg[t].cin = o->f32_cin[g];
-        s.fg[t].cout = o->f32_cout[g];
+        s.fab[t] = make_float4(o->f32_a[t], o->f32_a[t], o->f32_b[t], o->f32_b[t]);
+        s.fc[t] = make_float4(o->f32_cin[t], o->f32_cin[t], o->f32_cout[t], o->f32_cout[t]);
     } else if (t == 8) {
         s.box[0] = o->box[0];
         s.box[1] = o->box[1];
@@ -580,6 +573,8 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.boxf[1] = chf::f32_down(o->box[1]);
         s.boxf[2] = chf::f32_up(o->box[2]);
         s.boxf[3] = chf::f32_down(o->box[3]);
+        s.bxlo = make_float2(-s.boxf[0], -s.boxf[2]);
+        s.bxhi = make_float2(s.boxf[1], s.boxf[3]);
         s.cx = o->cx;
         s.cy = o->cy;
         s.nv = o->nv;
@@ -676,9 +671,7 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
         return 0u;
     const int nv = s.nv;
     unsigned keep = 0;
-    // With has_f32 the fp32 guessed-edge keep certificate (B) replaces 2'
-    // (measured faster for both storages, profiles/r01_k2_stage_order.txt).
-    if (!s.has_f32 && guess_mode <= 0) {
+    if (guess_mode <= 0) {
         // 2'. the guessed edge of the point's octant: D_g <= T_g => kept
 #pragma unroll
         for (int i = 0; i < NP; i++) {
@@ -698,125 +691,6 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
         guess_mode = 16; // the next stage was needed anyway: skip 2' for a while
     }
     guess_mode--;
-    if (s.has_f32) {
-        // fp32 certification (proof at chf::octagon_edge), chunk by chunk:
-        //  B. keep certificate on the octant-guessed edge: h_g <= -0;
-        //  A. inside certificate on every edge: all g_k >= +0 (the sign bits
-        //     of the g_k OR-ed);
-        //  C. keep certificate on any edge: some h_k <= -0.
-        // Two points per FFMA2 in A and C (fma.rn.f32x2: each half is one
-        // correctly rounded fma, bit-identical to the scalar __fmaf_rn chain).
-        unsigned in = 0, out = 0;
-        constexpr int CH = sizeof(C) == 4 ? 4 : 8; // points per pass (bounds register use)
-        static_assert(CH % 2 == 0, "points are processed in pairs");
-        const float2 mc = make_float2(-(float)s.cx, -(float)s.cy);
-#pragma unroll
-        for (int c0 = 0; c0 < NP; c0 += CH) {
-            unsigned undc = (und >> c0) & ((1u << CH) - 1u);
-            if (!__any_sync(FULL, undc))
-                continue;
-            float2 X[CH / 2], Y[CH / 2];
-            unsigned sg[CH];
-#pragma unroll
-            for (int q = 0; q < CH / 2; q++) {
-                X[q] = make_float2((float)px[c0 + 2 * q], (float)px[c0 + 2 * q + 1]); // exact for float storage
-                Y[q] = make_float2((float)py[c0 + 2 * q], (float)py[c0 + 2 * q + 1]);
-            }
-            // B. the octant-guessed edge (any edge is sound for "keep")
-            unsigned outc = 0;
-#pragma unroll
-            for (int q = 0; q < CH / 2; q++) {
-                const float2 dx = __fadd2_rn(X[q], make_float2(mc.x, mc.x));
-                const float2 dy = __fadd2_rn(Y[q], make_float2(mc.y, mc.y));
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const unsigned ux = __float_as_uint(h ? dx.y : dx.x), uy = __float_as_uint(h ? dy.y : dy.x);
-                    const unsigned code = ((uy >> 31) << 2) | ((ux >> 31) << 1) |
-                                          ((ux & 0x7fffffffu) < (uy & 0x7fffffffu) ? 1u : 0u);
-                    const FEdge f = s.fg[code];
-                    const float x = h ? X[q].y : X[q].x, y = h ? Y[q].y : Y[q].x;
-                    const float hv = __fmaf_rn(f.a, x, __fmaf_rn(f.b, y, f.cout));
-                    outc |= (__float_as_uint(hv) >> 31) << (2 * q + h);
-                }
-            }
-            outc &= undc;
-            undc &= ~outc;
-            unsigned inc = 0;
-            if (__any_sync(FULL, undc)) {
-                // A. inside certificate on every edge
-#pragma unroll
-                for (int i = 0; i < CH; i++)
-                    sg[i] = 0u;
-                auto edge_in = [&](const FEdge &f) {
-                    const float2 a = make_float2(f.a, f.a), b = make_float2(f.b, f.b),
-                                 c = make_float2(f.cin, f.cin);
-#pragma unroll
-                    for (int q = 0; q < CH / 2; q++) {
-                        const float2 g = __ffma2_rn(a, X[q], __ffma2_rn(b, Y[q], c));
-                        sg[2 * q] |= __float_as_uint(g.x);
-                        sg[2 * q + 1] |= __float_as_uint(g.y);
-                    }
-                };
-                if (nv == 8) {
-#pragma unroll
-                    for (int k = 0; k < 8; k++)
-                        edge_in(s.f[k]);
-                } else {
-                    for (int k = 0; k < nv; k++)
-                        edge_in(s.f[k]);
-                }
-#pragma unroll
-                for (int i = 0; i < CH; i++)
-                    inc |= ((~sg[i]) >> 31) << i;
-                inc &= undc;
-                undc &= ~inc;
-                if (__any_sync(FULL, undc)) {
-                    // C. keep certificate on any edge
-#pragma unroll
-                    for (int i = 0; i < CH; i++)
-                        sg[i] = 0u;
-                    auto edge_out = [&](const FEdge &f) {
-                        const float2 a = make_float2(f.a, f.a), b = make_float2(f.b, f.b),
-                                     c = make_float2(f.cout, f.cout);
-#pragma unroll
-                        for (int q = 0; q < CH / 2; q++) {
-                            const float2 h = __ffma2_rn(a, X[q], __ffma2_rn(b, Y[q], c));
-                            sg[2 * q] |= __float_as_uint(h.x);
-                            sg[2 * q + 1] |= __float_as_uint(h.y);
-                        }
-                    };
-                    if (nv == 8) {
-#pragma unroll
-                        for (int k = 0; k < 8; k++)
-                            edge_out(s.f[k]);
-                    } else {
-                        for (int k = 0; k < nv; k++)
-                            edge_out(s.f[k]);
-                    }
-                    unsigned o2 = 0;
-#pragma unroll
-                    for (int i = 0; i < CH; i++)
-                        o2 |= (sg[i] >> 31) << i;
-                    outc |= o2 & undc;
-                }
-            }
-            in |= inc << c0;
-            out |= outc << c0;
-        }
-        keep |= und & out;
-        und &= ~(in | out); // certified inside => discarded
-        if (!__any_sync(FULL, und))
-            return keep;
-        // fp64 on every edge for the (rare) points inside the uncertainty band
-        unsigned disc = und;
-        for (int k = 0; k < nv; k++) {
-#pragma unroll
-            for (int i = 0; i < NP; i++)
-                if ((disc >> i) & 1u)
-                    disc &= ~((edge_inside(s, k, s.exact, (double)px[i], (double)py[i]) ? 0u : 1u) << i);
-        }
-        return keep | (und & ~disc);
-    }
     unsigned disc = und;
     if (!s.exact) {
         for (int k = 0; k < nv; k++) {
@@ -836,6 +710,176 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
         }
     }
     return keep | (und & ~disc);
+}
+
+// OR of the sign bits of the fp32 certificate values over the octagon's
+// edges, two points per FFMA2: IN = g_k (constant cin, inside certificate),
+// else h_k (cout, keep certificate).  Edge-outer, so each edge's constants
+// are loaded once per pass; nv == 8 (the usual case) is fully unrolled.
+template <bool IN, int NQ>
+__device__ __forceinline__ void sign_or(const SOct &s, int nv, const float2 (&X)[NQ], const float2 (&Y)[NQ],
+                                        unsigned (&sg)[2 * NQ])
+{
+#pragma unroll
+    for (int i = 0; i < 2 * NQ; i++)
+        sg[i] = 0u;
+    auto edge = [&](int k) {
+        const float4 ab = s.fab[k];
+        const float2 a = make_float2(ab.x, ab.y), b = make_float2(ab.z, ab.w);
+        const float2 c = IN ? *(const float2 *)&s.fc[k].x : *(const float2 *)&s.fc[k].z;
+#pragma unroll
+        for (int q = 0; q < NQ; q++) {
+            const float2 v = __ffma2_rn(a, X[q], __ffma2_rn(b, Y[q], c));
+            sg[2 * q] |= __float_as_uint(v.x);
+            sg[2 * q + 1] |= __float_as_uint(v.y);
+        }
+    };
+    if (nv == 8) {
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            edge(k);
+    } else {
+        for (int k = 0; k < nv; k++)
+            edge(k);
+    }
+}
+
+// One full sub-tile of a consumer warp for has_f32 octagons, read straight from
+// the TMA stage (held until the caller releases it).  Writes, for each point
+// slot u, the warp ballot of "point u of this lane survives" to
+// mw[u * K2_CWARPS] (lane 0), bit-identical to "not (forall k: D_k > T_k)"
+// (R4).  Every stage is a certificate proven on its own (box:
+// chf::box_corner_ok; fp32: chf::octagon_edge), so the order cannot change a
+// result.  Per-point state is a sign word (bit 31), combined by LOP3; the
+// warp-uniform skips are one vote per half-tile:
+//  1. the accept box (4 DSETP / FSETP): inside => discarded.  A half whose
+//     points are all inside is done (normal data);
+//  2. keep certificate on any edge: some h_k <= -0 (circle-like data);
+//  3. if some point is still open: inside certificate, all g_k >= +0;
+//  4. fp64 D_k on every edge for points in neither (the ~1e-7 band), the
+//     doubles re-read from the stage.
+template <typename T, int NP>
+__device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTraits<T>::V2 *sp, unsigned *mw)
+{
+    constexpr int H = CH_CERT_H; // points per pass (register budget)
+    constexpr unsigned SIGN = 0x80000000u;
+    const int tid = threadIdx.x;
+    const bool lane0 = (tid & 31) == 0;
+    const int nv = s.nv;
+    auto point = [&](int u, T &x, T &y) { // full sub-tiles only
+        const auto v = sp[u * K2_CTHREADS + tid];
+        x = v.x;
+        y = v.y;
+    };
+#pragma unroll
+    for (int h0 = 0; h0 < NP; h0 += H) {
+        float2 X[H / 2], Y[H / 2];
+        unsigned ob[H]; // bit 31: valid and outside the accept box
+        unsigned anyout = 0;
+#pragma unroll
+        for (int i = 0; i < H; i++) {
+            T x, y;
+            point(h0 + i, x, y);
+            // Outside the accept box <=> a sign bit among x - x0, x1 - x, y - y0,
+            // y1 - y: an RNE difference has the sign of the exact one, and is
+            // +0 when equal (same decision as x >= x0 && ... on finite input)
+            if constexpr (sizeof(T) == 4) {
+                const float2 p = make_float2(x, y);
+                const float2 lo = __fadd2_rn(p, s.bxlo);
+                const float2 hi = __ffma2_rn(make_float2(-1.f, -1.f), p, s.bxhi);
+                ob[i] = (__float_as_uint(lo.x) | __float_as_uint(lo.y) | __float_as_uint(hi.x) |
+                         __float_as_uint(hi.y)) & SIGN;
+            } else {
+                const double t0 = __dsub_rn(x, s.box[0]), t1 = __dsub_rn(s.box[1], x);
+                const double t2 = __dsub_rn(y, s.box[2]), t3 = __dsub_rn(s.box[3], y);
+                ob[i] = (__double2hiint(t0) | __double2hiint(t1) | __double2hiint(t2) | __double2hiint(t3)) & SIGN;
+            }
+            anyout |= ob[i];
+            if (i & 1) {
+                X[i / 2].y = (float)x; // exact for float storage
+                Y[i / 2].y = (float)y;
+            } else {
+                X[i / 2].x = (float)x;
+                Y[i / 2].x = (float)y;
+            }
+        }
+        if (!__any_sync(FULL, anyout != 0u)) {
+#pragma unroll
+            for (int i = 0; i < H; i++)
+                if (lane0)
+                    mw[(h0 + i) * K2_CWARPS] = 0u;
+            continue;
+        }
+        unsigned keep[H], sg[H];
+        sign_or<false, H / 2>(s, nv, X, Y, sg); // 2. keep certificate
+        unsigned open = 0;
+#pragma unroll
+        for (int i = 0; i < H; i++) {
+            keep[i] = ob[i] & sg[i];
+            open |= ob[i] & ~sg[i];
+        }
+        if (__any_sync(FULL, open != 0u)) {
+            sign_or<true, H / 2>(s, nv, X, Y, sg); // 3. inside certificate
+            unsigned band = 0;
+#pragma unroll
+            for (int i = 0; i < H; i++) {
+                sg[i] = ob[i] & ~keep[i] & sg[i]; // open and not certified inside
+                band |= sg[i];
+            }
+            if (__any_sync(FULL, band != 0u)) {
+                // 4. fp64 on every edge for the band points (rare)
+#pragma unroll
+                for (int i = 0; i < H; i++) {
+                    if (sg[i]) {
+                        double x, y;
+                        if constexpr (sizeof(T) == 8) {
+                            // re-read (volatile: the doubles must not stay live across the pass)
+                            const volatile double *vp = (const volatile double *)(sp + (h0 + i) * K2_CTHREADS + tid);
+                            x = vp[0];
+                            y = vp[1];
+                        } else {
+                            T xs, ys;
+                            point(h0 + i, xs, ys);
+                            x = xs;
+                            y = ys;
+                        }
+                        bool kf = false;
+                        for (int k = 0; k < nv && !kf; k++)
+                            kf = !edge_inside(s, k, s.exact, x, y);
+                        keep[i] |= kf ? SIGN : 0u;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < H; i++) {
+            const unsigned m = __ballot_sync(FULL, (int)keep[i] < 0);
+            if (lane0)
+                mw[(h0 + i) * K2_CWARPS] = m;
+        }
+    }
+}
+
+// Survivor stores of one 32-point group: lane l stores v (its point's global
+// index) at pb[c + rank of l among the group's survivors] if bit l of the
+// group's ballot m is set -- one predicated, coalesced warp store (m is
+// warp-uniform, the bit test is per lane).
+__device__ __forceinline__ void store_group(long long *pb, unsigned m, int c, long long v, unsigned lb, unsigned lt)
+{
+    long long *p = pb + (c + __popc(m & lt));
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.global.s64 [%1], %2;\n}" ::"r"(m & lb), "l"(p),
+                 "l"(v)
+                 : "memory");
+}
+
+// The same with the index given as (lo, hi) 32-bit words (little endian).
+__device__ __forceinline__ void store_group32(long long *pb, unsigned m, int c, unsigned lo, unsigned hi, unsigned lb,
+                                              unsigned lt)
+{
+    long long *p = pb + (c + __popc(m & lt));
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.global.v2.u32 [%1], {%2, %3};\n}" ::"r"(m & lb),
+                 "l"(p), "r"(lo), "r"(hi)
+                 : "memory");
 }
 
 // ===================================================================== K2 ==
@@ -975,23 +1019,37 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
             if (s_total[bb] > 0) {
                 const int E = s_nsub[bb] * K2_GROUPS, per = E / K2_CWARPS, e0 = warp * per;
                 long long *ob = out + s_excl[bb];
+                asm("" : "+l"(ob)); // one base register: offsets below are 32-bit
                 long long v = (long long)s_tile[bb] * super_pts + index_base + 32LL * e0 + lane;
                 const uint4 *bw = (const uint4 *)(bits + bb * K2_ENTRIES + e0);
                 const int4 *sc = (const int4 *)(gscan + bb * K2_ENTRIES + e0);
                 const unsigned lb = 1u << lane;
+                const long long vend = v + 32LL * per; // this warp's index range: [v - lane, vend)
+                if ((v >> 32) == ((vend - 1) >> 32)) {
+                    // no 2^32 crossing: the high word is constant, the low word a 32-bit add
+                    const unsigned hi = (unsigned)(v >> 32);
+                    unsigned lo = (unsigned)v;
+                    for (int q = 0; q < per / 4; q++, lo += 128) {
+                        const uint4 m = bw[q];
+                        if ((m.x | m.y | m.z | m.w) == 0u)
+                            continue;
+                        const int4 c = sc[q];
+                        store_group32(ob, m.x, c.x, lo, hi, lb, lt);
+                        store_group32(ob, m.y, c.y, lo + 32, hi, lb, lt);
+                        store_group32(ob, m.z, c.z, lo + 64, hi, lb, lt);
+                        store_group32(ob, m.w, c.w, lo + 96, hi, lb, lt);
+                    }
+                    return;
+                }
                 for (int q = 0; q < per / 4; q++, v += 128) {
                     const uint4 m = bw[q];
                     if ((m.x | m.y | m.z | m.w) == 0u)
                         continue;
                     const int4 c = sc[q];
-                    if (m.x & lb)
-                        ob[c.x + __popc(m.x & lt)] = v;
-                    if (m.y & lb)
-                        ob[c.y + __popc(m.y & lt)] = v + 32;
-                    if (m.z & lb)
-                        ob[c.z + __popc(m.z & lt)] = v + 64;
-                    if (m.w & lb)
-                        ob[c.w + __popc(m.w & lt)] = v + 96;
+                    store_group(ob, m.x, c.x, v, lb, lt);
+                    store_group(ob, m.y, c.y, v + 32, lb, lt);
+                    store_group(ob, m.z, c.z, v + 64, lb, lt);
+                    store_group(ob, m.w, c.w, v + 96, lb, lt);
                 }
             }
         };
@@ -1011,6 +1069,13 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
             const long long base = (long long)sup * super_pts + (long long)j * K2_SUB;
             const V2 *sp = stage + (size_t)st * K2_SUB;
             const int copied = s_desc_copied[st];
+            unsigned *bw = bits + b * K2_ENTRIES + j * K2_GROUPS + warp;
+            if (so.has_f32 && copied == (int)K2_SUB) {
+                consume_cert<T, K2_NP>(so, sp, bw);
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive(&s_empty[st]); // this warp is done with stage st
+            } else {
             T px[K2_NP], py[K2_NP]; // storage precision; widened exactly where fp64 is needed
             unsigned valid = (1u << K2_NP) - 1u;
 #pragma unroll
@@ -1033,12 +1098,12 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
             if (lane == 0)
                 mbar_arrive(&s_empty[st]); // this warp is done with stage st
             const unsigned keep = so.degenerate ? valid : classify<T, K2_NP>(so, px, py, valid, guess_mode);
-            unsigned *bw = bits + b * K2_ENTRIES + j * K2_GROUPS;
 #pragma unroll
             for (int u = 0; u < K2_NP; u++) {
-                unsigned m = __ballot_sync(FULL, (keep >> u) & 1u);
+                const unsigned m = __ballot_sync(FULL, keep & (1u << u));
                 if (lane == 0)
-                    bw[u * K2_CWARPS + warp] = m;
+                    bw[u * K2_CWARPS] = m;
+            }
             }
             if (j == nsub - 1) {
                 // ---- end of super-tile: group prefix (block scan) + aggregate ----
