@@ -31,6 +31,18 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef CH_K2_NP_D
+#define CH_K2_NP_D 8 // K2 points per consumer thread per sub-tile, float64 storage
+#endif
+#ifndef CH_K2_NP_F
+#define CH_K2_NP_F 16 // the same, float32 storage
+#endif
+#ifndef CH_K2_STAGES
+#define CH_K2_STAGES 3 // K2 TMA ring depth
+#endif
+#ifndef CH_K2_MINB
+#define CH_K2_MINB 2 // K2 resident CTAs per SM the registers are sized for
+#endif
 #ifndef CH_CERT_H
 #define CH_CERT_H 8 // points per consume_cert pass
 #endif
@@ -44,14 +56,14 @@ template <typename T> struct PtTraits;
 template <> struct PtTraits<double> {
     using V2 = double2;
     static constexpr int K1_UNROLL = 4; // wide loads (2 points each) per thread per chunk
-    static constexpr int K2_NP = 8;     // points per consumer thread per sub-tile (32 KB)
-    static constexpr int K2_STAGES = 3; // TMA ring depth (sub-tiles)
+    static constexpr int K2_NP = CH_K2_NP_D;     // points per consumer thread per sub-tile
+    static constexpr int K2_STAGES = CH_K2_STAGES; // TMA ring depth (sub-tiles)
 };
 template <> struct PtTraits<float> {
     using V2 = float2;
     static constexpr int K1_UNROLL = 8;
-    static constexpr int K2_NP = 16;
-    static constexpr int K2_STAGES = 3;
+    static constexpr int K2_NP = CH_K2_NP_F;
+    static constexpr int K2_STAGES = CH_K2_STAGES;
 };
 template <typename T> constexpr long long k1_chunk() { return (long long)K1_THREADS * PtTraits<T>::K1_UNROLL * 2; }
 constexpr int K1_MAX_CTAS = 2048;
@@ -173,6 +185,14 @@ __device__ __forceinline__ unsigned lanemask_lt()
 __device__ __forceinline__ unsigned smem_u32(const void *p)
 {
     return (unsigned)__cvta_generic_to_shared(p);
+}
+// One float from shared memory (volatile: not merged into an (x, y) pair
+// load, so the value lands directly in its FFMA2 operand pair).
+__device__ __forceinline__ float lds_f32(unsigned addr)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
 }
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count)
 {
@@ -543,7 +563,7 @@ struct SOct {
     SEdge e[8];
     float4 fab[8]; // {a, a, b, b}: edge k's fp32 coefficients as FFMA2 operand pairs
     float4 fc[8];  // {cin, cin, cout, cout}
-    float2 bxlo, bxhi; // float storage: (-boxf[0], -boxf[2]), (boxf[1], boxf[3])
+    unsigned long long nbx0, bx1, nby0, by1; // float storage, as f32x2 pairs: (-boxf[0], -boxf[0]), (boxf[1], boxf[1]), ...
     double box[4];
     float boxf[4]; // float bounds with x >= boxf[0] <=> (double)x >= box[0], etc.
     double cx, cy;
@@ -573,8 +593,11 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.boxf[1] = chf::f32_down(o->box[1]);
         s.boxf[2] = chf::f32_up(o->box[2]);
         s.boxf[3] = chf::f32_down(o->box[3]);
-        s.bxlo = make_float2(-s.boxf[0], -s.boxf[2]);
-        s.bxhi = make_float2(s.boxf[1], s.boxf[3]);
+        auto dup = [](float v) { return ((unsigned long long)__float_as_uint(v) << 32) | __float_as_uint(v); };
+        s.nbx0 = dup(-s.boxf[0]);
+        s.bx1 = dup(s.boxf[1]);
+        s.nby0 = dup(-s.boxf[2]);
+        s.by1 = dup(s.boxf[3]);
         s.cx = o->cx;
         s.cy = o->cy;
         s.nv = o->nv;
@@ -712,27 +735,56 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
     return keep | (und & ~disc);
 }
 
+// Two fp32 lanes in one 64-bit register pair (low word = first point): the
+// operand form of the sm_100 paired FP32 instructions.  Keeping the pairs as
+// b64 values makes the register allocator hold each pair once instead of
+// re-packing it for every FFMA2.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi)
+{
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) // each half: one RN fma
+{
+    f32x2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b)
+{
+    f32x2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b)
+{
+    f32x2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
 // OR of the sign bits of the fp32 certificate values over the octagon's
-// edges, two points per FFMA2: IN = g_k (constant cin, inside certificate),
-// else h_k (cout, keep certificate).  Edge-outer, so each edge's constants
-// are loaded once per pass; nv == 8 (the usual case) is fully unrolled.
+// edges, two points per FFMA2 (sg[q] bit 31: point 2q, bit 63: point 2q+1):
+// IN = g_k = fma(a, x, fma(b, y, cin)) (inside certificate), else h_k with
+// cout (keep certificate) -- the same correctly rounded fma chain as the
+// scalar proof at chf::octagon_edge.  Edge-outer, so each edge's constants
+// load once per pass; nv == 8 (the usual case) is fully unrolled.
 template <bool IN, int NQ>
-__device__ __forceinline__ void sign_or(const SOct &s, int nv, const float2 (&X)[NQ], const float2 (&Y)[NQ],
-                                        unsigned (&sg)[2 * NQ])
+__device__ __forceinline__ void sign_or(const SOct &s, int nv, const f32x2 (&X)[NQ], const f32x2 (&Y)[NQ],
+                                        f32x2 (&sg)[NQ])
 {
 #pragma unroll
-    for (int i = 0; i < 2 * NQ; i++)
-        sg[i] = 0u;
+    for (int q = 0; q < NQ; q++)
+        sg[q] = 0ull;
     auto edge = [&](int k) {
-        const float4 ab = s.fab[k];
-        const float2 a = make_float2(ab.x, ab.y), b = make_float2(ab.z, ab.w);
-        const float2 c = IN ? *(const float2 *)&s.fc[k].x : *(const float2 *)&s.fc[k].z;
+        const f32x2 *e = (const f32x2 *)&s.fab[k];
+        const f32x2 a = e[0], b = e[1];
+        const f32x2 c = ((const f32x2 *)&s.fc[k])[IN ? 0 : 1];
 #pragma unroll
-        for (int q = 0; q < NQ; q++) {
-            const float2 v = __ffma2_rn(a, X[q], __ffma2_rn(b, Y[q], c));
-            sg[2 * q] |= __float_as_uint(v.x);
-            sg[2 * q + 1] |= __float_as_uint(v.y);
-        }
+        for (int q = 0; q < NQ; q++)
+            sg[q] |= ffma2(a, X[q], ffma2(b, Y[q], c));
     };
     if (nv == 8) {
 #pragma unroll
@@ -744,93 +796,102 @@ __device__ __forceinline__ void sign_or(const SOct &s, int nv, const float2 (&X)
     }
 }
 
-// One full sub-tile of a consumer warp for has_f32 octagons, read straight from
-// the TMA stage (held until the caller releases it).  Writes, for each point
-// slot u, the warp ballot of "point u of this lane survives" to
+// One full sub-tile of a consumer warp for has_f32 octagons, read straight
+// from the TMA stage (held until the caller releases it).  Writes, for each
+// point slot u, the warp ballot of "point u of this lane survives" to
 // mw[u * K2_CWARPS] (lane 0), bit-identical to "not (forall k: D_k > T_k)"
 // (R4).  Every stage is a certificate proven on its own (box:
 // chf::box_corner_ok; fp32: chf::octagon_edge), so the order cannot change a
-// result.  Per-point state is a sign word (bit 31), combined by LOP3; the
-// warp-uniform skips are one vote per half-tile:
-//  1. the accept box (4 DSETP / FSETP): inside => discarded.  A half whose
-//     points are all inside is done (normal data);
+// result.  Per-point state is a sign bit, combined by LOP3; the warp-uniform
+// skips are one vote per pass:
+//  1. the accept box: inside => discarded.  A pass whose points are all
+//     inside is done (normal data);
 //  2. keep certificate on any edge: some h_k <= -0 (circle-like data);
 //  3. if some point is still open: inside certificate, all g_k >= +0;
 //  4. fp64 D_k on every edge for points in neither (the ~1e-7 band), the
-//     doubles re-read from the stage.
+//     coordinates re-read from the stage.
 template <typename T, int NP>
 __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTraits<T>::V2 *sp, unsigned *mw)
 {
-    constexpr int H = CH_CERT_H; // points per pass (register budget)
-    constexpr unsigned SIGN = 0x80000000u;
+    constexpr int H = CH_CERT_H < NP ? CH_CERT_H : NP; // points per pass (register budget)
+    constexpr int HQ = H / 2;
+    constexpr f32x2 SIGN2 = 0x8000000080000000ull;
     const int tid = threadIdx.x;
     const bool lane0 = (tid & 31) == 0;
     const int nv = s.nv;
-    auto point = [&](int u, T &x, T &y) { // full sub-tiles only
-        const auto v = sp[u * K2_CTHREADS + tid];
-        x = v.x;
-        y = v.y;
-    };
 #pragma unroll
     for (int h0 = 0; h0 < NP; h0 += H) {
-        float2 X[H / 2], Y[H / 2];
-        unsigned ob[H]; // bit 31: valid and outside the accept box
-        unsigned anyout = 0;
+        f32x2 X[HQ], Y[HQ]; // x (resp. y) of points (2q, 2q + 1) of the pass
+        f32x2 ob[HQ];       // sign bits: outside the accept box
+        f32x2 anyout = 0;
+        // Outside the accept box <=> a sign bit among x - x0, x1 - x, y - y0,
+        // y1 - y: an RNE difference has the sign of the exact one and is +0
+        // when equal (the same decision as x >= x0 && ... on finite input).
+        if constexpr (sizeof(T) == 8) {
 #pragma unroll
-        for (int i = 0; i < H; i++) {
-            T x, y;
-            point(h0 + i, x, y);
-            // Outside the accept box <=> a sign bit among x - x0, x1 - x, y - y0,
-            // y1 - y: an RNE difference has the sign of the exact one, and is
-            // +0 when equal (same decision as x >= x0 && ... on finite input)
-            if constexpr (sizeof(T) == 4) {
-                const float2 p = make_float2(x, y);
-                const float2 lo = __fadd2_rn(p, s.bxlo);
-                const float2 hi = __ffma2_rn(make_float2(-1.f, -1.f), p, s.bxhi);
-                ob[i] = (__float_as_uint(lo.x) | __float_as_uint(lo.y) | __float_as_uint(hi.x) |
-                         __float_as_uint(hi.y)) & SIGN;
-            } else {
-                const double t0 = __dsub_rn(x, s.box[0]), t1 = __dsub_rn(s.box[1], x);
-                const double t2 = __dsub_rn(y, s.box[2]), t3 = __dsub_rn(s.box[3], y);
-                ob[i] = (__double2hiint(t0) | __double2hiint(t1) | __double2hiint(t2) | __double2hiint(t3)) & SIGN;
+            for (int q = 0; q < HQ; q++) {
+                float fx[2], fy[2];
+                unsigned o[2];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const double2 v = sp[(h0 + 2 * q + h) * K2_CTHREADS + tid];
+                    const double t0 = __dsub_rn(v.x, s.box[0]), t1 = __dsub_rn(s.box[1], v.x);
+                    const double t2 = __dsub_rn(v.y, s.box[2]), t3 = __dsub_rn(s.box[3], v.y);
+                    o[h] = (__double2hiint(t0) | __double2hiint(t1) | __double2hiint(t2) | __double2hiint(t3)) &
+                           0x80000000u;
+                    fx[h] = (float)v.x;
+                    fy[h] = (float)v.y;
+                }
+                X[q] = pk2(fx[0], fx[1]);
+                Y[q] = pk2(fy[0], fy[1]);
+                ob[q] = ((f32x2)o[1] << 32) | o[0];
+                anyout |= ob[q];
             }
-            anyout |= ob[i];
-            if (i & 1) {
-                X[i / 2].y = (float)x; // exact for float storage
-                Y[i / 2].y = (float)y;
-            } else {
-                X[i / 2].x = (float)x;
-                Y[i / 2].x = (float)y;
+        } else {
+            // float storage: each float loaded straight into its pair half;
+            // the box on the pairs (exact for floats)
+            const unsigned sa = smem_u32(sp) + 8u * tid;
+            const f32x2 m1 = pk2(-1.f, -1.f), ONE2 = pk2(1.f, 1.f);
+#pragma unroll
+            for (int q = 0; q < HQ; q++) {
+                const unsigned a0 = sa + 8u * (h0 + 2 * q) * K2_CTHREADS, a1 = a0 + 8u * K2_CTHREADS;
+                // (x 1.0: exact; makes each pair one FMUL2 result, which the
+                // register allocator then keeps whole)
+                X[q] = fmul2(pk2(lds_f32(a0), lds_f32(a1)), ONE2);
+                Y[q] = fmul2(pk2(lds_f32(a0 + 4), lds_f32(a1 + 4)), ONE2);
+                ob[q] = (fadd2(X[q], s.nbx0) | ffma2(m1, X[q], s.bx1) | fadd2(Y[q], s.nby0) |
+                         ffma2(m1, Y[q], s.by1)) & SIGN2;
+                anyout |= ob[q];
             }
         }
-        if (!__any_sync(FULL, anyout != 0u)) {
+        if (!__any_sync(FULL, anyout != 0ull)) {
 #pragma unroll
             for (int i = 0; i < H; i++)
                 if (lane0)
                     mw[(h0 + i) * K2_CWARPS] = 0u;
             continue;
         }
-        unsigned keep[H], sg[H];
-        sign_or<false, H / 2>(s, nv, X, Y, sg); // 2. keep certificate
-        unsigned open = 0;
+        f32x2 keep[HQ], sg[HQ];
+        sign_or<false, HQ>(s, nv, X, Y, sg); // 2. keep certificate
+        f32x2 open = 0;
 #pragma unroll
-        for (int i = 0; i < H; i++) {
-            keep[i] = ob[i] & sg[i];
-            open |= ob[i] & ~sg[i];
+        for (int q = 0; q < HQ; q++) {
+            keep[q] = ob[q] & sg[q];
+            open |= ob[q] & ~sg[q];
         }
-        if (__any_sync(FULL, open != 0u)) {
-            sign_or<true, H / 2>(s, nv, X, Y, sg); // 3. inside certificate
-            unsigned band = 0;
+        if (__any_sync(FULL, open != 0ull)) {
+            sign_or<true, HQ>(s, nv, X, Y, sg); // 3. inside certificate
+            f32x2 band = 0;
 #pragma unroll
-            for (int i = 0; i < H; i++) {
-                sg[i] = ob[i] & ~keep[i] & sg[i]; // open and not certified inside
-                band |= sg[i];
+            for (int q = 0; q < HQ; q++) {
+                sg[q] = ob[q] & ~keep[q] & sg[q]; // open and not certified inside
+                band |= sg[q];
             }
-            if (__any_sync(FULL, band != 0u)) {
+            if (__any_sync(FULL, band != 0ull)) {
                 // 4. fp64 on every edge for the band points (rare)
 #pragma unroll
                 for (int i = 0; i < H; i++) {
-                    if (sg[i]) {
+                    if ((sg[i / 2] >> (32 * (i & 1) + 31)) & 1ull) {
                         double x, y;
                         if constexpr (sizeof(T) == 8) {
                             // re-read (volatile: the doubles must not stay live across the pass)
@@ -838,22 +899,22 @@ __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTra
                             x = vp[0];
                             y = vp[1];
                         } else {
-                            T xs, ys;
-                            point(h0 + i, xs, ys);
-                            x = xs;
-                            y = ys;
+                            const auto v = sp[(h0 + i) * K2_CTHREADS + tid];
+                            x = v.x;
+                            y = v.y;
                         }
                         bool kf = false;
                         for (int k = 0; k < nv && !kf; k++)
                             kf = !edge_inside(s, k, s.exact, x, y);
-                        keep[i] |= kf ? SIGN : 0u;
+                        if (kf)
+                            keep[i / 2] |= 1ull << (32 * (i & 1) + 31);
                     }
                 }
             }
         }
 #pragma unroll
         for (int i = 0; i < H; i++) {
-            const unsigned m = __ballot_sync(FULL, (int)keep[i] < 0);
+            const unsigned m = __ballot_sync(FULL, (keep[i / 2] >> (32 * (i & 1) + 31)) & 1ull);
             if (lane0)
                 mw[(h0 + i) * K2_CWARPS] = m;
         }
@@ -914,7 +975,7 @@ __device__ __forceinline__ void bar_arrive(int id, int nthreads)
 }
 
 template <typename T>
-__global__ void __launch_bounds__(K2_THREADS, 2)
+__global__ void __launch_bounds__(K2_THREADS, CH_K2_MINB)
 k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
                   const ch_octagon *__restrict__ oct, WsHeader *hdr,
                   unsigned long long *status, long long *__restrict__ out,

@@ -13,6 +13,6 @@ print(f\"$1 {d['config']['workload']:28s} {d['value']:8.2f} Gpts/s k1 {r['k1_ms'
 cp $L /tmp/new.so
 for R in ${ROUNDS:-1}; do
   cp /tmp/new.so $L; touch $L; run new
-  cp build/alt/libchfilter.so $L; touch $L; run alt
+  cp ${ALT:-build/alt/libchfilter.so} $L; touch $L; run alt
 done
 cp /tmp/new.so $L; touch $L
