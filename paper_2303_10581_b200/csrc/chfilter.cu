@@ -947,22 +947,25 @@ __device__ __forceinline__ void store_group32(long long *pb, unsigned m, int c, 
 // Persistent, warp-specialized CTAs: 8 consumer warps, 1 publisher warp and
 // 1 TMA producer warp.  The producer claims "super-tiles" of `subs` x K2_SUB
 // consecutive points with one atomic each (in increasing order, one claim
-// ahead) and streams them as 16 KB sub-tiles through a K2_STAGES-deep ring
+// ahead) and streams them as 32 KB sub-tiles through a K2_STAGES-deep ring
 // in shared memory (cp.async.bulk + full/empty mbarriers), so loads stay in
 // flight while the consumers compute.  Consumer thread t tests points
-// base_j + u*256 + t (u < K2_NP) of sub-tile j; the results are
-// ballot-ed per (sub-tile, u, warp) -- 32 consecutive points -- into one of
-// two shared-memory buffers.  The
-// publisher warp takes a full buffer, publishes the super-tile's count and
-// runs ONE decoupled look-back (Merrill & Garland) for it, then writes the
-// survivors' int64 indices in index order ((j, u, warp, lane)
-// lexicographic == increasing index) and hands the buffer back -- while the
-// compute warps already stream the next super-tile into the other buffer.
-// Claims are made in increasing order by running CTAs, so every predecessor
-// of a claimed super-tile is owned by a running CTA: the look-back always
-// makes progress.  Hand-offs use named barriers (bar.arrive / bar.sync).
-// named barriers K2_BAR_BASE + b: consumers arrive, publisher syncs (buffer b full);
-// K2_BAR_BASE + 2 + b: publisher arrives, consumers sync (buffer b empty).
+// u * 256 + t (u < K2_NP) of each sub-tile j; the results are ballot-ed per
+// (sub-tile, u, warp) -- 32 consecutive points, group e = (j * K2_NP + u) *
+// 8 + warp, so e order is index order -- into one of two shared-memory
+// buffers.  At the end of a super-tile the consumers block-scan the group
+// popcounts and publish the super-tile's aggregate (flag A) at once; the
+// publisher warp then runs ONE decoupled look-back (Merrill & Garland) for
+// it and publishes the inclusive prefix (flag P), while the consumers stream
+// the next super-tile into the other buffer.  When a buffer comes round
+// again, each consumer warp writes its own groups' survivors (int64 global
+// indices, in index order) with predicated coalesced stores.  Claims are
+// made in increasing order by running CTAs, so every predecessor of a
+// claimed super-tile is owned by a running CTA: the look-back always makes
+// progress.  Hand-offs use named barriers (bar.arrive / bar.sync):
+// K2_BAR_BASE + b: consumers arrive, publisher syncs (buffer b full);
+// K2_BAR_BASE + 2 + b: publisher arrives, consumers sync (buffer b's offset
+// known); K2_BAR_BASE + 4: consumers only.
 constexpr unsigned TILE_DONE = 0xffffffffu;
 
 __device__ __forceinline__ void bar_sync(int id, int nthreads)
