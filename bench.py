@@ -28,6 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Gpts/s filtered and % of HBM peak at 1/2/4/8 B200; survivor ratio per distribution"
+L2_BYTES = 126 * 1024 * 1024   # B200 L2
 UNIT = "Gpts/s"
 
 NVML_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -56,6 +57,8 @@ def parse():
                     help="point storage precision (f32: the paper's, widened exactly to f64)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",  # noqa: E501
+                    help="replay the step as a CUDA graph (ch_graph_launch); auto: 1 GPU and n <= 2^20")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU work for the oracle baseline")
     return ap.parse_args()
@@ -251,14 +254,19 @@ def run_ours(a):
     stream = torch.cuda.current_stream()
 
     small = world == 1 and n_local <= 4096   # latency-bound C1: the single-kernel step (K5)
+    # launch-bound sizes: the whole step replayed as one CUDA graph
+    graphed = world == 1 and (a.graph == "on" or (a.graph == "auto" and n_local <= (1 << 20)))
     if world == 1:
         ws = chf.Workspace(n_local, device=dev)
         out = torch.empty(max(n_local, 1), dtype=torch.int64, device=dev)
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
         launches_per_step = 1 if small else 2
+        graph = chf.FilterGraph(xy, ws, out, cnt, plain=a.plain) if graphed else None
 
         def k1():
-            if small:
+            if graphed:
+                graph.launch()
+            elif small:
                 chf.filter_async(xy, ws, out, cnt, plain=a.plain)
             else:
                 chf.extremes8_async(xy, ws, plain=a.plain)
@@ -267,7 +275,7 @@ def run_ours(a):
             pass
 
         def k2():
-            if not small:
+            if not small and not graphed:
                 chf.filter_compact(xy, ws, out=out, count=cnt)
 
         def exch2():
@@ -305,25 +313,55 @@ def run_ours(a):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # inputs smaller than 2x the 126 MB L2: flush L2 before every timed step
+    # (a 512 MB memset, outside the step's own events) and time steps alone
+    flush = bpp * n_local < 2 * L2_BYTES
+    fbuf = torch.empty(4 * L2_BYTES, dtype=torch.uint8, device=dev) if flush else None
+    step_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)] if flush else None
     with ClockSampler(local) as clk:
         t_start.record(stream)
-        for k in range(K):
-            ev[k][0].record(stream)
-            k1()
-            ev[k][1].record(stream)
-            exch()
-            ev[k][2].record(stream)
-            k2()
-            ev[k][3].record(stream)
-            exch2()
+        if flush:
+            for k in range(K):
+                fbuf.zero_()
+                step_ev[k][0].record(stream)
+                if graphed:
+                    k1()
+                else:
+                    ev[k][0].record(stream)
+                    k1()
+                    ev[k][1].record(stream)
+                    exch()
+                    ev[k][2].record(stream)
+                    k2()
+                    ev[k][3].record(stream)
+                    exch2()
+                step_ev[k][1].record(stream)
+        elif graphed:   # one graph launch per step, no per-step events (host cost)
+            for k in range(K):
+                k1()
+        else:
+            for k in range(K):
+                ev[k][0].record(stream)
+                k1()
+                ev[k][1].record(stream)
+                exch()
+                ev[k][2].record(stream)
+                k2()
+                ev[k][3].record(stream)
+                exch2()
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     total_ms = t_start.elapsed_time(t_end)
-    k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
-    k2_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
-    ex_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    if flush:   # the steps' own time: L2 flushes excluded
+        total_ms = float(np.sum([e[0].elapsed_time(e[1]) for e in step_ev]))
+    if graphed:
+        k1_ms, k2_ms, ex_ms = total_ms / K, 0.0, 0.0
+    else:
+        k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+        k2_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
+        ex_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
     res = chf.read_result(ws)
     s_local = int(res.count)
     if world > 1:
@@ -338,7 +376,10 @@ def run_ours(a):
     peak, peak_src = measured_peaks()
     k1_bytes = bpp * n_local
     k2_bytes = bpp * n_local + 8.0 * s_local
-    if small:
+    if graphed:
+        dom = "graph(k5_small_filter)" if small else "graph(k1_extremes8+k2_filter_compact)"
+        dom_bytes, dom_ms = k1_bytes + k2_bytes, k1_ms
+    elif small:
         dom, dom_bytes, dom_ms = "k5_small_filter", k1_bytes + k2_bytes, k1_ms
     elif k2_ms >= k1_ms:
         dom, dom_bytes, dom_ms = "k2_filter_compact", k2_bytes, k2_ms
@@ -348,8 +389,8 @@ def run_ours(a):
     step_bytes = k1_bytes + k2_bytes
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": ncu_traffic(dom, workload_name(a)), "peak_source": peak_src,
-            "k1_ms": k1_ms, "k2_ms": k2_ms, "k1_gbs": k1_bytes / (k1_ms / 1e3) / 1e9,
-            "k2_gbs": k2_bytes / (k2_ms / 1e3) / 1e9,
+            "k1_ms": k1_ms, "k2_ms": k2_ms, "k1_gbs": k1_bytes / (k1_ms / 1e3) / 1e9 if not graphed else None,
+            "k2_gbs": k2_bytes / (k2_ms / 1e3) / 1e9 if k2_ms > 0 else None,
             "step_gbs_per_gpu": step_bytes / (ms_step / 1e3) / 1e9,
             "step_frac": step_bytes / (ms_step / 1e3) / 1e9 / peak,
             "step_frac_theoretical_8184": step_bytes / (ms_step / 1e3) / 1e9 / 8184.0}
@@ -418,8 +459,11 @@ def run_ours(a):
             "config": {"workload": workload_name(a), "n": n_total, "n_per_gpu": n_local, "dist": a.dist,
                        "seed": a.seed, "p": a.p if a.dist == "displaced" else None,
                        "predicate": a.predicate, "storage": a.storage,
-                       "parallelism": f"dp{world}", "l2": f"inputs larger than L2 ({int(bpp)} B/pt)"
-                       if bpp * n_local > 126e6 else "inputs smaller than L2 (not flushed)"},
+                       "parallelism": f"dp{world}",
+                       "l2": (f"L2 flushed before every step (512 MB memset outside the step events); "
+                              f"inputs {bpp * n_local / 1e6:.3g} MB" if flush
+                              else f"inputs larger than L2 ({int(bpp)} B/pt)"),
+                       "cuda_graph": bool(graphed)},
             "survivors": s_total, "survivor_ratio": s_total / n_total,
             "hbm_frac": roof["step_frac"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

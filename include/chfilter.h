@@ -215,6 +215,23 @@ ch_status ch_filter_async(const double *d_xy, int64_t n, int flags, int64_t *d_s
 ch_status ch_filter_async_f32(const float *d_xy, int64_t n, int flags, int64_t *d_survivors,
                               int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
 
+/* The step of ch_filter_async captured once into a CUDA graph, then replayed
+ * with one launch per step (Blackwell: a graph launch costs one host call
+ * for the whole K1 + K2 or K5 sequence, the point of the latency-bound C1
+ * config).  Capture happens on a private stream; the arguments (pointers,
+ * n, flags) are baked into the graph, so the caller keeps the buffers alive
+ * and unchanged in place until ch_graph_destroy.  *out receives an opaque
+ * handle owned by the caller.  Errors: the ch_filter_async ones, or
+ * CH_ERR_CUDA if capture / instantiation fails.  ch_graph_launch enqueues one
+ * step on `stream` (asynchronous, like ch_filter_async). */
+typedef struct ch_graph ch_graph;
+ch_status ch_filter_graph_create(const double *d_xy, int64_t n, int flags, int64_t *d_survivors,
+                                 int64_t *d_count, void *d_ws, size_t ws_bytes, ch_graph **out);
+ch_status ch_filter_graph_create_f32(const float *d_xy, int64_t n, int flags, int64_t *d_survivors,
+                                     int64_t *d_count, void *d_ws, size_t ws_bytes, ch_graph **out);
+ch_status ch_graph_launch(ch_graph *g, void *stream);
+ch_status ch_graph_destroy(ch_graph *g);
+
 /* The same step end to end from HOST memory: copies h_xy (pinned for full
  * speed) into d_xy_staging (capacity n points), filters, and copies the
  * survivor indices back to h_survivors (capacity n).  Synchronizes. */

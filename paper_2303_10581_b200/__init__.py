@@ -191,6 +191,37 @@ def filter_async(xy: torch.Tensor, ws: Workspace, out: torch.Tensor, count: torc
                                                 ws.ptr, ws.nbytes, _stream(stream)), "ch_filter_async")
 
 
+class FilterGraph:
+    """The filter_async step captured once as a CUDA graph (ch_filter_graph_create)
+    and replayed by launch(): one host call per step.  The tensors are baked
+    into the graph, so they are kept referenced here and must not move."""
+
+    def __init__(self, xy: torch.Tensor, ws: Workspace, out: torch.Tensor, count: torch.Tensor | None = None,
+                 plain: bool = False):
+        lib = _lib.load()
+        self._xy = _points(xy)
+        self._keep = (ws, out, count)
+        h = ctypes.c_void_p()
+        _lib.check(_fn(lib, "ch_filter_graph_create", self._xy)(
+            _ptr(self._xy), self._xy.shape[0], _plain(plain), _ptr(out), _ptr(count), ws.ptr, ws.nbytes,
+            ctypes.byref(h)), "ch_filter_graph_create")
+        self._h = h
+
+    def launch(self, stream=None):
+        _lib.check(_lib.load().ch_graph_launch(self._h, _stream(stream)), "ch_graph_launch")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().ch_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def filter_host(h_xy: torch.Tensor, ws: Workspace, d_staging: torch.Tensor, d_out: torch.Tensor,
                 h_out: torch.Tensor, plain: bool = False, stream=None) -> int:
     """End-to-end step from host memory (H2D copy, filter, D2H survivors)."""

@@ -68,6 +68,10 @@ SIGNATURES = {
     "ch_filter": (ctypes.c_int, [P, I64, ctypes.c_int, P, ctypes.POINTER(I64), P, SZ, P]),
     "ch_filter_async": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, SZ, P]),
     "ch_filter_async_f32": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, SZ, P]),
+    "ch_filter_graph_create": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, SZ, ctypes.POINTER(P)]),
+    "ch_filter_graph_create_f32": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, SZ, ctypes.POINTER(P)]),
+    "ch_graph_launch": (ctypes.c_int, [P, P]),
+    "ch_graph_destroy": (ctypes.c_int, [P]),
     "ch_filter_host": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, ctypes.POINTER(I64), P, SZ, P]),
     "ch_gather_points": (ctypes.c_int, [P, I64, P, I64, P, P]),
     "ch_hull_points": (ctypes.c_int, [P, P, I64, P, ctypes.POINTER(I64)]),

@@ -1893,6 +1893,88 @@ ch_status ch_filter_f32(const float *d_xy, int64_t n, int flags, int64_t *d_surv
     return filter_impl(d_xy, n, flags, d_survivors, h_count, d_ws, ws_bytes, stream);
 }
 
+} // extern "C"
+
+struct ch_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
+namespace {
+template <typename T>
+ch_status graph_create(const T *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *d_count, void *d_ws,
+                       size_t ws_bytes, ch_graph **out)
+{
+    if (!out)
+        return fail(CH_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    dev_info(); // function attributes / occupancy queried before capture
+    cudaStream_t cs;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(CH_ERR_CUDA, "graph: stream create failed");
+    ch_graph *g = new ch_graph();
+    ch_status s = CH_OK;
+    if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        s = fail(CH_ERR_CUDA, "graph: begin capture failed");
+    } else {
+        s = filter_async_impl(d_xy, n, flags, d_survivors, d_count, d_ws, ws_bytes, (void *)cs);
+        const cudaError_t e = cudaStreamEndCapture(cs, &g->graph);
+        if (s == CH_OK && e != cudaSuccess)
+            s = fail(CH_ERR_CUDA, std::string("graph: capture failed: ") + cudaGetErrorString(e));
+        if (s == CH_OK && cudaGraphInstantiate(&g->exec, g->graph, 0) != cudaSuccess)
+            s = fail(CH_ERR_CUDA, "graph: instantiate failed");
+    }
+    cudaGetLastError();
+    cudaStreamDestroy(cs);
+    if (s != CH_OK) {
+        if (g->exec)
+            cudaGraphExecDestroy(g->exec);
+        if (g->graph)
+            cudaGraphDestroy(g->graph);
+        delete g;
+        return s;
+    }
+    *out = g;
+    return CH_OK;
+}
+} // namespace
+
+extern "C" {
+
+ch_status ch_filter_graph_create(const double *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *d_count,
+                                 void *d_ws, size_t ws_bytes, ch_graph **out)
+{
+    return graph_create(d_xy, n, flags, d_survivors, d_count, d_ws, ws_bytes, out);
+}
+
+ch_status ch_filter_graph_create_f32(const float *d_xy, int64_t n, int flags, int64_t *d_survivors,
+                                     int64_t *d_count, void *d_ws, size_t ws_bytes, ch_graph **out)
+{
+    return graph_create(d_xy, n, flags, d_survivors, d_count, d_ws, ws_bytes, out);
+}
+
+ch_status ch_graph_launch(ch_graph *g, void *stream)
+{
+    if (!g || !g->exec)
+        return fail(CH_ERR_INVALID_ARG, "graph is NULL");
+    const cudaError_t e = cudaGraphLaunch(g->exec, (cudaStream_t)stream);
+    if (e != cudaSuccess)
+        return fail(CH_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(e));
+    return CH_OK;
+}
+
+ch_status ch_graph_destroy(ch_graph *g)
+{
+    if (!g)
+        return CH_OK;
+    if (g->exec)
+        cudaGraphExecDestroy(g->exec);
+    if (g->graph)
+        cudaGraphDestroy(g->graph);
+    delete g;
+    return CH_OK;
+}
+
 ch_status ch_filter_host(const double *h_xy, int64_t n, int flags, double *d_xy_staging, int64_t *d_survivors,
                          int64_t *h_survivors, int64_t *h_count, void *d_ws, size_t ws_bytes, void *stream)
 {

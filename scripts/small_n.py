@@ -39,7 +39,8 @@ def main():
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     lines = ["# one filter step at small n, 1x B200, us per step (CUDA events, back-to-back, inputs resident)",
-             f"{'workload':16s} {'K5 us':>9s} {'K1+K2 us':>9s}"]
+             f"{'workload':16s} {'K5 us':>9s} {'K1+K2 us':>9s} {'graph us':>9s}  (graph: ch_graph_launch of the "
+             f"ch_filter_async step; K5 for n <= 4096, else K1 + K2)"]
     print(lines[0], flush=True)
     for dist in a.dists:
         for nf in a.sizes:
@@ -57,10 +58,13 @@ def main():
                 chf.extremes8_async(xy, ws2)
                 chf.filter_compact(xy, ws2, out=out2)
 
-            t5, t12 = time_us(k5, a.iters), time_us(k12, a.iters)
-            c5, c12 = chf.read_result(ws).count, chf.read_result(ws2).count
-            assert c5 == c12 and torch.equal(out[:c5], out2[:c12])
-            lines.append(f"{dist + '_' + format(n, '.0e'):16s} {t5:9.2f} {t12:9.2f}")
+            ws3 = chf.Workspace(n)
+            out3 = torch.empty(n, dtype=torch.int64, device="cuda")
+            g = chf.FilterGraph(xy, ws3, out3, cnt)
+            t5, t12, tg = time_us(k5, a.iters), time_us(k12, a.iters), time_us(g.launch, a.iters)
+            c5, c12, cg = chf.read_result(ws).count, chf.read_result(ws2).count, chf.read_result(ws3).count
+            assert c5 == c12 == cg and torch.equal(out[:c5], out2[:c12]) and torch.equal(out[:c5], out3[:cg])
+            lines.append(f"{dist + '_' + format(n, '.0e'):16s} {t5:9.2f} {t12:9.2f} {tg:9.2f}")
             print(lines[-1], flush=True)
     if a.out:
         open(a.out, "w").write("\n".join(lines) + "\n")

@@ -598,3 +598,28 @@ def test_small_n_single_kernel_equals_two_kernels(dist):
                     want, _ = oracle.filter_compact(xy, certified=not mode)
                 assert np.array_equal(k5, want), (dist, n, storage, mode)
                 assert np.array_equal(k12, want), (dist, n, storage, mode)
+
+
+@pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
+def test_graph_replay_equals_oracle(dist):
+    """ch_filter_graph_create / ch_graph_launch: the captured step (K5 for
+    n <= 4096, K1 + K2 above), replayed several times, gives the oracle's
+    survivors every time, f64 and f32."""
+    for n in (4096, 10_000, 300_007):
+        for storage in ("f64", "f32"):
+            xy_d = synth.points(dist, n, seed=7, device=DEV)
+            if storage == "f32":
+                xy_d = xy_d.float()
+            want, _ = oracle.filter_compact(xy_d.double().cpu().numpy())
+            ws = chf.Workspace(n)
+            out = torch.full((n,), -1, dtype=torch.int64, device=DEV)
+            cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+            g = chf.FilterGraph(xy_d, ws, out, cnt)
+            for rep in range(3):
+                out.fill_(-1)
+                g.launch()
+                torch.cuda.synchronize()
+                c = int(cnt.item())
+                assert c == len(want) == chf.read_result(ws).count, (dist, n, storage, rep)
+                assert np.array_equal(out[:c].cpu().numpy(), want), (dist, n, storage, rep)
+            g.close()
