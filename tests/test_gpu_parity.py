@@ -140,6 +140,20 @@ def test_parity_misaligned_input_16B():
     check_against_oracle(xy_d.contiguous() if not xy_d.is_contiguous() else xy_d, name="misaligned")
 
 
+def test_parity_f32_16B_and_32B_aligned():
+    """float32 storage: a 32-byte aligned base takes K1's 256-bit (4-point)
+    loads, a 16-byte aligned one the 128-bit loads; both equal the oracle."""
+    big = synth.points("circle", 200_003, seed=9, device=DEV).float()
+    for off in (0, 2):           # 2 points = 16 bytes
+        xy_d = big[off:]
+        assert xy_d.data_ptr() % 32 == (0 if off == 0 else 16)
+        want, idx8 = oracle.filter_compact(xy_d.double().cpu().numpy())
+        ws = chf.Workspace(xy_d.shape[0])
+        e, _ = chf.extremes8(xy_d, ws)
+        assert np.array_equal(np.array(e.idx[:]), idx8), off
+        assert np.array_equal(chf.filter(xy_d).cpu().numpy(), want), off
+
+
 def test_octagon_bits_vs_oracle_flags():
     for dist, n in (("normal", 100_003), ("circle", 65), ("displaced", 77_777)):
         xy_d = synth.points(dist, n, seed=6, device=DEV)
