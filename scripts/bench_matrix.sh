@@ -8,8 +8,10 @@ done; done; done
 timeout 300 python bench.py --no-e2e --no-cpu-baseline --dist normal --points 1e4 --steps 500 --warmup 20 > gpurun_out/bench_normal_1e4_f64.json 2>/dev/null
 python - <<'PY'
 import json,glob
-for f in sorted(glob.glob("gpurun_out/bench_*_f*.json")):
-    try: d=json.loads(open(f).read().strip().splitlines()[-1])
-    except Exception as e: print(f, "ERR", e); continue
-    r=d["roofline"]; print(f"{d['config']['workload']:28s} {d['value']:8.2f} Gpts/s  step {d['ms_per_step']*1e3:9.1f} us  k1 {r['k1_ms']:.3f} ({r['k1_gbs']:.0f} GB/s)  k2 {r['k2_ms']:.3f} ({r['k2_gbs']:.0f} GB/s)  hbm {d['hbm_frac']:.3f}  clk {d['clocks']['sm_mhz']} {d['clocks']['reasons']}")
+f = lambda v, fmt: format(v, fmt) if v is not None else "-"
+for fn in sorted(glob.glob("gpurun_out/bench_*_f*.json")):
+    try: d=json.loads(open(fn).read().strip().splitlines()[-1])
+    except Exception as e: print(fn, "ERR", e); continue
+    r=d["roofline"]
+    print(f"{d['config']['workload']:28s} {d['value']:8.2f} Gpts/s  step {d['ms_per_step']*1e3:9.1f} us  k1 {r['k1_ms']:.3f} ({f(r['k1_gbs'],'.0f')} GB/s)  k2 {r['k2_ms']:.3f} ({f(r['k2_gbs'],'.0f')} GB/s)  frac {r['frac']:.3f} step {d['hbm_frac']:.3f}  surv {d['survivors']}  clk {d['clocks']['sm_mhz']} {d['clocks']['reasons']}")
 PY
