@@ -57,6 +57,9 @@ def parse():
                     help="point storage precision (f32: the paper's, widened exactly to f64)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", choices=["auto", "peer", "nccl"], default="auto",
+                    help="N > 1: extremes / count exchange fused into the kernels over peer memory (peer), or "
+                         "NCCL all-gathers; auto = peer if it initializes")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",  # noqa: E501
                     help="replay the step as a CUDA graph (ch_graph_launch); auto: 1 GPU and n <= 2^20")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -254,6 +257,7 @@ def run_ours(a):
     stream = torch.cuda.current_stream()
 
     small = world == 1 and n_local <= 4096   # latency-bound C1: the single-kernel step (K5)
+    peer, exchange = False, None
     # launch-bound sizes: the whole step replayed as one CUDA graph
     graphed = world == 1 and (a.graph == "on" or (a.graph == "auto" and n_local <= (1 << 20)))
     if world == 1:
@@ -281,22 +285,41 @@ def run_ours(a):
         def exch2():
             pass
     else:
-        df = chdist.DistFilter(n_total, xy, plain=a.plain)
+        exchange = a.exchange
+        df = None
+        if exchange in ("auto", "peer"):
+            try:   # the exchanges fused into K1 / K3 / K2 over peer memory (cudaIpc, NVLink)
+                df = chdist.DistFilter(n_total, xy, plain=a.plain, exchange="peer")
+                exchange = "peer"
+            except Exception as e:   # e.g. IPC unavailable in this container
+                if a.exchange == "peer":
+                    raise
+                print(f"[bench] peer exchange unavailable ({e}); using NCCL all-gathers", file=sys.stderr)
+                exchange = "nccl"
+        if df is None:
+            df = chdist.DistFilter(n_total, xy, plain=a.plain, exchange="nccl")
         ws = df.ws
         launches_per_step = 3
+        peer = exchange == "peer"
 
         def k1():
+            if peer:
+                df.step()   # K1 (+ record push) -> K3 (acquire + combine) -> K2 (+ count push)
+                return
             chf.extremes8_async(xy, df.ws, index_base=df.lo, plain=a.plain, ext_out=df.ext_local)
 
         def exch():
-            chdist.exchange_extremes(df.ext_local, out=df.ext_all)
-            chf.combine8(df.ext_all, world, df.ws, plain=a.plain)
+            if not peer:
+                chdist.exchange_extremes(df.ext_local, out=df.ext_all)
+                chf.combine8(df.ext_all, world, df.ws, plain=a.plain)
 
         def k2():
-            chf.filter_compact(xy, df.ws, index_base=df.lo, out=df.out, count=df.count)
+            if not peer:
+                chf.filter_compact(xy, df.ws, index_base=df.lo, out=df.out, count=df.count)
 
         def exch2():
-            chdist.exclusive_offsets(df.count, out=df.counts)
+            if not peer:
+                chdist.exclusive_offsets(df.count, out=df.counts)
 
     def step():
         k1(); exch(); k2(); exch2()
@@ -379,6 +402,8 @@ def run_ours(a):
     if graphed:
         dom = "graph(k5_small_filter)" if small else "graph(k1_extremes8+k2_filter_compact)"
         dom_bytes, dom_ms = k1_bytes + k2_bytes, k1_ms
+    elif peer:   # one call enqueues K1, K3 and K2: the whole step is timed
+        dom, dom_bytes, dom_ms = "step(k1_extremes8+k3_combine8_peer+k2_filter_compact)", k1_bytes + k2_bytes, k1_ms
     elif small:
         dom, dom_bytes, dom_ms = "k5_small_filter", k1_bytes + k2_bytes, k1_ms
     elif k2_ms >= k1_ms:
@@ -389,7 +414,7 @@ def run_ours(a):
     step_bytes = k1_bytes + k2_bytes
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": ncu_traffic(dom, workload_name(a)), "peak_source": peak_src,
-            "k1_ms": k1_ms, "k2_ms": k2_ms, "k1_gbs": k1_bytes / (k1_ms / 1e3) / 1e9 if not graphed else None,
+            "k1_ms": k1_ms, "k2_ms": k2_ms, "k1_gbs": k1_bytes / (k1_ms / 1e3) / 1e9 if not (graphed or peer) else None,
             "k2_gbs": k2_bytes / (k2_ms / 1e3) / 1e9 if k2_ms > 0 else None,
             "step_gbs_per_gpu": step_bytes / (ms_step / 1e3) / 1e9,
             "step_frac": step_bytes / (ms_step / 1e3) / 1e9 / peak,
@@ -417,7 +442,7 @@ def run_ours(a):
             torch.cuda.synchronize()
             e2e_ms = e_s.elapsed_time(e_e) / a.e2e_steps
         else:
-            df2 = chdist.DistFilter(n_total, d_stage, plain=a.plain)
+            df2 = chdist.DistFilter(n_total, d_stage, plain=a.plain, exchange=exchange)
             d2h = 0
 
             def e2e_step():
@@ -463,7 +488,8 @@ def run_ours(a):
                        "l2": (f"L2 flushed before every step (512 MB memset outside the step events); "
                               f"inputs {bpp * n_local / 1e6:.3g} MB" if flush
                               else f"inputs larger than L2 ({int(bpp)} B/pt)"),
-                       "cuda_graph": bool(graphed)},
+                       "cuda_graph": bool(graphed),
+                       "exchange": exchange if world > 1 else None},
             "survivors": s_total, "survivor_ratio": s_total / n_total,
             "hbm_frac": roof["step_frac"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

@@ -55,7 +55,8 @@ typedef enum {
     CH_ERR_NONFINITE = 3,  /* a NaN / infinite coordinate        */
     CH_ERR_MISALIGNED = 4, /* d_xy not 16-byte aligned                  */
     CH_ERR_WORKSPACE = 5,  /* workspace missing or too small            */
-    CH_ERR_CUDA = 6        /* a CUDA runtime error (see ch_last_error)  */
+    CH_ERR_CUDA = 6,       /* a CUDA runtime error (see ch_last_error)  */
+    CH_ERR_PEER = 7        /* peer exchange: a rank's record did not arrive (timeout) */
 } ch_status;
 
 /* Predicate switch (DESIGN R4).  Default: certified thresholds T_k. */
@@ -231,6 +232,43 @@ ch_status ch_filter_graph_create_f32(const float *d_xy, int64_t n, int flags, in
                                      int64_t *d_count, void *d_ws, size_t ws_bytes, ch_graph **out);
 ch_status ch_graph_launch(ch_graph *g, void *stream);
 ch_status ch_graph_destroy(ch_graph *g);
+
+/* ---- Multi-GPU with the exchanges fused into the kernels (north_star a4, a7;
+ * SURVEY 8(e) "v2") ------------------------------------------------------------
+ * One process per GPU, points sharded by contiguous index ranges.  Every rank
+ * owns a small exchange buffer (2 banks x CH_MAX_PEERS slots x 256 B), exported
+ * with cudaIpcGetMemHandle and opened by every peer (NVLink / NVSwitch peer
+ * memory; on one GPU shared by several processes, plain device memory).
+ *   K1's last CTA stores its eight extremes (one ch_extremes record) straight
+ *   into slot[rank] of every peer's buffer, then a release flag (the step
+ *   epoch) -- the all-gather of a4 without a collective launch;
+ *   K3 (one CTA) acquires the W flags of its own buffer and combines the W
+ *   records into the global octagon, identically on every rank;
+ *   K2's last CTA stores the survivor count into every peer's slot[rank]
+ *   (a7), read back on the host by ch_peer_counts.
+ * Banks alternate with the step epoch (a rank can run at most one step ahead
+ * of a peer's reads).  Waits time out after ~10 s (CH_ERR_PEER from the next
+ * ch_read_result / ch_peer_counts) instead of hanging.
+ *   ch_peer_create: allocates the buffer, writes its IPC handle (64 bytes,
+ *     ch_peer_handle_bytes()) to h_handle.  ch_peer_open: takes the world
+ *     handles in rank order (the caller all-gathers them, e.g. with
+ *     torch.distributed) and opens the peers'.  Both synchronize.
+ *   ch_filter_step_peer: one sharded step on `stream` (asynchronous); n_local
+ *     may be 0 (an empty shard still takes part).  index_base = the shard's
+ *     first global index.  d_survivors: global indices, increasing.
+ *   ch_peer_counts: synchronizes `stream`, then waits for every rank's count of
+ *     the last step; h_counts[world] in rank order (exclusive scan = offsets). */
+#define CH_MAX_PEERS 16
+typedef struct ch_peer ch_peer;
+size_t ch_peer_handle_bytes(void);
+ch_status ch_peer_create(int rank, int world, ch_peer **out, void *h_handle);
+ch_status ch_peer_open(ch_peer *p, const void *h_handles);
+ch_status ch_peer_destroy(ch_peer *p);
+ch_status ch_filter_step_peer(ch_peer *p, const double *d_xy, int64_t n_local, int64_t index_base, int flags,
+                              int64_t *d_survivors, void *d_ws, size_t ws_bytes, void *stream);
+ch_status ch_filter_step_peer_f32(ch_peer *p, const float *d_xy, int64_t n_local, int64_t index_base, int flags,
+                                  int64_t *d_survivors, void *d_ws, size_t ws_bytes, void *stream);
+ch_status ch_peer_counts(ch_peer *p, int64_t *h_counts, void *stream);
 
 /* The same step end to end from HOST memory: copies h_xy (pinned for full
  * speed) into d_xy_staging (capacity n points), filters, and copies the

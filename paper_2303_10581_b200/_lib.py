@@ -17,7 +17,8 @@ DBL = ctypes.c_double
 SZ = ctypes.c_size_t
 
 CH_OK, CH_ERR_INVALID_ARG, CH_ERR_EMPTY, CH_ERR_NONFINITE = 0, 1, 2, 3
-CH_ERR_MISALIGNED, CH_ERR_WORKSPACE, CH_ERR_CUDA = 4, 5, 6
+CH_ERR_MISALIGNED, CH_ERR_WORKSPACE, CH_ERR_CUDA, CH_ERR_PEER = 4, 5, 6, 7
+CH_MAX_PEERS = 16
 CH_CERTIFIED, CH_PLAIN, CH_EXACT = 0, 1, 2
 CH_HULL_HOST = 4
 
@@ -71,6 +72,13 @@ SIGNATURES = {
     "ch_filter_graph_create": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, SZ, ctypes.POINTER(P)]),
     "ch_filter_graph_create_f32": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, SZ, ctypes.POINTER(P)]),
     "ch_graph_launch": (ctypes.c_int, [P, P]),
+    "ch_peer_handle_bytes": (SZ, []),
+    "ch_peer_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.POINTER(P), P]),
+    "ch_peer_open": (ctypes.c_int, [P, P]),
+    "ch_peer_destroy": (ctypes.c_int, [P]),
+    "ch_filter_step_peer": (ctypes.c_int, [P, P, I64, I64, ctypes.c_int, P, P, SZ, P]),
+    "ch_filter_step_peer_f32": (ctypes.c_int, [P, P, I64, I64, ctypes.c_int, P, P, SZ, P]),
+    "ch_peer_counts": (ctypes.c_int, [P, P, P]),
     "ch_graph_destroy": (ctypes.c_int, [P]),
     "ch_filter_host": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, ctypes.POINTER(I64), P, SZ, P]),
     "ch_gather_points": (ctypes.c_int, [P, I64, P, I64, P, P]),

@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/chfilter.h"
@@ -103,6 +104,8 @@ struct WsHeader {
     unsigned k2_claim;
     unsigned k2_exit;
     unsigned epoch;
+    unsigned peer_timeout; // K3's wait for a peer's record timed out (CH_ERR_PEER)
+    unsigned pad_[3];
     ch_result result;
     ch_extremes ext;
     ch_octagon oct;
@@ -179,6 +182,64 @@ __device__ __forceinline__ unsigned lanemask_lt()
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
+}
+
+// --------------------------------------------------- peer exchange (a4, a7) --
+// Exchange buffer of one rank: [2 banks][CH_MAX_PEERS slots][PEER_SLOT words];
+// slot s holds what rank s sent: words 0..23 its ch_extremes record, 24 the
+// record's epoch flag, 25 its survivor count, 26 the count's epoch flag.
+constexpr int PEER_SLOT = 32; // 256 B
+constexpr int PEER_REC_FLAG = 24, PEER_CNT = 25, PEER_CNT_FLAG = 26;
+constexpr size_t PEER_BUF_BYTES = 2ull * CH_MAX_PEERS * PEER_SLOT * 8;
+struct PeerPush {
+    unsigned long long *base[CH_MAX_PEERS]; // every rank's buffer, as mapped in this process
+    int world, rank;                        // world == 0: no peer exchange
+    unsigned long long epoch;               // step number (>= 1), bank = epoch & 1
+    __device__ __forceinline__ unsigned long long *slot(int peer, int of) const
+    {
+        return base[peer] + ((size_t)(epoch & 1) * CH_MAX_PEERS + of) * PEER_SLOT;
+    }
+};
+static_assert(sizeof(ch_extremes) == 24 * 8, "record = 24 words");
+
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Store one 24-word record into slot[rank] of every peer, then (after a
+// system-scope fence) the epoch flag.  Called by every thread of one CTA;
+// `rec` may be in shared or global memory.
+__device__ void peer_push_record(const PeerPush &pp, const unsigned long long *rec)
+{
+    const int tid = threadIdx.x;
+    for (int q = tid; q < 24 * pp.world; q += blockDim.x)
+        pp.slot(q / 24, pp.rank)[q % 24] = rec[q % 24];
+    __threadfence_system();
+    __syncthreads();
+    if (tid < pp.world)
+        st_release_sys(pp.slot(tid, pp.rank) + PEER_REC_FLAG, pp.epoch);
+}
+// The survivor count into slot[rank] of every peer, then its flag.
+__device__ void peer_push_count(const PeerPush &pp, long long count)
+{
+    for (int t = 0; t < pp.world; t++)
+        pp.slot(t, pp.rank)[PEER_CNT] = (unsigned long long)count;
+    __threadfence_system();
+    for (int t = 0; t < pp.world; t++)
+        st_release_sys(pp.slot(t, pp.rank) + PEER_CNT_FLAG, pp.epoch);
 }
 
 // ------------------------------------------------- TMA bulk copy + mbarrier --
@@ -345,7 +406,7 @@ __device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o
 
 template <typename T>
 __device__ void k1_finalize(const T *__restrict__ xy, long long index_base, int flags,
-                            WsHeader *hdr, const Partial *parts, int nparts, void *ext_out)
+                            WsHeader *hdr, const Partial *parts, int nparts, void *ext_out, const PeerPush &pp)
 {
     // Called by every thread of the last CTA.
     __shared__ double s_v[K1_THREADS / 32][8];
@@ -415,12 +476,14 @@ __device__ void k1_finalize(const T *__restrict__ xy, long long index_base, int 
         hdr->result.degenerate = s_o.degenerate;
         hdr->k1_ticket = 0; // ready for the next call (stream order)
     }
+    if (pp.world > 0) // a4 fused: this rank's record into every peer's buffer
+        peer_push_record(pp, (const unsigned long long *)&s_e);
 }
 
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(K1_THREADS, 3)
 k1_extremes8(const T *__restrict__ xy, long long n, long long index_base, int flags,
-             WsHeader *hdr, Partial *parts, void *ext_out)
+             WsHeader *hdr, Partial *parts, void *ext_out, const PeerPush pp)
 {
     constexpr int K1_UNROLL = PtTraits<T>::K1_UNROLL;
     constexpr long long K1_CHUNK = k1_chunk<T>();
@@ -508,13 +571,15 @@ k1_extremes8(const T *__restrict__ xy, long long n, long long index_base, int fl
     __syncthreads();
     if (s_last) {
         __threadfence();
-        k1_finalize(xy, index_base, flags, hdr, parts, gridDim.x, ext_out);
+        k1_finalize(xy, index_base, flags, hdr, parts, gridDim.x, ext_out, pp);
     }
 }
 
 // ===================================================================== K3 ==
-__global__ void __launch_bounds__(256) k3_combine8(const ch_extremes *__restrict__ all, int world, int flags,
-                                                   WsHeader *hdr)
+// The combine of a4, by one CTA: W per-rank records (max key, tie -> min
+// global index; empty shards have idx -1) -> the global extremes and octagon
+// in the workspace header, bit-identical to the 1-GPU K1.
+__device__ void combine_records(const ch_extremes *all, int world, int flags, WsHeader *hdr)
 {
     __shared__ ch_extremes s_e;
     __shared__ ch_octagon s_o;
@@ -553,6 +618,59 @@ __global__ void __launch_bounds__(256) k3_combine8(const ch_extremes *__restrict
         de[i] = se[i];
     if (tid == 0)
         hdr->result.degenerate = s_o.degenerate;
+}
+
+__global__ void __launch_bounds__(256) k3_combine8(const ch_extremes *__restrict__ all, int world, int flags,
+                                                   WsHeader *hdr)
+{
+    combine_records(all, world, flags, hdr);
+}
+
+// K3 of the fused exchange: acquire the W epoch flags of this rank's own
+// exchange buffer (the peers' K1s store their records there), then combine.
+// A wait longer than ~10 s sets hdr->peer_timeout (CH_ERR_PEER) and
+// combines what is there rather than hanging.
+__global__ void __launch_bounds__(256) k3_combine8_peer(const PeerPush pp, int flags, WsHeader *hdr)
+{
+    __shared__ ch_extremes s_all[CH_MAX_PEERS];
+    __shared__ int s_late;
+    const int tid = threadIdx.x;
+    if (tid == 0)
+        s_late = 0;
+    __syncthreads();
+    if (tid < pp.world) {
+        const unsigned long long *slot = pp.slot(pp.rank, tid); // own buffer, sender tid
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_sys(slot + PEER_REC_FLAG) != pp.epoch) {
+            if (globaltimer_ns() - t0 > 10000000000ull) {
+                s_late = 1;
+                break;
+            }
+            __nanosleep(100);
+        }
+        unsigned long long *dst = (unsigned long long *)&s_all[tid];
+        for (int w = 0; w < 24; w++)
+            dst[w] = *(const volatile unsigned long long *)(slot + w);
+    }
+    __syncthreads();
+    if (tid == 0 && s_late)
+        hdr->peer_timeout = 1;
+    combine_records(s_all, pp.world, flags, hdr);
+}
+
+// An empty shard's part of the exchange: its empty record (what = 0) or its
+// zero count (what = 1).
+__global__ void k_peer_push(const PeerPush pp, int what)
+{
+    if (what == 0) {
+        __shared__ unsigned long long rec[24];
+        if (threadIdx.x < 24)
+            rec[threadIdx.x] = threadIdx.x < 8 ? ~0ull : 0ull; // idx = -1, x = y = 0
+        __syncthreads();
+        peer_push_record(pp, rec);
+    } else if (threadIdx.x == 0) {
+        peer_push_count(pp, 0);
+    }
 }
 
 // ========================================================= octagon test ==
@@ -982,7 +1100,7 @@ __global__ void __launch_bounds__(K2_THREADS, CH_K2_MINB)
 k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
                   const ch_octagon *__restrict__ oct, WsHeader *hdr,
                   unsigned long long *status, long long *__restrict__ out,
-                  long long *d_count, unsigned nsuper, int subs)
+                  long long *d_count, unsigned nsuper, int subs, const PeerPush pp)
 {
     extern __shared__ __align__(128) unsigned char dsm[];
     using V2 = typename PtTraits<T>::V2;
@@ -1298,6 +1416,10 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
                 if (d_count)
                     *d_count = 0;
             }
+            if (pp.world > 0) { // a7 fused: this rank's count into every peer's buffer
+                __threadfence();
+                peer_push_count(pp, *(volatile long long *)&hdr->result.count);
+            }
         }
     }
 }
@@ -1585,7 +1707,7 @@ inline unsigned long long *status_of(void *d_ws)
 
 template <typename T>
 ch_status launch_k1(const T *d_xy, long long n, long long index_base, int flags, void *d_ext_out,
-                    void *d_ws, cudaStream_t st)
+                    void *d_ws, cudaStream_t st, const PeerPush &pp = PeerPush{})
 {
     DevInfo di = dev_info();
     constexpr long long K1_CHUNK = k1_chunk<T>();
@@ -1597,10 +1719,10 @@ ch_status launch_k1(const T *d_xy, long long n, long long index_base, int flags,
     // wide loads need the pair of points aligned to its size (32 B / 16 B)
     if (((uintptr_t)d_xy & (4 * sizeof(T) - 1)) == 0)
         k1_extremes8<T, true><<<(unsigned)g, K1_THREADS, 0, st>>>(d_xy, n, index_base, flags, hdr_of(d_ws),
-                                                                   parts_of(d_ws), d_ext_out);
+                                                                   parts_of(d_ws), d_ext_out, pp);
     else
         k1_extremes8<T, false><<<(unsigned)g, K1_THREADS, 0, st>>>(d_xy, n, index_base, flags, hdr_of(d_ws),
-                                                                    parts_of(d_ws), d_ext_out);
+                                                                    parts_of(d_ws), d_ext_out, pp);
     return cuda_check("k1_extremes8");
 }
 
@@ -1623,7 +1745,8 @@ ch_status stage_octagon(const ch_octagon *h_oct, void *d_ws, cudaStream_t st, co
 
 template <typename T>
 ch_status launch_k2(const T *d_xy, long long n, long long index_base, const ch_octagon *d_oct,
-                    long long *d_surv, long long *d_count, void *d_ws, cudaStream_t st)
+                    long long *d_surv, long long *d_count, void *d_ws, cudaStream_t st,
+                    const PeerPush &pp = PeerPush{})
 {
     DevInfo di = dev_info();
     long long resident = (long long)di.sms * (sizeof(T) == 8 ? di.k2_per_sm_d : di.k2_per_sm_f);
@@ -1635,7 +1758,8 @@ ch_status launch_k2(const T *d_xy, long long n, long long index_base, const ch_o
     long long nsuper = (nsub_total + subs - 1) / subs;
     long long grid = std::max<long long>(1, std::min<long long>(resident, nsuper));
     k2_filter_compact<T><<<(unsigned)grid, K2_THREADS, k2_dsmem<T>(), st>>>(
-        d_xy, n, index_base, d_oct, hdr_of(d_ws), status_of(d_ws), d_surv, d_count, (unsigned)nsuper, (int)subs);
+        d_xy, n, index_base, d_oct, hdr_of(d_ws), status_of(d_ws), d_surv, d_count, (unsigned)nsuper, (int)subs,
+        pp);
     return cuda_check("k2_filter_compact");
 }
 
@@ -1682,6 +1806,7 @@ const char *ch_status_str(ch_status s)
     case CH_ERR_MISALIGNED: return "CH_ERR_MISALIGNED";
     case CH_ERR_WORKSPACE: return "CH_ERR_WORKSPACE";
     case CH_ERR_CUDA: return "CH_ERR_CUDA";
+    case CH_ERR_PEER: return "CH_ERR_PEER";
     }
     return "CH_ERR_UNKNOWN";
 }
@@ -1725,6 +1850,10 @@ ch_status ch_read_result(const void *d_ws, ch_result *h_res, void *stream)
         return s;
     if (h_res->nonfinite)
         return fail(CH_ERR_NONFINITE, "non-finite coordinate in input");
+    unsigned late = 0;
+    cudaMemcpy(&late, &((const WsHeader *)d_ws)->peer_timeout, sizeof(unsigned), cudaMemcpyDeviceToHost);
+    if (late)
+        return fail(CH_ERR_PEER, "peer exchange timed out (a rank's record did not arrive)");
     return CH_OK;
 }
 
@@ -1973,6 +2102,157 @@ ch_status ch_graph_destroy(ch_graph *g)
         cudaGraphDestroy(g->graph);
     delete g;
     return CH_OK;
+}
+
+} // extern "C"
+
+struct ch_peer {
+    int rank = 0, world = 0;
+    unsigned long long *d_buf = nullptr;           // this rank's exchange buffer
+    unsigned long long *base[CH_MAX_PEERS] = {};   // every rank's, mapped here
+    bool opened[CH_MAX_PEERS] = {};
+    unsigned long long epoch = 0;                  // steps issued
+};
+
+namespace {
+template <typename T>
+ch_status step_peer(ch_peer *p, const T *d_xy, int64_t n_local, int64_t index_base, int flags, int64_t *d_survivors,
+                    void *d_ws, size_t ws_bytes, void *stream)
+{
+    if (!p || !p->base[0])
+        return fail(CH_ERR_INVALID_ARG, "peer exchange not opened");
+    if (n_local < 0 || (n_local > 0 && !d_survivors))
+        return fail(CH_ERR_INVALID_ARG, "bad shard arguments");
+    ch_status s;
+    if (n_local > 0 && (s = check_points(d_xy, n_local)) != CH_OK)
+        return s;
+    if ((s = check_ws(d_ws, ws_bytes, n_local)) != CH_OK)
+        return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    PeerPush pp{};
+    for (int r = 0; r < p->world; r++)
+        pp.base[r] = p->base[r];
+    pp.world = p->world;
+    pp.rank = p->rank;
+    pp.epoch = ++p->epoch;
+    if (n_local > 0) {
+        if ((s = launch_k1(d_xy, n_local, index_base, flags, nullptr, d_ws, st, pp)) != CH_OK)
+            return s;
+    } else {
+        k_peer_push<<<1, 256, 0, st>>>(pp, 0);
+    }
+    k3_combine8_peer<<<1, 256, 0, st>>>(pp, flags, hdr_of(d_ws));
+    if ((s = cuda_check("k3_combine8_peer")) != CH_OK)
+        return s;
+    if (n_local > 0)
+        return launch_k2(d_xy, n_local, index_base, &hdr_of(d_ws)->oct, (long long *)d_survivors, nullptr, d_ws, st,
+                         pp);
+    k_peer_push<<<1, 32, 0, st>>>(pp, 1);
+    return cuda_check("k_peer_push");
+}
+} // namespace
+
+extern "C" {
+
+size_t ch_peer_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+ch_status ch_peer_create(int rank, int world, ch_peer **out, void *h_handle)
+{
+    if (!out || !h_handle || world < 1 || world > CH_MAX_PEERS || rank < 0 || rank >= world)
+        return fail(CH_ERR_INVALID_ARG, "bad rank / world (1 <= world <= CH_MAX_PEERS)");
+    ch_peer *p = new ch_peer();
+    p->rank = rank;
+    p->world = world;
+    if (cudaMalloc((void **)&p->d_buf, PEER_BUF_BYTES) != cudaSuccess ||
+        cudaMemset(p->d_buf, 0, PEER_BUF_BYTES) != cudaSuccess) {
+        delete p;
+        return cuda_check("peer buffer");
+    }
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, p->d_buf) != cudaSuccess) {
+        cudaFree(p->d_buf);
+        delete p;
+        return fail(CH_ERR_CUDA, "cudaIpcGetMemHandle failed");
+    }
+    memcpy(h_handle, &h, sizeof(h));
+    p->base[rank] = p->d_buf;
+    *out = p;
+    return CH_OK;
+}
+
+ch_status ch_peer_open(ch_peer *p, const void *h_handles)
+{
+    if (!p || !h_handles)
+        return fail(CH_ERR_INVALID_ARG, "NULL argument");
+    for (int r = 0; r < p->world; r++) {
+        if (r == p->rank || p->opened[r])
+            continue;
+        cudaIpcMemHandle_t h;
+        memcpy(&h, (const char *)h_handles + r * sizeof(h), sizeof(h));
+        void *ptr = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(CH_ERR_CUDA, std::string("cudaIpcOpenMemHandle failed: ") + cudaGetErrorString(e));
+        }
+        p->base[r] = (unsigned long long *)ptr;
+        p->opened[r] = true;
+    }
+    cudaDeviceSynchronize();
+    return cuda_check("peer open");
+}
+
+ch_status ch_peer_destroy(ch_peer *p)
+{
+    if (!p)
+        return CH_OK;
+    cudaDeviceSynchronize();
+    for (int r = 0; r < p->world; r++)
+        if (p->opened[r])
+            cudaIpcCloseMemHandle(p->base[r]);
+    cudaFree(p->d_buf);
+    delete p;
+    cudaGetLastError();
+    return CH_OK;
+}
+
+ch_status ch_filter_step_peer(ch_peer *p, const double *d_xy, int64_t n_local, int64_t index_base, int flags,
+                              int64_t *d_survivors, void *d_ws, size_t ws_bytes, void *stream)
+{
+    return step_peer(p, d_xy, n_local, index_base, flags, d_survivors, d_ws, ws_bytes, stream);
+}
+
+ch_status ch_filter_step_peer_f32(ch_peer *p, const float *d_xy, int64_t n_local, int64_t index_base, int flags,
+                                  int64_t *d_survivors, void *d_ws, size_t ws_bytes, void *stream)
+{
+    return step_peer(p, d_xy, n_local, index_base, flags, d_survivors, d_ws, ws_bytes, stream);
+}
+
+ch_status ch_peer_counts(ch_peer *p, int64_t *h_counts, void *stream)
+{
+    if (!p || !h_counts)
+        return fail(CH_ERR_INVALID_ARG, "NULL argument");
+    cudaStreamSynchronize((cudaStream_t)stream);
+    ch_status s = cuda_check("peer counts");
+    if (s != CH_OK)
+        return s;
+    const size_t bank = (size_t)(p->epoch & 1) * CH_MAX_PEERS * PEER_SLOT;
+    std::vector<unsigned long long> buf((size_t)p->world * PEER_SLOT);
+    const auto t0 = std::chrono::steady_clock::now();
+    while (true) {
+        cudaMemcpy(buf.data(), p->d_buf + bank, buf.size() * 8, cudaMemcpyDeviceToHost);
+        bool all = true;
+        for (int r = 0; r < p->world; r++)
+            all = all && buf[(size_t)r * PEER_SLOT + PEER_CNT_FLAG] == p->epoch;
+        if (all)
+            break;
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10))
+            return fail(CH_ERR_PEER, "peer exchange timed out (a rank's count did not arrive)");
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    for (int r = 0; r < p->world; r++)
+        h_counts[r] = (int64_t)buf[(size_t)r * PEER_SLOT + PEER_CNT];
+    return cuda_check("peer counts");
 }
 
 ch_status ch_filter_host(const double *h_xy, int64_t n, int flags, double *d_xy_staging, int64_t *d_survivors,

@@ -11,17 +11,26 @@ exchange steps of the path (north_star):
 The survivors stay distributed (rank r owns [off_r, off_r + cnt_r)); the
 physical gather belongs to the separately timed hull stage.
 
+Two transports for those exchanges (DistFilter(exchange=...)):
+  "peer"  fused into the kernels over peer memory (ch_filter_step_peer): K1's
+          last CTA stores its record into every peer's exchange buffer
+          (cudaIpc-mapped, NVLink / NVSwitch), K3 acquires the W records,
+          K2's last CTA stores its count likewise -- no collective launches;
+  "nccl"  torch.distributed all-gathers (NCCL over NVLink; gloo on CPU).
+
 The collective helpers (`exchange_extremes`, `exclusive_offsets`) work on
 CPU tensors with the gloo backend as well, which is how the host logic is
 tested without GPUs (tests/test_dist_gloo.py).
 """
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import Workspace, _points, combine8, extremes8_async, filter_compact
+from . import Workspace, _fn, _lib, _plain, _points, _ptr, _stream, combine8, extremes8_async, filter_compact
 
 EXT_WORDS = 24  # ch_extremes = int64 idx[8] + double x[8] + double y[8]
 
@@ -84,11 +93,63 @@ def offsets_from_counts(counts, rank: int) -> tuple[int, int]:
     return sum(c[:rank]), sum(c)
 
 
+class PeerExchange:
+    """The fused-exchange endpoint of one rank (ch_peer_*): its exchange
+    buffer's IPC handle is all-gathered once over the process group (the only
+    use of torch.distributed on this path) and the peers' buffers mapped."""
+
+    def __init__(self, group=None):
+        lib = _lib.load()
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world > _lib.CH_MAX_PEERS:
+            raise ValueError(f"peer exchange supports at most {_lib.CH_MAX_PEERS} ranks")
+        hb = int(lib.ch_peer_handle_bytes())
+        mine = (ctypes.c_uint8 * hb)()
+        h = ctypes.c_void_p()
+        _lib.check(lib.ch_peer_create(self.rank, self.world, ctypes.byref(h), mine), "ch_peer_create")
+        self._h = h
+        t = torch.tensor(bytearray(mine), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        allh = torch.empty(self.world * hb, dtype=torch.uint8, device=t.device)
+        _all_gather_flat(allh, t, group)
+        buf = (ctypes.c_uint8 * (self.world * hb)).from_buffer_copy(bytes(allh.cpu().numpy()))
+        _lib.check(lib.ch_peer_open(self._h, buf), "ch_peer_open")
+
+    @property
+    def handle(self):
+        return self._h
+
+    def step(self, xy, n_local: int, index_base: int, ws: Workspace, out: torch.Tensor, plain=False, stream=None):
+        lib = _lib.load()
+        _lib.check(_fn(lib, "ch_filter_step_peer", xy)(self._h, _ptr(xy), n_local, index_base, _plain(plain),
+                                                       _ptr(out), ws.ptr, ws.nbytes, _stream(stream)),
+                   "ch_filter_step_peer")
+
+    def counts(self, stream=None) -> list[int]:
+        c = (ctypes.c_int64 * self.world)()
+        _lib.check(_lib.load().ch_peer_counts(self._h, c, _stream(stream)), "ch_peer_counts")
+        return list(c)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().ch_peer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class DistFilter:
     """Per-rank state for the sharded filter step (all device buffers are
     allocated once; `step` only enqueues work)."""
 
-    def __init__(self, n_global: int, xy_local: torch.Tensor, group=None, plain: bool = False):
+    def __init__(self, n_global: int, xy_local: torch.Tensor, group=None, plain: bool = False,
+                 exchange: str = "nccl"):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -106,10 +167,17 @@ class DistFilter:
         self.count = torch.zeros(1, dtype=torch.int64, device=dev)
         self.counts = torch.empty(self.world, dtype=torch.int64, device=dev)
         self.out = torch.empty(max(self.n_local, 1), dtype=torch.int64, device=dev)
+        if exchange not in ("nccl", "peer"):
+            raise ValueError("exchange must be 'nccl' or 'peer'")
+        self.exchange = exchange
+        self.peer = PeerExchange(group) if exchange == "peer" else None
 
     def step(self, xy_local: torch.Tensor | None = None):
         """K1 -> all-gather extremes -> K3 -> K2 -> all-gather counts (async)."""
         xy = self.xy if xy_local is None else xy_local
+        if self.peer is not None:   # the exchanges fused into K1 / K3 / K2
+            self.peer.step(xy, self.n_local, self.lo, self.ws, self.out, plain=self.plain)
+            return
         if self.n_local > 0:
             extremes8_async(xy, self.ws, index_base=self.lo, plain=self.plain, ext_out=self.ext_local)
         exchange_extremes(self.ext_local, self.group, out=self.ext_all)
@@ -120,6 +188,11 @@ class DistFilter:
 
     def result(self):
         """(local survivor indices (device view), offset, total) -- synchronizes."""
+        if self.peer is not None:
+            c = self.peer.counts()
+            self.counts.copy_(torch.tensor(c, dtype=torch.int64))
+            off, total = offsets_from_counts(c, self.rank)
+            return self.out[: c[self.rank]], off, total
         off, total = offsets_from_counts(self.counts, self.rank)
         cnt = int(self.counts[self.rank].item())
         return self.out[:cnt], off, total

@@ -7,6 +7,7 @@ out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--
 npts = float(sys.argv[2]); top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
 hdr, cur, path = None, None, ""
 lines = collections.OrderedDict()
+seen = set()  # an inlined SASS instruction is listed under several source lines: count it once
 for r in csv.reader(io.StringIO(out)):
     if len(r) == 2 and r[0] == "File Path":
         path = r[1].split("/")[-1]; continue
@@ -17,6 +18,9 @@ for r in csv.reader(io.StringIO(out)):
     if r[0]:
         cur = (path, r[0], r[1].strip()[:70]); lines.setdefault(cur, collections.Counter())
     elif cur and r[2].startswith("0x"):
+        if r[2] in seen:
+            continue
+        seen.add(r[2])
         try: n = float(r[hdr.index("Thread Instructions Executed")])
         except ValueError: continue
         s = r[3].split()

@@ -422,6 +422,72 @@ def test_distfilter_multirank_single_gpu(world, storage):
     assert offs == sorted(offs) and offs[0] == 0
 
 
+def _peer_worker(rank, world, port, n, dist_name, storage, steps, q):
+    import os
+    import torch.distributed as tdist
+    from paper_2303_10581_b200 import dist as chdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = chdist.shard_range(n, world, rank)
+        xy = synth.points(dist_name, n, seed=4, device="cuda", lo=lo, hi=hi)
+        if storage == "f32":
+            xy = xy.float()
+        df = chdist.DistFilter(n, xy, exchange="peer")
+        outs = []
+        for _ in range(steps):       # several steps: both exchange banks, epochs
+            df.out.fill_(-1)
+            df.step()
+            loc, off, total = df.result()
+            outs.append((off, total, loc.cpu().numpy()))
+        tdist.barrier()
+        df.peer.close()
+        q.put((rank, lo, hi, outs))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,dist_name,storage", [(2, 1_000_003, "displaced", "f64"),
+                                                       (3, 777_777, "circle", "f32"),
+                                                       (3, 2, "normal", "f64")])
+def test_peer_exchange_multirank_single_gpu(world, n, dist_name, storage):
+    """The fused exchange (ch_filter_step_peer: K1 stores its extremes record
+    into every peer's cudaIpc-mapped buffer, K3 acquires them, K2 stores its
+    count) with `world` processes sharing cuda:0: every step's concatenated
+    survivors equal the oracle, offsets are the exclusive scan.  n = 2 with
+    3 ranks leaves rank 0 with an empty shard."""
+    import socket
+    import torch.multiprocessing as mp
+    steps = 3
+    s0 = socket.socket(); s0.bind(("127.0.0.1", 0)); port = s0.getsockname()[1]; s0.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, n, dist_name, storage, steps, q))
+             for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for p_ in procs:
+        p_.join(timeout=60)
+    for r in res:
+        assert len(r) == 4, r[1]
+    full = synth.points(dist_name, n, seed=4, device="cuda")
+    if storage == "f32":
+        full = full.float()
+    want, _ = oracle.filter_compact(full.double().cpu().numpy())
+    for k in range(steps):
+        got = np.concatenate([r[3][k][2] for r in res])
+        assert np.array_equal(got, want), k
+        assert all(r[3][k][1] == len(want) for r in res)
+        offs = [r[3][k][0] for r in res]
+        sizes = [len(r[3][k][2]) for r in res]
+        assert offs == [sum(sizes[:i]) for i in range(world)]
+
+
 def test_cub_variant_baseline_same_survivors():
     """the CUB Variant #4 rebuild finds the same survivors."""
     import ctypes
