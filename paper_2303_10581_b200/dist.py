@@ -102,20 +102,38 @@ class PeerExchange:
         lib = _lib.load()
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self._h = None
         if self.world > _lib.CH_MAX_PEERS:
             raise ValueError(f"peer exchange supports at most {_lib.CH_MAX_PEERS} ranks")
         hb = int(lib.ch_peer_handle_bytes())
         mine = (ctypes.c_uint8 * hb)()
         h = ctypes.c_void_p()
-        _lib.check(lib.ch_peer_create(self.rank, self.world, ctypes.byref(h), mine), "ch_peer_create")
-        self._h = h
-        t = torch.tensor(bytearray(mine), dtype=torch.uint8)
+        ok = lib.ch_peer_create(self.rank, self.world, ctypes.byref(h), mine) == _lib.CH_OK
+        if ok:
+            self._h = h
+        # every rank takes part in both gathers, so a failure anywhere is
+        # seen everywhere and all ranks fall back together
+        allh = self._gather(bytes([int(ok)]) + bytes(mine), group)
+        if not all(allh[r * (hb + 1)] for r in range(self.world)):
+            self.close()
+            raise RuntimeError("peer exchange unavailable on some rank (ch_peer_create)")
+        handles = b"".join(allh[r * (hb + 1) + 1:(r + 1) * (hb + 1)] for r in range(self.world))
+        buf = (ctypes.c_uint8 * len(handles)).from_buffer_copy(handles)
+        st = lib.ch_peer_open(self._h, buf)
+        oks = self._gather(bytes([int(st == _lib.CH_OK)]), group)
+        if not all(oks):
+            detail = (lib.ch_last_error() or b"").decode() if st != _lib.CH_OK else "on another rank"
+            self.close()
+            raise RuntimeError(f"peer exchange unavailable (ch_peer_open: {detail})")
+
+    @staticmethod
+    def _gather(payload: bytes, group) -> bytes:
+        t = torch.tensor(bytearray(payload), dtype=torch.uint8)
         if dist.get_backend(group) == "nccl":
             t = t.cuda()
-        allh = torch.empty(self.world * hb, dtype=torch.uint8, device=t.device)
-        _all_gather_flat(allh, t, group)
-        buf = (ctypes.c_uint8 * (self.world * hb)).from_buffer_copy(bytes(allh.cpu().numpy()))
-        _lib.check(lib.ch_peer_open(self._h, buf), "ch_peer_open")
+        out = torch.empty(dist.get_world_size(group) * len(payload), dtype=torch.uint8, device=t.device)
+        _all_gather_flat(out, t, group)
+        return bytes(out.cpu().numpy())
 
     @property
     def handle(self):

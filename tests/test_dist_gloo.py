@@ -114,3 +114,39 @@ def test_pack_unpack_roundtrip():
     assert np.array_equal(i2[0], idx)
     assert np.array_equal(x2[0].view(np.int64), x.view(np.int64))
     assert np.array_equal(y2[0].view(np.int64), y.view(np.int64))
+
+
+def _peer_fallback_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        try:
+            chdist.PeerExchange()
+            q.put((rank, "created"))
+        except RuntimeError as e:
+            q.put((rank, "unavailable: " + str(e)))
+        dist.barrier()   # no rank is left hanging in a collective
+        q.put((rank, "done"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_failure_is_collective():
+    """Without a GPU ch_peer_create fails; every rank must see the failure
+    (and fall back together) rather than some ranks waiting in the handle
+    all-gather -- the consistency logic of PeerExchange, on CPU."""
+    if torch.cuda.is_available():
+        pytest.skip("needs a machine without a GPU")
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_fallback_worker, args=(r, world, port, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    msgs = [q.get(timeout=120) for _ in range(2 * world)]
+    for p_ in procs:
+        p_.join(timeout=60)
+    status = [m[1] for m in msgs if m[1] != "done"]
+    assert len(status) == world and all(m.startswith("unavailable") for m in status), status
+    assert sum(m[1] == "done" for m in msgs) == world
