@@ -525,6 +525,11 @@ k1_extremes8(const T *__restrict__ xy, long long n, long long index_base, int fl
         if ((it & (K1_SHARE - 1)) == 0)
             k1_warp_share(b); // uniform: every lane of the CTA runs the same iterations
     }
+    // PDL: this CTA is done reading the points; K2 (launched with programmatic
+    // stream serialization) may start its prologue and stream its first
+    // sub-tiles while the reductions and the last CTA's octagon build finish
+    // (K2's octagon readers wait with griddepcontrol.wait).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     double v[8];
     long long id[8];
 #pragma unroll
@@ -1083,7 +1088,8 @@ __device__ __forceinline__ void store_group32(long long *pb, unsigned m, int c, 
 // progress.  Hand-offs use named barriers (bar.arrive / bar.sync):
 // K2_BAR_BASE + b: consumers arrive, publisher syncs (buffer b full);
 // K2_BAR_BASE + 2 + b: publisher arrives, consumers sync (buffer b's offset
-// known); K2_BAR_BASE + 4: consumers only.
+// known); K2_BAR_BASE + 4: consumers only; K2_BAR_BASE + 5: consumers and
+// publisher, once (the octagon is loaded).
 constexpr unsigned TILE_DONE = 0xffffffffu;
 
 __device__ __forceinline__ void bar_sync(int id, int nthreads)
@@ -1133,9 +1139,16 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    load_soct(so, oct);
     __syncthreads();
     const unsigned epoch = s_epoch & ST_EPOCH_MASK;
+    if (warp != K2_PROD_WARP) {
+        // PDL: the octagon comes from the preceding kernel (K1's last CTA or
+        // K3); everything that reads it or publishes results waits for that
+        // grid here.  The producer only streams points, so it starts at once.
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        load_soct(so, oct);
+        bar_sync(K2_BAR_BASE + 5, K2_CTHREADS + 32); // consumers + publisher: `so` is ready
+    }
 
     if (warp == K2_PROD_WARP) {
         // ------------------------------------------------ TMA producer --
@@ -1757,9 +1770,22 @@ ch_status launch_k2(const T *d_xy, long long n, long long index_base, const ch_o
     subs = std::max<long long>(1, std::min<long long>(subs, (long long)k2_maxsub<T>()));
     long long nsuper = (nsub_total + subs - 1) / subs;
     long long grid = std::max<long long>(1, std::min<long long>(resident, nsuper));
-    k2_filter_compact<T><<<(unsigned)grid, K2_THREADS, k2_dsmem<T>(), st>>>(
-        d_xy, n, index_base, d_oct, hdr_of(d_ws), status_of(d_ws), d_surv, d_count, (unsigned)nsuper, (int)subs,
-        pp);
+    // programmatic dependent launch: K2's producer overlaps the tail of K1
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(K2_THREADS);
+    cfg.dynamicSmemBytes = k2_dsmem<T>();
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k2_filter_compact<T>, d_xy, (long long)n, (long long)index_base, d_oct,
+                                             hdr_of(d_ws), status_of(d_ws), (long long *)d_surv, (long long *)d_count,
+                                             (unsigned)nsuper, (int)subs, pp);
+    if (e != cudaSuccess)
+        return fail(CH_ERR_CUDA, std::string("k2_filter_compact: ") + cudaGetErrorString(e));
     return cuda_check("k2_filter_compact");
 }
 
