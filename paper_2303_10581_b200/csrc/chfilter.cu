@@ -628,6 +628,7 @@ __device__ void combine_records(const ch_extremes *all, int world, int flags, Ws
 __global__ void __launch_bounds__(256) k3_combine8(const ch_extremes *__restrict__ all, int world, int flags,
                                                    WsHeader *hdr)
 {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // K2's producer may start (PDL)
     combine_records(all, world, flags, hdr);
 }
 
@@ -640,6 +641,7 @@ __global__ void __launch_bounds__(256) k3_combine8_peer(const PeerPush pp, int f
     __shared__ ch_extremes s_all[CH_MAX_PEERS];
     __shared__ int s_late;
     const int tid = threadIdx.x;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // K2's producer streams while we wait (PDL)
     if (tid == 0)
         s_late = 0;
     __syncthreads();
