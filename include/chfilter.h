@@ -292,21 +292,22 @@ ch_status ch_hull_points(const double *h_pts, const int64_t *h_ids, int64_t m,
                          int64_t *h_hull, int64_t *h_n_hull);
 
 /* f1: Algorithm 1 line 4 on the device (future work P:432):
- * the exact strict hull of the m survivors d_surv (indices into d_xy), same
- * canonical form as ch_hull_points (DESIGN R8).  Two stable radix sorts by
+ * the exact strict hull of the m survivors d_surv (indices into d_xy, which
+ * holds n_points points), same canonical form as ch_hull_points (DESIGN R8).
+ * n_points < 2^32 lets the sorts carry 32-bit ids.  Two stable radix sorts by
  * (x, y), per-chunk exact monotone chains, a tree of exact bridge merges.
  * Scratch: ch_hull_gpu_temp_bytes(m) bytes at d_tmp.  Hull ids go to h_hull
  * (host, capacity m); synchronizes `stream`. */
 size_t ch_hull_gpu_temp_bytes(int64_t m);
-ch_status ch_hull_gpu(const double *d_xy, const int64_t *d_surv, int64_t m, int64_t *h_hull,
+ch_status ch_hull_gpu(const double *d_xy, int64_t n_points, const int64_t *d_surv, int64_t m, int64_t *h_hull,
                       int64_t *h_n_hull, void *d_tmp, size_t tmp_bytes, void *stream);
 /* The same hull kept on the device ("avoiding unnecessary data copying
  * between the device and host"): ids to d_hull (device, capacity m), the
  * count to *d_n_hull (device int64).  Fully asynchronous on `stream`; d_tmp
  * (ch_hull_gpu_temp_bytes(m)) must stay untouched until the stream reaches
  * this point.  m == 0 writes a zero count. */
-ch_status ch_hull_gpu_async(const double *d_xy, const int64_t *d_surv, int64_t m, int64_t *d_hull,
-                            int64_t *d_n_hull, void *d_tmp, size_t tmp_bytes, void *stream);
+ch_status ch_hull_gpu_async(const double *d_xy, int64_t n_points, const int64_t *d_surv, int64_t m,
+                            int64_t *d_hull, int64_t *d_n_hull, void *d_tmp, size_t tmp_bytes, void *stream);
 
 #define CH_HULL_HOST 4 /* flag for ch_hull_end_to_end: gather + host monotone chain */
 

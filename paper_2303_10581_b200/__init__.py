@@ -266,8 +266,8 @@ def hull_gpu(xy: torch.Tensor, surv: torch.Tensor, stream=None) -> np.ndarray:
     tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=xy.device)
     out = np.zeros(max(m, 1), dtype=np.int64)
     h = ctypes.c_int64(0)
-    _lib.check(lib.ch_hull_gpu(_ptr(xy), _ptr(surv), m, out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(h),
-                               _ptr(tmp), tb, _stream(stream)), "ch_hull_gpu")
+    _lib.check(lib.ch_hull_gpu(_ptr(xy), xy.shape[0], _ptr(surv), m, out.ctypes.data_as(ctypes.c_void_p),
+                               ctypes.byref(h), _ptr(tmp), tb, _stream(stream)), "ch_hull_gpu")
     return out[: h.value].copy()
 
 
@@ -283,8 +283,8 @@ def hull_gpu_async(xy: torch.Tensor, surv: torch.Tensor, tmp: torch.Tensor | Non
         tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=xy.device)
     ids = torch.empty(max(m, 1), dtype=torch.int64, device=xy.device)
     cnt = torch.empty(1, dtype=torch.int64, device=xy.device)
-    _lib.check(lib.ch_hull_gpu_async(_ptr(xy), _ptr(surv), m, _ptr(ids), _ptr(cnt), _ptr(tmp), tb, _stream(stream)),
-               "ch_hull_gpu_async")
+    _lib.check(lib.ch_hull_gpu_async(_ptr(xy), xy.shape[0], _ptr(surv), m, _ptr(ids), _ptr(cnt), _ptr(tmp), tb,
+                                     _stream(stream)), "ch_hull_gpu_async")
     return ids, cnt
 
 

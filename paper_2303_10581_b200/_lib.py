@@ -84,8 +84,8 @@ SIGNATURES = {
     "ch_gather_points": (ctypes.c_int, [P, I64, P, I64, P, P]),
     "ch_hull_points": (ctypes.c_int, [P, P, I64, P, ctypes.POINTER(I64)]),
     "ch_hull_gpu_temp_bytes": (SZ, [I64]),
-    "ch_hull_gpu": (ctypes.c_int, [P, P, I64, P, ctypes.POINTER(I64), P, SZ, P]),
-    "ch_hull_gpu_async": (ctypes.c_int, [P, P, I64, P, P, P, SZ, P]),
+    "ch_hull_gpu": (ctypes.c_int, [P, I64, P, I64, P, ctypes.POINTER(I64), P, SZ, P]),
+    "ch_hull_gpu_async": (ctypes.c_int, [P, I64, P, I64, P, P, P, SZ, P]),
     "ch_hull_workspace_bytes": (SZ, [I64]),
     "ch_hull_end_to_end": (ctypes.c_int, [P, I64, ctypes.c_int, P, ctypes.POINTER(I64), P,
                                           ctypes.POINTER(I64), ctypes.POINTER(Stats), P, SZ, P]),

@@ -2373,7 +2373,7 @@ ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *
         void *d_tmp = tail ? (void *)((char *)d_ws + off) : nullptr;
         if (!tail && cudaMallocAsync(&d_tmp, tb, st) != cudaSuccess)
             return fail(CH_ERR_CUDA, "cudaMallocAsync for the device hull failed");
-        s = ch_hull_gpu(d_xy, d_survivors, cnt, h_hull, &h, d_tmp, tb, stream);
+        s = ch_hull_gpu(d_xy, n, d_survivors, cnt, h_hull, &h, d_tmp, tb, stream);
         if (!tail)
             cudaFreeAsync(d_tmp, st);
         cudaStreamSynchronize(st);

@@ -17,6 +17,9 @@
 //      bridge (two-pointer walk with the same exact turn test; the result is
 //      the unique strict lower chain of A u B), then copied in parallel;
 //   4. lower[0..-1) + upper[0..-1) mapped back to ids.
+// Chain positions (indices into the sorted points) are 32-bit words when
+// m < 2^32, else 64-bit; the merge copies index groups with shifts (the
+// group span is a power of two).
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
@@ -40,28 +43,31 @@ __device__ __forceinline__ unsigned long long okey(double d)
     return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
 }
 
+template <typename V>
 __global__ void k_ykeys(const double *__restrict__ xy, const long long *__restrict__ surv, long long m,
-                        unsigned long long *__restrict__ key, long long *__restrict__ val)
+                        unsigned long long *__restrict__ key, V *__restrict__ val)
 {
     for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x) {
         const long long id = surv[j];
         key[j] = okey(xy[2 * id + 1]);
-        val[j] = id;
+        val[j] = (V)id;
     }
 }
 
-__global__ void k_xkeys(const double *__restrict__ xy, const long long *__restrict__ val, long long m,
+template <typename V>
+__global__ void k_xkeys(const double *__restrict__ xy, const V *__restrict__ val, long long m,
                         unsigned long long *__restrict__ key)
 {
     for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x)
-        key[j] = okey(xy[2 * val[j]]);
+        key[j] = okey(xy[2 * (long long)val[j]]);
 }
 
-__global__ void k_points(const double *__restrict__ xy, const long long *__restrict__ val, long long m,
+template <typename V>
+__global__ void k_points(const double *__restrict__ xy, const V *__restrict__ val, long long m,
                          double2 *__restrict__ P)
 {
     for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x) {
-        const long long id = val[j];
+        const long long id = (long long)val[j];
         P[j] = make_double2(xy[2 * id], xy[2 * id + 1]);
     }
 }
@@ -86,7 +92,8 @@ __device__ __forceinline__ int turn(const double2 &a, const double2 &b, const do
 }
 
 // Andrew's monotone chain over one chunk; the stack lives in pos[start..].
-__global__ void k_chunk_chain(Seq s, long long nchunks, long long *__restrict__ pos, long long *__restrict__ len)
+template <typename I>
+__global__ void k_chunk_chain(Seq s, long long nchunks, I *__restrict__ pos, long long *__restrict__ len)
 {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nchunks)
@@ -104,7 +111,7 @@ __global__ void k_chunk_chain(Seq s, long long nchunks, long long *__restrict__ 
             if (top >= 2)
                 p2 = s.at(pos[start + top - 2]);
         }
-        pos[start + top] = r;
+        pos[start + top] = (I)r;
         top++;
         p2 = p1;
         p1 = pr;
@@ -113,7 +120,8 @@ __global__ void k_chunk_chain(Seq s, long long nchunks, long long *__restrict__ 
 }
 
 // Bridge of the chains of chunk groups L = 2pw and R = (2p+1)w.
-__global__ void k_bridge(Seq s, long long nchunks, long long w, const long long *__restrict__ pos,
+template <typename I>
+__global__ void k_bridge(Seq s, long long nchunks, long long w, const I *__restrict__ pos,
                          const long long *__restrict__ len, long long *__restrict__ bi, long long *__restrict__ bj,
                          long long *__restrict__ len_out)
 {
@@ -125,7 +133,7 @@ __global__ void k_bridge(Seq s, long long nchunks, long long w, const long long 
     const long long lb = R < nchunks ? len[R] : 0;
     long long i = la - 1, j = 0;
     if (la > 0 && lb > 0) {
-        const long long *A = pos + L * HG_CHUNK, *B = pos + R * HG_CHUNK;
+        const I *A = pos + L * HG_CHUNK, *B = pos + R * HG_CHUNK;
         while (true) {
             bool changed = false;
             while (i > 0 && turn(s.at(A[i - 1]), s.at(A[i]), s.at(B[j])) <= 0) {
@@ -145,14 +153,16 @@ __global__ void k_bridge(Seq s, long long nchunks, long long w, const long long 
     len_out[L] = (i + 1) + (lb - j);
 }
 
-// Parallel copy of every merged chain: A[0..i] then B[j..].
-__global__ void k_merge_copy(long long m_cap, long long nchunks, long long w, const long long *__restrict__ pos_in,
-                             const long long *__restrict__ len_out, const long long *__restrict__ bi,
-                             const long long *__restrict__ bj, long long *__restrict__ pos_out)
+// Parallel copy of every merged chain: A[0..i] then B[j..].  The group span
+// 2 w HG_CHUNK is a power of two: group and offset by shift and mask.
+template <typename I>
+__global__ void k_merge_copy(long long m_cap, long long nchunks, long long w, int span_log2,
+                             const I *__restrict__ pos_in, const long long *__restrict__ len_out,
+                             const long long *__restrict__ bi, const long long *__restrict__ bj, I *__restrict__ pos_out)
 {
-    const long long span = 2 * w * HG_CHUNK;
+    const long long mask = (1ll << span_log2) - 1;
     for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m_cap; g += (long long)gridDim.x * blockDim.x) {
-        const long long p = g / span, q = g - p * span;
+        const long long p = g >> span_log2, q = g & mask;
         const long long L = 2 * p * w;
         if (L >= nchunks || q >= len_out[L])
             continue;
@@ -164,15 +174,16 @@ __global__ void k_merge_copy(long long m_cap, long long nchunks, long long w, co
 // lower[0 .. nl-1) then upper[0 .. nu-1) (each excludes its last point,
 // which is the other's first); upper positions are in reversed order.  The
 // chain lengths are read on the device, so nothing waits for the host.
-__global__ void k_assemble(long long m, const long long *__restrict__ low, const long long *__restrict__ d_nl,
-                           const long long *__restrict__ up, const long long *__restrict__ d_nu,
-                           const long long *__restrict__ val, long long *__restrict__ out, long long *__restrict__ d_nh)
+template <typename I, typename V>
+__global__ void k_assemble(long long m, const I *__restrict__ low, const long long *__restrict__ d_nl,
+                           const I *__restrict__ up, const long long *__restrict__ d_nu,
+                           const V *__restrict__ val, long long *__restrict__ out, long long *__restrict__ d_nh)
 {
     const long long nl = *d_nl, nu = *d_nu;
     if (nl <= 1) {
         // a single distinct point: the lowest id among all survivors
         if (blockIdx.x == 0 && threadIdx.x == 0) {
-            out[0] = val[low[0]];
+            out[0] = (long long)val[low[0]];
             *d_nh = 1;
         }
         return;
@@ -181,7 +192,7 @@ __global__ void k_assemble(long long m, const long long *__restrict__ low, const
     if (blockIdx.x == 0 && threadIdx.x == 0)
         *d_nh = total;
     for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x)
-        out[g] = g < a ? val[low[g]] : val[m - 1 - up[g - a]];
+        out[g] = (long long)(g < a ? val[low[g]] : val[m - 1 - (long long)up[g - a]]);
 }
 
 int grid_for(long long work, int threads)
@@ -195,18 +206,25 @@ int grid_for(long long work, int threads)
 // One chain (lower: rev = 0, upper: rev = 1) of the m sorted points P; the
 // result positions are in the returned buffer (pos_a or pos_b), the length in
 // the returned device word (len_a[0] or len_b[0]).  Asynchronous.
-static long long *chain_gpu(const double2 *P, long long m, int rev, long long *pos_a, long long *pos_b, long long *len_a,
-                            long long *len_b, long long *bi, long long *bj, const long long **d_len, cudaStream_t st)
+template <typename I>
+static I *chain_gpu(const double2 *P, long long m, int rev, I *pos_a, I *pos_b, long long *len_a, long long *len_b,
+                    long long *bi, long long *bj, const long long **d_len, cudaStream_t st)
 {
     const long long nchunks = (m + HG_CHUNK - 1) / HG_CHUNK;
     const long long m_cap = nchunks * HG_CHUNK;
     Seq s{P, m, rev};
-    k_chunk_chain<<<(unsigned)((nchunks + HG_THREADS - 1) / HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, pos_a, len_a);
-    for (long long w = 1; w < nchunks; w *= 2) {
+    k_chunk_chain<I><<<(unsigned)((nchunks + HG_THREADS - 1) / HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, pos_a,
+                                                                                                  len_a);
+    static_assert((HG_CHUNK & (HG_CHUNK - 1)) == 0, "chunk size is a power of two");
+    int span_log2 = 1;
+    while ((1ll << span_log2) < 2 * HG_CHUNK)
+        span_log2++;
+    for (long long w = 1; w < nchunks; w *= 2, span_log2++) {
         const long long npairs = (nchunks + 2 * w - 1) / (2 * w);
-        k_bridge<<<(unsigned)((npairs + HG_THREADS - 1) / HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, w, pos_a, len_a,
-                                                                                             bi, bj, len_b);
-        k_merge_copy<<<grid_for(m_cap, 256), 256, 0, st>>>(m_cap, nchunks, w, pos_a, len_b, bi, bj, pos_b);
+        k_bridge<I><<<(unsigned)((npairs + HG_THREADS - 1) / HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, w, pos_a,
+                                                                                                len_a, bi, bj, len_b);
+        k_merge_copy<I><<<grid_for(m_cap, 256), 256, 0, st>>>(m_cap, nchunks, w, span_log2, pos_a, len_b, bi, bj,
+                                                              pos_b);
         std::swap(pos_a, pos_b);
         std::swap(len_a, len_b);
     }
@@ -223,6 +241,7 @@ struct HullTmp {
         if (m < 1)
             m = 1;
         const size_t nchunks = (size_t)((m + HG_CHUNK - 1) / HG_CHUNK), cap = nchunks * HG_CHUNK;
+        const size_t isz = m < (1ll << 32) ? 4 : 8; // chain position width
         cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
         cub::DoubleBuffer<long long> vb(nullptr, nullptr);
         cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, kb, vb, (int64_t)m);
@@ -232,7 +251,7 @@ struct HullTmp {
         o_k0 = take((size_t)m * 8); o_k1 = take((size_t)m * 8);
         o_v0 = take((size_t)m * 8); o_v1 = take((size_t)m * 8);
         o_P = take((size_t)m * 16);
-        o_pa = take(cap * 8); o_pb = take(cap * 8); o_pc = take(cap * 8); o_pd = take(cap * 8);
+        o_pa = take(cap * isz); o_pb = take(cap * isz); o_pc = take(cap * isz); o_pd = take(cap * isz);
         o_la = take(nchunks * 8 + 8); o_lb = take(nchunks * 8 + 8);
         o_lc = take(nchunks * 8 + 8); o_ld = take(nchunks * 8 + 8);
         o_bi = take(nchunks * 8 + 8); o_bj = take(nchunks * 8 + 8);
@@ -240,6 +259,50 @@ struct HullTmp {
         total = p;
     }
 };
+
+// The pipeline with sort values (survivor ids) of type V.
+template <typename V>
+static ch_status hull_async(const double *d_xy, const long long *surv, long long m, long long *d_hull,
+                            long long *d_n_hull, void *d_tmp, const HullTmp &L, cudaStream_t st)
+{
+    char *b = (char *)d_tmp;
+    auto *k0 = (unsigned long long *)(b + L.o_k0), *k1 = (unsigned long long *)(b + L.o_k1);
+    auto *v0 = (V *)(b + L.o_v0), *v1 = (V *)(b + L.o_v1);
+    auto *P = (double2 *)(b + L.o_P);
+    auto *pa = b + L.o_pa, *pb = b + L.o_pb, *pc = b + L.o_pc, *pd = b + L.o_pd;
+    auto *la = (long long *)(b + L.o_la), *lb = (long long *)(b + L.o_lb);
+    auto *lc = (long long *)(b + L.o_lc), *ld = (long long *)(b + L.o_ld);
+    auto *bi = (long long *)(b + L.o_bi), *bj = (long long *)(b + L.o_bj);
+
+    const int g = grid_for(m, 256);
+    k_ykeys<V><<<g, 256, 0, st>>>(d_xy, surv, m, k0, v0);
+    cub::DoubleBuffer<unsigned long long> kb(k0, k1);
+    cub::DoubleBuffer<V> vb(v0, v1);
+    size_t tb = L.sort_tmp;
+    if (cub::DeviceRadixSort::SortPairs(d_tmp, tb, kb, vb, (int64_t)m, 0, 64, st) != cudaSuccess)
+        return CH_ERR_CUDA;
+    // x keys in the y-sorted order, then a stable sort by x
+    k_xkeys<V><<<g, 256, 0, st>>>(d_xy, vb.Current(), m, kb.Alternate());
+    kb.selector ^= 1;
+    tb = L.sort_tmp;
+    if (cub::DeviceRadixSort::SortPairs(d_tmp, tb, kb, vb, (int64_t)m, 0, 64, st) != cudaSuccess)
+        return CH_ERR_CUDA;
+    const V *val = vb.Current();
+    k_points<V><<<g, 256, 0, st>>>(d_xy, val, m, P);
+
+    auto chains = [&](auto tag) {
+        using I = decltype(tag);
+        const long long *d_hl, *d_hu;
+        const I *low = chain_gpu<I>(P, m, 0, (I *)pa, (I *)pb, la, lb, bi, bj, &d_hl, st);
+        const I *up = chain_gpu<I>(P, m, 1, (I *)pc, (I *)pd, lc, ld, bi, bj, &d_hu, st);
+        k_assemble<I, V><<<grid_for(m, 256), 256, 0, st>>>(m, low, d_hl, up, d_hu, val, d_hull, d_n_hull);
+    };
+    if (m < (1ll << 32))
+        chains((unsigned)0);
+    else
+        chains((long long)0);
+    return cudaGetLastError() == cudaSuccess ? CH_OK : CH_ERR_CUDA;
+}
 
 extern "C" {
 
@@ -251,55 +314,30 @@ size_t ch_hull_gpu_temp_bytes(int64_t m)
 
 // The device hull, asynchronous: hull ids to d_hull (device, capacity m), the
 // count to *d_n_hull (device).  No host synchronization.
-ch_status ch_hull_gpu_async(const double *d_xy, const int64_t *d_surv, int64_t m, int64_t *d_hull, int64_t *d_n_hull,
-                            void *d_tmp, size_t tmp_bytes, void *stream)
+ch_status ch_hull_gpu_async(const double *d_xy, int64_t n_points, const int64_t *d_surv, int64_t m,
+                            int64_t *d_hull, int64_t *d_n_hull, void *d_tmp, size_t tmp_bytes, void *stream)
 {
     cudaStream_t st = (cudaStream_t)stream;
-    if (m < 0 || !d_n_hull || (m > 0 && (!d_xy || !d_surv || !d_hull || !d_tmp)))
+    if (m < 0 || n_points < 0 || !d_n_hull || (m > 0 && (!d_xy || !d_surv || !d_hull || !d_tmp)))
         return CH_ERR_INVALID_ARG;
     if (m == 0)
         return cudaMemsetAsync(d_n_hull, 0, sizeof(int64_t), st) == cudaSuccess ? CH_OK : CH_ERR_CUDA;
     const HullTmp L(m);
     if (tmp_bytes < L.total)
         return CH_ERR_WORKSPACE;
-    char *b = (char *)d_tmp;
-    auto *k0 = (unsigned long long *)(b + L.o_k0), *k1 = (unsigned long long *)(b + L.o_k1);
-    auto *v0 = (long long *)(b + L.o_v0), *v1 = (long long *)(b + L.o_v1);
-    auto *P = (double2 *)(b + L.o_P);
-    auto *pa = (long long *)(b + L.o_pa), *pb = (long long *)(b + L.o_pb);
-    auto *pc = (long long *)(b + L.o_pc), *pd = (long long *)(b + L.o_pd);
-    auto *la = (long long *)(b + L.o_la), *lb = (long long *)(b + L.o_lb);
-    auto *lc = (long long *)(b + L.o_lc), *ld = (long long *)(b + L.o_ld);
-    auto *bi = (long long *)(b + L.o_bi), *bj = (long long *)(b + L.o_bj);
-
-    const int g = grid_for(m, 256);
-    k_ykeys<<<g, 256, 0, st>>>(d_xy, (const long long *)d_surv, m, k0, v0);
-    cub::DoubleBuffer<unsigned long long> kb(k0, k1);
-    cub::DoubleBuffer<long long> vb(v0, v1);
-    size_t tb = L.sort_tmp;
-    if (cub::DeviceRadixSort::SortPairs(d_tmp, tb, kb, vb, (int64_t)m, 0, 64, st) != cudaSuccess)
-        return CH_ERR_CUDA;
-    // x keys in the y-sorted order, then a stable sort by x
-    k_xkeys<<<g, 256, 0, st>>>(d_xy, vb.Current(), m, kb.Alternate());
-    kb.selector ^= 1;
-    tb = L.sort_tmp;
-    if (cub::DeviceRadixSort::SortPairs(d_tmp, tb, kb, vb, (int64_t)m, 0, 64, st) != cudaSuccess)
-        return CH_ERR_CUDA;
-    const long long *val = vb.Current();
-    k_points<<<g, 256, 0, st>>>(d_xy, val, m, P);
-
-    const long long *d_hl, *d_hu;
-    const long long *low = chain_gpu(P, m, 0, pa, pb, la, lb, bi, bj, &d_hl, st);
-    const long long *up = chain_gpu(P, m, 1, pc, pd, lc, ld, bi, bj, &d_hu, st);
-    k_assemble<<<grid_for(m, 256), 256, 0, st>>>(m, low, d_hl, up, d_hu, val, (long long *)d_hull,
-                                                 (long long *)d_n_hull);
-    return cudaGetLastError() == cudaSuccess ? CH_OK : CH_ERR_CUDA;
+    // ids fit 32 bits when the point array does: the sorts then move 12, not
+    // 16, bytes per element and pass
+    return n_points <= (1ll << 32) ? hull_async<unsigned>(d_xy, (const long long *)d_surv, m, (long long *)d_hull,
+                                                           (long long *)d_n_hull, d_tmp, L, st)
+                                   : hull_async<unsigned long long>(d_xy, (const long long *)d_surv, m,
+                                                                    (long long *)d_hull, (long long *)d_n_hull, d_tmp,
+                                                                    L, st);
 }
 
 // The device hull with the ids copied to h_hull (host, capacity m).
 // Synchronizes `stream`.
-ch_status ch_hull_gpu(const double *d_xy, const int64_t *d_surv, int64_t m, int64_t *h_hull, int64_t *h_n_hull,
-                      void *d_tmp, size_t tmp_bytes, void *stream)
+ch_status ch_hull_gpu(const double *d_xy, int64_t n_points, const int64_t *d_surv, int64_t m, int64_t *h_hull,
+                      int64_t *h_n_hull, void *d_tmp, size_t tmp_bytes, void *stream)
 {
     cudaStream_t st = (cudaStream_t)stream;
     if (!h_n_hull || (m > 0 && (!d_xy || !d_surv || !h_hull || !d_tmp)))
@@ -313,7 +351,7 @@ ch_status ch_hull_gpu(const double *d_xy, const int64_t *d_surv, int64_t m, int6
         return CH_ERR_WORKSPACE;
     int64_t *d_out = (int64_t *)((char *)d_tmp + L.o_out);
     int64_t *d_nh = d_out + m; // the word after the ids (o_out holds m + 1 words)
-    ch_status s = ch_hull_gpu_async(d_xy, d_surv, m, d_out, d_nh, d_tmp, tmp_bytes, stream);
+    ch_status s = ch_hull_gpu_async(d_xy, n_points, d_surv, m, d_out, d_nh, d_tmp, tmp_bytes, stream);
     if (s != CH_OK)
         return s;
     int64_t nh = 0;
