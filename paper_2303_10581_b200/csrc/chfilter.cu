@@ -786,19 +786,17 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
 }
 
 // Survivor mask for NP points of one thread (bit i = point i), bit-identical
-// to "not (forall k: D_k > T_k)" for every valid point (R4).  Stages, each
-// skipped when no lane of the warp needs it (warp-uniform branches):
+// to "not (forall k: D_k > T_k)" for every valid point (R4), without the
+// fp32 certificates: K2's path for caller-supplied octagons, degenerate or
+// out-of-domain ones, and the partial last sub-tile (full sub-tiles of
+// octagons built from the data take consume_cert).  Stages, each skipped
+// when no lane of the warp needs it (warp-uniform branches):
 //  1. the certified accept box (4 DSETP): inside => discarded (proof at
 //     chf::box_corner_ok);
-//  2. (has_f32) the fp32 pre-filter (proof at chf::octagon_edge): h_g <= 0
-//     on the octant-guessed edge certifies keep; then g_k >= 0 on every edge
-//     certifies discard; then h_k <= 0 on some edge certifies keep (these
-//     two with two points per FFMA2);
-//  3. fp64 D_k on every edge for the points left in the uncertainty band.
-// Without has_f32 (caller-supplied octagon), instead of stage 2, adaptively:
-// 2'. the guessed edge in fp64 (D_g <= T_g => kept, the oracle's exists-k
-// condition; a warp whose points 2' did not settle skips 2' for the next 15
-// sub-tiles), then stage 3 on every edge of every undecided point.
+//  2. adaptively, the octant-guessed edge in fp64 (D_g <= T_g => kept, the
+//     oracle's exists-k condition; a warp whose points it did not settle
+//     skips it for the next 15 sub-tiles);
+//  3. fp64 D_k on every edge for every undecided point.
 template <typename C, int NP>
 __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], const C (&py)[NP],
                                              unsigned valid, int &guess_mode)
