@@ -57,6 +57,7 @@ def parse():
                     help="point storage precision (f32: the paper's, widened exactly to f64)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--timed-events", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--exchange", choices=["auto", "peer", "nccl"], default="auto",
                     help="N > 1: extremes / count exchange fused into the kernels over peer memory (peer), or "
                          "NCCL all-gathers; auto = peer if it initializes")
@@ -376,6 +377,16 @@ def run_ours(a):
                     ev[k][3].record(stream)
                     exch2()
                 step_ev[k][1].record(stream)
+        elif a.timed_events:   # developer A/B: events between the kernels in the timed region
+            for k in range(K):
+                ev[k][0].record(stream)
+                k1()
+                ev[k][1].record(stream)
+                exch()
+                ev[k][2].record(stream)
+                k2()
+                ev[k][3].record(stream)
+                exch2()
         else:   # no events between the kernels (see the split pass above)
             for k in range(K):
                 k1(); exch(); k2(); exch2()
