@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", choices=["ours", "reference", "cub"], default="ours",
+    ap.add_argument("--impl", choices=["ours", "reference", "cub", "thrust-scan", "thrust-copy"], default="ours",
                     help="ours | reference (the CPU oracle arm) | cub (the paper's Variant #4 rebuilt "
                          "with CUB on this GPU, SURVEY f4: an in-box prior-art bar, not a driver arm)")
     ap.add_argument("--dist", choices=["normal", "circle", "displaced"], default="normal")
@@ -523,31 +523,37 @@ def run_ours(a):
 
 
 def run_cub(a):
-    """the paper's CUB Variant #4 (8 ArgMin/ArgMax reductions,
-    a flag kernel, DeviceSelect::Flagged) on the same GPU, same input."""
+    """the paper's library variants on the same GPU, same
+    input: #4 CUB (8 ArgMin/ArgMax reductions, a flag kernel,
+    DeviceSelect::Flagged), #2 Thrust scan + scatter, #3 Thrust copy_if."""
     import ctypes
     import paper_2303_10581_b200 as chf
     import synth
     sys.path.insert(0, os.path.join(ROOT, "baselines"))
     import build as bbuild  # baselines/build.py
     lib = ctypes.CDLL(bbuild.build())
-    lib.chb_cub_temp_bytes.restype = ctypes.c_size_t
-    lib.chb_cub_temp_bytes.argtypes = [ctypes.c_int64]
+    P, SZ, I64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int64
+    for f in ("chb_cub_temp_bytes", "chb_thrust_temp_bytes"):
+        getattr(lib, f).restype = SZ
+        getattr(lib, f).argtypes = [I64]
     lib.chb_cub_filter.restype = ctypes.c_int
-    lib.chb_cub_filter.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
-                                   ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    lib.chb_cub_filter.argtypes = [P, I64, P, ctypes.POINTER(I64), P, SZ, P]
+    lib.chb_thrust_filter.restype = ctypes.c_int
+    lib.chb_thrust_filter.argtypes = [ctypes.c_int, P, I64, P, ctypes.POINTER(I64), P, SZ, P]
     dev = torch.device("cuda", 0)
     n = int(a.n)
     xy = synth.points(a.dist, n, seed=a.seed, p=a.p, device=dev)
     out = torch.empty(n, dtype=torch.int64, device=dev)
-    tb = int(lib.chb_cub_temp_bytes(n))
+    variant = {"cub": 4, "thrust-scan": 2, "thrust-copy": 3}[a.impl]
+    tb = int(lib.chb_cub_temp_bytes(n) if variant == 4 else lib.chb_thrust_temp_bytes(n))
     tmp = torch.empty(tb, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     cnt = ctypes.c_int64(0)
 
     def step():
-        rc = lib.chb_cub_filter(ctypes.c_void_p(xy.data_ptr()), n, ctypes.c_void_p(out.data_ptr()), ctypes.byref(cnt),
-                                ctypes.c_void_p(tmp.data_ptr()), tb, ctypes.c_void_p(stream.cuda_stream))
+        args = (P(xy.data_ptr()), n, P(out.data_ptr()), ctypes.byref(cnt), P(tmp.data_ptr()), tb,
+                P(stream.cuda_stream))
+        rc = lib.chb_cub_filter(*args) if variant == 4 else lib.chb_thrust_filter(variant, *args)
         assert rc == 0, rc
 
     for _ in range(a.warmup):
@@ -562,11 +568,14 @@ def run_cub(a):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
-    print(json.dumps({"impl": "cub", "metric": METRIC, "value": n / (ms / 1e3) / 1e9, "unit": UNIT, "n_gpus": 1,
+    desc = {4: "paper Variant #4 cub-flagged (P:237-242), rebuilt with CUB",
+            2: "paper Variant #2 thrust-scan (P:219-222): min/max_element, transform, exclusive_scan, scatter",
+            3: "paper Variant #3 thrust-copy (P:224-225): min/max_element, copy_if"}[variant]
+    print(json.dumps({"impl": a.impl, "metric": METRIC, "value": n / (ms / 1e3) / 1e9, "unit": UNIT, "n_gpus": 1,
                       "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
                       "dtype": "f64", "data": "synthetic",
                       "config": {"workload": workload_name(a), "n": n, "survivors": int(cnt.value),
-                                 "variant": "paper Variant #4 cub-flagged (P:237-242), rebuilt with CUB"}}),
+                                 "variant": desc}}),
           flush=True)
     return 0
 
@@ -579,7 +588,7 @@ def main():
     a.plain = {"certified": False, "plain": True, "exact": "exact"}[a.predicate]
     if a.impl == "reference":
         return run_reference(a)
-    if a.impl == "cub":
+    if a.impl in ("cub", "thrust-scan", "thrust-copy"):
         return run_cub(a)
     return run_ours(a)
 

@@ -515,6 +515,36 @@ def test_cub_variant_baseline_same_survivors():
         assert np.array_equal(out[: cnt.value].cpu().numpy(), want), dist
 
 
+def test_thrust_variants_baseline_same_survivors():
+    """the Thrust Variants #2 (scan + scatter) and #3 (copy_if)
+    rebuilt on B200 find the oracle's survivors."""
+    import ctypes
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baselines"))
+    import build as bbuild
+    lib = ctypes.CDLL(bbuild.build())
+    lib.chb_thrust_temp_bytes.restype = ctypes.c_size_t
+    lib.chb_thrust_temp_bytes.argtypes = [ctypes.c_int64]
+    lib.chb_thrust_filter.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                      ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_size_t,
+                                      ctypes.c_void_p]
+    for dist in ("normal", "displaced", "circle"):
+        n = 777_777
+        xy = synth.points(dist, n, seed=3, device=DEV)
+        want, _ = oracle.filter_compact(xy.cpu().numpy())
+        for variant in (2, 3):
+            out = torch.full((n,), -1, dtype=torch.int64, device=DEV)
+            tb = int(lib.chb_thrust_temp_bytes(n))
+            tmp = torch.empty(tb, dtype=torch.uint8, device=DEV)
+            cnt = ctypes.c_int64(0)
+            rc = lib.chb_thrust_filter(variant, ctypes.c_void_p(xy.data_ptr()), n, ctypes.c_void_p(out.data_ptr()),
+                                       ctypes.byref(cnt), ctypes.c_void_p(tmp.data_ptr()), tb,
+                                       ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+            assert rc == 0
+            assert np.array_equal(out[: cnt.value].cpu().numpy(), want), (dist, variant)
+
+
 # --------------------------------------------- f3: the exact predicate ------
 @pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
 def test_parity_exact_predicate(dist):
