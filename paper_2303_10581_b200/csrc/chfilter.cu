@@ -32,6 +32,9 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef CH_K1_MINB_F
+#define CH_K1_MINB_F 3 // K1 CTAs per SM for float32 storage
+#endif
 #ifndef CH_K2_NP_D
 #define CH_K2_NP_D 8 // K2 points per consumer thread per sub-tile, float64 storage
 #endif
@@ -57,12 +60,14 @@ template <typename T> struct PtTraits;
 template <> struct PtTraits<double> {
     using V2 = double2;
     static constexpr int K1_UNROLL = 4; // wide loads (2 points each) per thread per chunk
+    static constexpr int K1_MINB = 3;   // K1 CTAs per SM the registers are sized for
     static constexpr int K2_NP = CH_K2_NP_D;     // points per consumer thread per sub-tile
     static constexpr int K2_STAGES = CH_K2_STAGES; // TMA ring depth (sub-tiles)
 };
 template <> struct PtTraits<float> {
     using V2 = float2;
     static constexpr int K1_UNROLL = 8;
+    static constexpr int K1_MINB = CH_K1_MINB_F;
     static constexpr int K2_NP = CH_K2_NP_F;
     static constexpr int K2_STAGES = CH_K2_STAGES;
 };
@@ -481,7 +486,7 @@ __device__ void k1_finalize(const T *__restrict__ xy, long long index_base, int 
 }
 
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(K1_THREADS, 3)
+__global__ void __launch_bounds__(K1_THREADS, PtTraits<T>::K1_MINB)
 k1_extremes8(const T *__restrict__ xy, long long n, long long index_base, int flags,
              WsHeader *hdr, Partial *parts, void *ext_out, const PeerPush pp)
 {
@@ -1653,7 +1658,8 @@ ch_status cuda_check(const char *what)
 
 struct DevInfo {
     int sms = 0;
-    int k1_per_sm = 0;  // same for every instantiation (launch bounds 256 x 4)
+    int k1_per_sm = 0;   // float64 storage
+    int k1_per_sm_f = 0; // float32 storage
     int k2_per_sm_d = 0; // double points
     int k2_per_sm_f = 0; // float points
 };
@@ -1667,8 +1673,9 @@ DevInfo dev_info()
     if (dev != cached_dev) {
         cudaDeviceGetAttribute(&info.sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k1_per_sm, k1_extremes8<double, true>, K1_THREADS, 0);
-        if (info.k1_per_sm < 1)
-            info.k1_per_sm = 1;
+        info.k1_per_sm = std::max(1, info.k1_per_sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k1_per_sm_f, k1_extremes8<float, true>, K1_THREADS, 0);
+        info.k1_per_sm_f = std::max(1, info.k1_per_sm_f);
         cudaFuncSetAttribute(k2_filter_compact<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)k2_dsmem<double>());
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.k2_per_sm_d, k2_filter_compact<double>, K2_THREADS,
@@ -1725,7 +1732,7 @@ ch_status launch_k1(const T *d_xy, long long n, long long index_base, int flags,
     DevInfo di = dev_info();
     constexpr long long K1_CHUNK = k1_chunk<T>();
     long long nchunks = (n + K1_CHUNK - 1) / K1_CHUNK;
-    long long g = std::min<long long>((long long)di.sms * di.k1_per_sm, nchunks);
+    long long g = std::min<long long>((long long)di.sms * (sizeof(T) == 8 ? di.k1_per_sm : di.k1_per_sm_f), nchunks);
     g = std::min<long long>(g, K1_MAX_CTAS);
     if (g < 1)
         g = 1;
