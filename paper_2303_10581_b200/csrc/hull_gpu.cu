@@ -119,28 +119,48 @@ __global__ void k_chunk_chain(Seq s, long long nchunks, I *__restrict__ pos, lon
     len[t] = top;
 }
 
-// Bridge of the chains of chunk groups L = 2pw and R = (2p+1)w.
-template <typename I>
-__global__ void k_bridge(Seq s, long long nchunks, long long w, const I *__restrict__ pos,
-                         const long long *__restrict__ len, long long *__restrict__ bi, long long *__restrict__ bj,
-                         long long *__restrict__ len_out)
+// Chain access for the merges.  Mat: the chains as stored (the chain of the
+// group starting at chunk L is pos[L HG_CHUNK ...]).  Merged: the chains of
+// the groups one merge level up, not materialised: group L (2w chunks) is
+// A[0..i] ++ B[j..] of its two halves (i, j of its pair p = L / 2w).
+template <typename I> struct Mat {
+    using Idx = I;
+    const I *pos;
+    __device__ __forceinline__ I at(long long L, long long q) const { return pos[L * HG_CHUNK + q]; }
+};
+template <typename Inner> struct Merged {
+    using Idx = typename Inner::Idx;
+    Inner in;             // the chains one level down
+    const long long *bi, *bj;
+    long long w;          // chunks per half
+    int lg2w;             // log2(2 w)
+    __device__ __forceinline__ Idx at(long long L, long long q) const
+    {
+        const long long p = L >> lg2w, i = bi[p];
+        return q <= i ? in.at(L, q) : in.at(L + w, bj[p] + (q - i - 1));
+    }
+};
+
+// Bridge of the chains of groups L = 2pW and R = (2p+1)W (W chunks each).
+template <typename I, typename Acc>
+__global__ void k_bridge(Seq s, long long nchunks, long long W, const Acc acc, const long long *__restrict__ len,
+                         long long *__restrict__ bi, long long *__restrict__ bj, long long *__restrict__ len_out)
 {
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long L = 2 * p * w, R = L + w;
+    const long long L = 2 * p * W, R = L + W;
     if (L >= nchunks)
         return;
     const long long la = len[L];
     const long long lb = R < nchunks ? len[R] : 0;
     long long i = la - 1, j = 0;
     if (la > 0 && lb > 0) {
-        const I *A = pos + L * HG_CHUNK, *B = pos + R * HG_CHUNK;
         while (true) {
             bool changed = false;
-            while (i > 0 && turn(s.at(A[i - 1]), s.at(A[i]), s.at(B[j])) <= 0) {
+            while (i > 0 && turn(s.at(acc.at(L, i - 1)), s.at(acc.at(L, i)), s.at(acc.at(R, j))) <= 0) {
                 i--;
                 changed = true;
             }
-            while (j < lb - 1 && turn(s.at(A[i]), s.at(B[j]), s.at(B[j + 1])) <= 0) {
+            while (j < lb - 1 && turn(s.at(acc.at(L, i)), s.at(acc.at(R, j)), s.at(acc.at(R, j + 1))) <= 0) {
                 j++;
                 changed = true;
             }
@@ -153,21 +173,22 @@ __global__ void k_bridge(Seq s, long long nchunks, long long w, const I *__restr
     len_out[L] = (i + 1) + (lb - j);
 }
 
-// Parallel copy of every merged chain: A[0..i] then B[j..].  The group span
-// 2 w HG_CHUNK is a power of two: group and offset by shift and mask.
-template <typename I>
-__global__ void k_merge_copy(long long m_cap, long long nchunks, long long w, int span_log2,
-                             const I *__restrict__ pos_in, const long long *__restrict__ len_out,
-                             const long long *__restrict__ bi, const long long *__restrict__ bj, I *__restrict__ pos_out)
+// Parallel copy of every merged chain (groups of 2W chunks): A[0..i] then
+// B[j..], A and B read through `acc`.  The group span 2 W HG_CHUNK is a power
+// of two: group and offset by shift and mask.
+template <typename I, typename Acc>
+__global__ void k_merge_copy(long long m_cap, long long nchunks, long long W, int span_log2, const Acc acc,
+                             const long long *__restrict__ len_out, const long long *__restrict__ bi,
+                             const long long *__restrict__ bj, I *__restrict__ pos_out)
 {
     const long long mask = (1ll << span_log2) - 1;
     for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < m_cap; g += (long long)gridDim.x * blockDim.x) {
         const long long p = g >> span_log2, q = g & mask;
-        const long long L = 2 * p * w;
+        const long long L = 2 * p * W;
         if (L >= nchunks || q >= len_out[L])
             continue;
         const long long i = bi[p];
-        pos_out[g] = q <= i ? pos_in[L * HG_CHUNK + q] : pos_in[(L + w) * HG_CHUNK + bj[p] + (q - i - 1)];
+        pos_out[g] = q <= i ? acc.at(L, q) : acc.at(L + W, bj[p] + (q - i - 1));
     }
 }
 
@@ -195,6 +216,9 @@ __global__ void k_assemble(long long m, const I *__restrict__ low, const long lo
         out[g] = (long long)(g < a ? val[low[g]] : val[m - 1 - (long long)up[g - a]]);
 }
 
+// One thread per item (the bridges: not grid-stride).
+unsigned blocks_for(long long items, int threads) { return (unsigned)std::max<long long>(1, (items + threads - 1) / threads); }
+
 int grid_for(long long work, int threads)
 {
     long long b = (work + threads - 1) / threads;
@@ -208,7 +232,8 @@ int grid_for(long long work, int threads)
 // the returned device word (len_a[0] or len_b[0]).  Asynchronous.
 template <typename I>
 static I *chain_gpu(const double2 *P, long long m, int rev, I *pos_a, I *pos_b, long long *len_a, long long *len_b,
-                    long long *bi, long long *bj, const long long **d_len, cudaStream_t st)
+                    long long *bi, long long *bj, long long *bi2, long long *bj2, long long *bi3, long long *bj3,
+                    long long *len_m, long long *len_m2, const long long **d_len, cudaStream_t st)
 {
     const long long nchunks = (m + HG_CHUNK - 1) / HG_CHUNK;
     const long long m_cap = nchunks * HG_CHUNK;
@@ -216,15 +241,45 @@ static I *chain_gpu(const double2 *P, long long m, int rev, I *pos_a, I *pos_b, 
     k_chunk_chain<I><<<(unsigned)((nchunks + HG_THREADS - 1) / HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, pos_a,
                                                                                                   len_a);
     static_assert((HG_CHUNK & (HG_CHUNK - 1)) == 0, "chunk size is a power of two");
-    int span_log2 = 1;
-    while ((1ll << span_log2) < 2 * HG_CHUNK)
-        span_log2++;
-    for (long long w = 1; w < nchunks; w *= 2, span_log2++) {
-        const long long npairs = (nchunks + 2 * w - 1) / (2 * w);
-        k_bridge<I><<<(unsigned)((npairs + HG_THREADS - 1) / HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, w, pos_a,
-                                                                                                len_a, bi, bj, len_b);
-        k_merge_copy<I><<<grid_for(m_cap, 256), 256, 0, st>>>(m_cap, nchunks, w, span_log2, pos_a, len_b, bi, bj,
-                                                              pos_b);
+    int lgw = 0, lgc = 0; // log2 w, log2 HG_CHUNK
+    while ((1ll << lgc) < HG_CHUNK)
+        lgc++;
+    // Up to three merge levels per copy: each level's bridges read the chains
+    // of the level below through Merged (not materialised), then one copy
+    // materialises them -- a third of the copies of one level at a time.
+    for (long long w = 1; w < nchunks;) {
+        const long long np1 = (nchunks + 2 * w - 1) / (2 * w);
+        const Mat<I> m0{pos_a};
+        if (2 * w >= nchunks) {
+            k_bridge<I><<<blocks_for(np1, HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, w, m0, len_a, bi, bj, len_b);
+            k_merge_copy<I><<<grid_for(m_cap, 256), 256, 0, st>>>(m_cap, nchunks, w, lgw + 1 + lgc, m0, len_b, bi,
+                                                                  bj, pos_b);
+            w *= 2;
+            lgw += 1;
+        } else {
+            k_bridge<I><<<blocks_for(np1, HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, w, m0, len_a, bi, bj, len_m);
+            const Merged<Mat<I>> m1{m0, bi, bj, w, lgw + 1};
+            const long long np2 = (nchunks + 4 * w - 1) / (4 * w);
+            if (4 * w >= nchunks) {
+                k_bridge<I><<<blocks_for(np2, HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, 2 * w, m1, len_m, bi2, bj2,
+                                                                              len_b);
+                k_merge_copy<I><<<grid_for(m_cap, 256), 256, 0, st>>>(m_cap, nchunks, 2 * w, lgw + 2 + lgc, m1, len_b,
+                                                                      bi2, bj2, pos_b);
+                w *= 4;
+                lgw += 2;
+            } else {
+                k_bridge<I><<<blocks_for(np2, HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, 2 * w, m1, len_m, bi2, bj2,
+                                                                              len_m2);
+                const Merged<Merged<Mat<I>>> m2{m1, bi2, bj2, 2 * w, lgw + 2};
+                const long long np3 = (nchunks + 8 * w - 1) / (8 * w);
+                k_bridge<I><<<blocks_for(np3, HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, 4 * w, m2, len_m2, bi3, bj3,
+                                                                              len_b);
+                k_merge_copy<I><<<grid_for(m_cap, 256), 256, 0, st>>>(m_cap, nchunks, 4 * w, lgw + 3 + lgc, m2, len_b,
+                                                                      bi3, bj3, pos_b);
+                w *= 8;
+                lgw += 3;
+            }
+        }
         std::swap(pos_a, pos_b);
         std::swap(len_a, len_b);
     }
@@ -236,6 +291,7 @@ static I *chain_gpu(const double2 *P, long long m, int rev, I *pos_a, I *pos_b, 
 struct HullTmp {
     size_t sort_tmp = 0, total = 0;
     size_t o_k0, o_k1, o_v0, o_v1, o_P, o_pa, o_pb, o_pc, o_pd, o_la, o_lb, o_lc, o_ld, o_bi, o_bj, o_out;
+    size_t o_bi2, o_bj2, o_lm, o_bi3, o_bj3, o_lm2;
     explicit HullTmp(long long m)
     {
         if (m < 1)
@@ -255,6 +311,8 @@ struct HullTmp {
         o_la = take(nchunks * 8 + 8); o_lb = take(nchunks * 8 + 8);
         o_lc = take(nchunks * 8 + 8); o_ld = take(nchunks * 8 + 8);
         o_bi = take(nchunks * 8 + 8); o_bj = take(nchunks * 8 + 8);
+        o_bi2 = take(nchunks * 8 + 8); o_bj2 = take(nchunks * 8 + 8); o_lm = take(nchunks * 8 + 8);
+        o_bi3 = take(nchunks * 8 + 8); o_bj3 = take(nchunks * 8 + 8); o_lm2 = take(nchunks * 8 + 8);
         o_out = take((size_t)m * 8 + 8);
         total = p;
     }
@@ -273,6 +331,8 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
     auto *la = (long long *)(b + L.o_la), *lb = (long long *)(b + L.o_lb);
     auto *lc = (long long *)(b + L.o_lc), *ld = (long long *)(b + L.o_ld);
     auto *bi = (long long *)(b + L.o_bi), *bj = (long long *)(b + L.o_bj);
+    auto *bi2 = (long long *)(b + L.o_bi2), *bj2 = (long long *)(b + L.o_bj2), *lm = (long long *)(b + L.o_lm);
+    auto *bi3 = (long long *)(b + L.o_bi3), *bj3 = (long long *)(b + L.o_bj3), *lm2 = (long long *)(b + L.o_lm2);
 
     const int g = grid_for(m, 256);
     k_ykeys<V><<<g, 256, 0, st>>>(d_xy, surv, m, k0, v0);
@@ -293,8 +353,8 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
     auto chains = [&](auto tag) {
         using I = decltype(tag);
         const long long *d_hl, *d_hu;
-        const I *low = chain_gpu<I>(P, m, 0, (I *)pa, (I *)pb, la, lb, bi, bj, &d_hl, st);
-        const I *up = chain_gpu<I>(P, m, 1, (I *)pc, (I *)pd, lc, ld, bi, bj, &d_hu, st);
+        const I *low = chain_gpu<I>(P, m, 0, (I *)pa, (I *)pb, la, lb, bi, bj, bi2, bj2, bi3, bj3, lm, lm2, &d_hl, st);
+        const I *up = chain_gpu<I>(P, m, 1, (I *)pc, (I *)pd, lc, ld, bi, bj, bi2, bj2, bi3, bj3, lm, lm2, &d_hu, st);
         k_assemble<I, V><<<grid_for(m, 256), 256, 0, st>>>(m, low, d_hl, up, d_hu, val, d_hull, d_n_hull);
     };
     if (m < (1ll << 32))
