@@ -1764,9 +1764,14 @@ ch_status stage_octagon(const ch_octagon *h_oct, void *d_ws, cudaStream_t st, co
 }
 
 template <typename T>
+// pdl: launch with programmatic stream serialization.  Only when the kernel
+// just before K2 on the stream is our K1 or K3 (they trigger early and never
+// touch K2's claim counter, epoch or status words); a K2 right after another
+// K2 on the same workspace must see that K2's exit protocol, so by default
+// K2 is serialized normally.
 ch_status launch_k2(const T *d_xy, long long n, long long index_base, const ch_octagon *d_oct,
                     long long *d_surv, long long *d_count, void *d_ws, cudaStream_t st,
-                    const PeerPush &pp = PeerPush{})
+                    const PeerPush &pp = PeerPush{}, bool pdl = false)
 {
     DevInfo di = dev_info();
     long long resident = (long long)di.sms * (sizeof(T) == 8 ? di.k2_per_sm_d : di.k2_per_sm_f);
@@ -1787,7 +1792,7 @@ ch_status launch_k2(const T *d_xy, long long n, long long index_base, const ch_o
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, k2_filter_compact<T>, d_xy, (long long)n, (long long)index_base, d_oct,
                                              hdr_of(d_ws), status_of(d_ws), (long long *)d_surv, (long long *)d_count,
                                              (unsigned)nsuper, (int)subs, pp);
@@ -1801,7 +1806,8 @@ ch_status extremes8_impl(const T *d_xy, int64_t n, int64_t index_base, int flags
                          ch_extremes *h_ext, ch_octagon *h_oct, void *d_ws, size_t ws_bytes, void *stream);
 template <typename T>
 ch_status filter_compact_impl(const T *d_xy, int64_t n, int64_t index_base, const ch_octagon *h_oct,
-                              int64_t *d_survivors, int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
+                              int64_t *d_survivors, int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream,
+                              bool after_k1 = false);
 template <typename T>
 ch_status filter_impl(const T *d_xy, int64_t n, int flags, int64_t *d_survivors, int64_t *h_count, void *d_ws,
                       size_t ws_bytes, void *stream);
@@ -1919,7 +1925,8 @@ ch_status extremes8_impl(const T *d_xy, int64_t n, int64_t index_base, int flags
 
 template <typename T>
 ch_status filter_compact_impl(const T *d_xy, int64_t n, int64_t index_base, const ch_octagon *h_oct,
-                              int64_t *d_survivors, int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream)
+                              int64_t *d_survivors, int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream,
+                              bool after_k1)
 {
     ch_status s = check_points(d_xy, n);
     if (s != CH_OK)
@@ -1932,7 +1939,8 @@ ch_status filter_compact_impl(const T *d_xy, int64_t n, int64_t index_base, cons
     const ch_octagon *d_oct;
     if ((s = stage_octagon(h_oct, d_ws, st, &d_oct)) != CH_OK)
         return s;
-    return launch_k2(d_xy, n, index_base, d_oct, (long long *)d_survivors, (long long *)d_count, d_ws, st);
+    return launch_k2(d_xy, n, index_base, d_oct, (long long *)d_survivors, (long long *)d_count, d_ws, st,
+                     PeerPush{}, after_k1 && !h_oct);
 }
 
 // One step, asynchronous: K5 (one CTA, one launch) for small n, else K1 + K2.
@@ -1955,7 +1963,7 @@ ch_status filter_async_impl(const T *d_xy, int64_t n, int flags, int64_t *d_surv
     ch_status s = extremes8_impl(d_xy, n, 0, flags, nullptr, nullptr, nullptr, d_ws, ws_bytes, stream);
     if (s != CH_OK)
         return s;
-    return filter_compact_impl(d_xy, n, 0, nullptr, d_survivors, d_count, d_ws, ws_bytes, stream);
+    return filter_compact_impl(d_xy, n, 0, nullptr, d_survivors, d_count, d_ws, ws_bytes, stream, true);
 }
 
 template <typename T>
@@ -2179,7 +2187,7 @@ ch_status step_peer(ch_peer *p, const T *d_xy, int64_t n_local, int64_t index_ba
         return s;
     if (n_local > 0)
         return launch_k2(d_xy, n_local, index_base, &hdr_of(d_ws)->oct, (long long *)d_survivors, nullptr, d_ws, st,
-                         pp);
+                         pp, true); // K3 (peer) just before
     k_peer_push<<<1, 32, 0, st>>>(pp, 1);
     return cuda_check("k_peer_push");
 }

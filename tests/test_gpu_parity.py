@@ -733,3 +733,29 @@ def test_graph_replay_equals_oracle(dist):
                 assert c == len(want) == chf.read_result(ws).count, (dist, n, storage, rep)
                 assert np.array_equal(out[:c].cpu().numpy(), want), (dist, n, storage, rep)
             g.close()
+
+
+def test_back_to_back_k2_and_steps_same_workspace():
+    """K2 launched right after K2 on the same workspace (filter_compact twice),
+    and whole steps back to back (K2 -> K1 -> K2 with the programmatic
+    launch): every result equals the oracle -- K2's claim counter, epoch and
+    look-back words are handed from one launch to the next in stream order."""
+    for dist in ("displaced", "circle"):
+        n = 600_011
+        xy = synth.points(dist, n, seed=8, device=DEV)
+        want, _ = oracle.filter_compact(xy.cpu().numpy())
+        ws = chf.Workspace(n)
+        chf.extremes8_async(xy, ws)
+        outs = [torch.full((n,), -1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        for o in outs:
+            chf.filter_compact(xy, ws, out=o)          # K2, K2, K2
+        c = chf.read_result(ws).count
+        for o in outs:
+            assert np.array_equal(o[:c].cpu().numpy(), want), dist
+        cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+        outs = [torch.full((n,), -1, dtype=torch.int64, device=DEV) for _ in range(3)]
+        for o in outs:
+            chf.filter_async(xy, ws, o, cnt)             # K1, K2 (PDL), K1, K2, ...
+        torch.cuda.synchronize()
+        for o in outs:
+            assert np.array_equal(o[: int(cnt.item())].cpu().numpy(), want), dist
