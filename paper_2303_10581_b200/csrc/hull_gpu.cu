@@ -101,20 +101,33 @@ __global__ void k_chunk_chain(Seq s, long long nchunks, I *__restrict__ pos, lon
     const long long start = t * HG_CHUNK, end = min(start + HG_CHUNK, s.m);
     long long top = 0;
     double2 p1 = make_double2(0, 0), p2 = make_double2(0, 0); // stack[top-1], stack[top-2]
+    // One new point per step, loaded a step ahead: the next point in
+    // traversal order, which in the upper chain's (reversed) order is also
+    // the sorted predecessor P[f - 1] the duplicate test needs; in the lower
+    // chain's order the predecessor is the previous point, kept in a register.
+    const long long f0 = s.fwd(start);
+    double2 cur = s.P[f0];
+    double2 pred = (!s.rev && f0 > 0) ? s.P[f0 - 1] : make_double2(0, 0);
     for (long long r = start; r < end; r++) {
-        if (s.dup(r))
-            continue;
-        const double2 pr = s.at(r);
-        while (top >= 2 && turn(p2, p1, pr) <= 0) {
-            top--;
-            p1 = p2;
-            if (top >= 2)
-                p2 = s.at(pos[start + top - 2]);
+        const long long f = s.fwd(r);
+        const bool have_nx = s.rev ? f > 0 : r + 1 < end;
+        const double2 nx = have_nx ? s.P[s.rev ? f - 1 : f + 1] : cur;
+        const double2 pd = s.rev ? nx : pred;
+        const bool dup = f > 0 && cur.x == pd.x && cur.y == pd.y;
+        if (!dup) {
+            while (top >= 2 && turn(p2, p1, cur) <= 0) {
+                top--;
+                p1 = p2;
+                if (top >= 2)
+                    p2 = s.at(pos[start + top - 2]);
+            }
+            pos[start + top] = (I)r;
+            top++;
+            p2 = p1;
+            p1 = cur;
         }
-        pos[start + top] = (I)r;
-        top++;
-        p2 = p1;
-        p1 = pr;
+        pred = cur;
+        cur = nx;
     }
     len[t] = top;
 }
