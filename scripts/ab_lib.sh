@@ -1,5 +1,5 @@
 # A/B of two prebuilt libraries on the same box: the in-tree build ("new")
-# vs build/alt/libchfilter.so ("alt", e.g. built from an older commit by
+# vs ab_alt/libchfilter.so ("alt", e.g. built from an older commit by
 # scripts/build_alt.sh).  Runs the bench matrix for each; 1 GPU.
 B="python bench.py --no-e2e --no-cpu-baseline --steps ${STEPS:-30} --warmup 3"
 L=paper_2303_10581_b200/libchfilter.so
@@ -13,6 +13,6 @@ print(f\"$1 {d['config']['workload']:28s} {d['value']:8.2f} Gpts/s k1 {r['k1_ms'
 cp $L /tmp/new.so
 for R in ${ROUNDS:-1}; do
   cp /tmp/new.so $L; touch $L; run new
-  cp ${ALT:-build/alt/libchfilter.so} $L; touch $L; run alt
+  cp ${ALT:-ab_alt/libchfilter.so} $L; touch $L; run alt
 done
 cp /tmp/new.so $L; touch $L
