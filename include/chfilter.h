@@ -247,7 +247,7 @@ ch_status ch_graph_destroy(ch_graph *g);
  *   K2's last CTA stores the survivor count into every peer's slot[rank]
  *   (a7), read back on the host by ch_peer_counts.
  * Banks alternate with the step epoch (a rank can run at most one step ahead
- * of a peer's reads).  Waits time out after ~10 s (CH_ERR_PEER from the next
+ * of a peer's reads).  Waits time out after ~60 s (CH_ERR_PEER from the next
  * ch_read_result / ch_peer_counts) instead of hanging.
  *   ch_peer_create: allocates the buffer, writes its IPC handle (64 bytes,
  *     ch_peer_handle_bytes()) to h_handle.  ch_peer_open: takes the world

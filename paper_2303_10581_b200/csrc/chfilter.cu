@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(256) k3_combine8(const ch_extremes *__restrict
 
 // K3 of the fused exchange: acquire the W epoch flags of this rank's own
 // exchange buffer (the peers' K1s store their records there), then combine.
-// A wait longer than ~10 s sets hdr->peer_timeout (CH_ERR_PEER) and
+// A wait longer than ~60 s sets hdr->peer_timeout (CH_ERR_PEER) and
 // combines what is there rather than hanging.
 __global__ void __launch_bounds__(256) k3_combine8_peer(const PeerPush pp, int flags, WsHeader *hdr)
 {
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(256) k3_combine8_peer(const PeerPush pp, int f
         const unsigned long long *slot = pp.slot(pp.rank, tid); // own buffer, sender tid
         const unsigned long long t0 = globaltimer_ns();
         while (ld_acquire_sys(slot + PEER_REC_FLAG) != pp.epoch) {
-            if (globaltimer_ns() - t0 > 10000000000ull) {
+            if (globaltimer_ns() - t0 > 60000000000ull) {
                 s_late = 1;
                 break;
             }
@@ -2287,7 +2287,7 @@ ch_status ch_peer_counts(ch_peer *p, int64_t *h_counts, void *stream)
             all = all && buf[(size_t)r * PEER_SLOT + PEER_CNT_FLAG] == p->epoch;
         if (all)
             break;
-        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10))
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
             return fail(CH_ERR_PEER, "peer exchange timed out (a rank's count did not arrive)");
         std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
