@@ -1882,15 +1882,15 @@ ch_status ch_read_result(const void *d_ws, ch_result *h_res, void *stream)
     if (!d_ws || !h_res)
         return fail(CH_ERR_INVALID_ARG, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
+    unsigned late = 0;
     cudaMemcpyAsync(h_res, &((const WsHeader *)d_ws)->result, sizeof(ch_result), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&late, &((const WsHeader *)d_ws)->peer_timeout, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     ch_status s = cuda_check("read result");
     if (s != CH_OK)
         return s;
     if (h_res->nonfinite)
         return fail(CH_ERR_NONFINITE, "non-finite coordinate in input");
-    unsigned late = 0;
-    cudaMemcpy(&late, &((const WsHeader *)d_ws)->peer_timeout, sizeof(unsigned), cudaMemcpyDeviceToHost);
     if (late)
         return fail(CH_ERR_PEER, "peer exchange timed out (a rank's record did not arrive)");
     return CH_OK;
@@ -2281,7 +2281,8 @@ ch_status ch_peer_counts(ch_peer *p, int64_t *h_counts, void *stream)
     std::vector<unsigned long long> buf((size_t)p->world * PEER_SLOT);
     const auto t0 = std::chrono::steady_clock::now();
     while (true) {
-        cudaMemcpy(buf.data(), p->d_buf + bank, buf.size() * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpyAsync(buf.data(), p->d_buf + bank, buf.size() * 8, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+        cudaStreamSynchronize((cudaStream_t)stream);
         bool all = true;
         for (int r = 0; r < p->world; r++)
             all = all && buf[(size_t)r * PEER_SLOT + PEER_CNT_FLAG] == p->epoch;
