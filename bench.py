@@ -418,7 +418,8 @@ def run_ours(a):
     k1_bytes = bpp * n_local
     k2_bytes = bpp * n_local + 8.0 * s_local
     if graphed:
-        dom = "graph(k5_small_filter)" if small else "graph(k1_extremes8+k2_filter_compact)"
+        dom = ("graph(k5_small_filter)" if small else "graph(k6_cluster_filter)" if n_local <= 32768
+               else "graph(k1_extremes8+k2_filter_compact)")
         dom_bytes, dom_ms = k1_bytes + k2_bytes, k1_ms
     elif peer:   # one call enqueues K1, K3 and K2: the whole step is timed
         dom, dom_bytes, dom_ms = "step(k1_extremes8+k3_combine8_peer+k2_filter_compact)", k1_bytes + k2_bytes, k1_ms

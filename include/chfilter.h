@@ -208,8 +208,10 @@ ch_status ch_filter(const double *d_xy, int64_t n, int flags, int64_t *d_survivo
                     int64_t *h_count, void *d_ws, size_t ws_bytes, void *stream);
 
 /* The same step without synchronizing: the count goes to *d_count (device,
- * nullable) and to the workspace result.  For n <= 4096 (the latency-bound
- * C1 case) the whole step runs as ONE single-CTA kernel (K5); above, K1 + K2.
+ * nullable) and to the workspace result.  For n <= 4096 the whole step runs
+ * as ONE single-CTA kernel (K5); for n <= 32768 (the latency-bound C1 case)
+ * as ONE launch of an 8-CTA thread-block cluster (K6: extremes combined and
+ * the octagon shared through distributed shared memory); above, K1 + K2.
  * _f32: float32 storage. */
 ch_status ch_filter_async(const double *d_xy, int64_t n, int flags, int64_t *d_survivors,
                           int64_t *d_count, void *d_ws, size_t ws_bytes, void *stream);
@@ -310,6 +312,8 @@ ch_status ch_hull_gpu_async(const double *d_xy, int64_t n_points, const int64_t 
                             int64_t *d_hull, int64_t *d_n_hull, void *d_tmp, size_t tmp_bytes, void *stream);
 
 #define CH_HULL_HOST 4 /* flag for ch_hull_end_to_end: gather + host monotone chain */
+#define CH_NO_CLUSTER 8 /* flag for ch_filter / ch_filter_async: no single-cluster step (K6)
+                           for mid-small n; K1 + K2 instead (tests, A/B) */
 
 /* Algorithm 1 complete: ch_filter on device-resident d_xy, then
  * the exact hull of the survivors -- on the device (ch_hull_gpu, default)

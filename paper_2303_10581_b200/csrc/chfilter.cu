@@ -11,6 +11,7 @@
 //
 // Arithmetic follows DESIGN.md "Readings": binary64 RNE, explicit __d*_rn
 // intrinsics (never contracted), built with -fmad=false as well.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1602,6 +1603,184 @@ k5_small_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hdr,
     }
 }
 
+// ===================================================================== K6 ==
+// Mid-small inputs (KS_MAX_N < n <= KC_MAX_N, e.g. the C1 config): the whole
+// step in ONE launch of one 8-CTA thread-block cluster, each point read once
+// into registers.  Extremes per CTA (k1_update, shuffles), combined by CTA 0
+// through distributed shared memory; CTA 0 builds the octagon
+// (build_octagon_cta) and every CTA copies it from CTA 0's shared memory; the
+// octagon test and a stable compaction whose CTA offsets are read from the
+// other CTAs' shared memory.  Same decisions as K1 + K2 (same functions).
+constexpr int KC_CTAS = 8, KC_THREADS = 512, KC_P = 8;
+constexpr long long KC_MAX_N = (long long)KC_CTAS * KC_THREADS * KC_P;
+
+template <typename T>
+__global__ void __cluster_dims__(KC_CTAS, 1, 1) __launch_bounds__(KC_THREADS, 1)
+k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hdr, long long *__restrict__ out,
+                  long long *d_count)
+{
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    constexpr int NW = KC_THREADS / 32;
+    __shared__ double s_v[NW][8];
+    __shared__ long long s_i[NW][8];
+    __shared__ double s_pv[8];     // this CTA's partial extremes
+    __shared__ long long s_pi[8];
+    __shared__ int s_nf;
+    __shared__ ch_extremes s_e;    // CTA 0
+    __shared__ ch_octagon s_o;     // CTA 0
+    __shared__ SOct so;
+    __shared__ int s_cnt[KC_P * NW], s_pre[KC_P * NW], s_tot;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = (int)cluster.block_rank();
+    const long long base = (long long)r * KC_THREADS * KC_P;
+    // ---- the points, once, into registers; extremes walking downward ----
+    double px[KC_P], py[KC_P];
+#pragma unroll
+    for (int j = 0; j < KC_P; j++) {
+        const long long i = base + (long long)j * KC_THREADS + tid;
+        px[j] = py[j] = 0.0;
+        if (i < n)
+            ld1pt(xy, i, px[j], py[j]);
+    }
+    Best b;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        b.v[k] = chf::slot_is_max(k) ? -CH_INF : CH_INF;
+        b.i[k] = LLONG_MAX;
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int j = KC_P - 1; j >= 0; j--) {
+        const long long i = base + (long long)j * KC_THREADS + tid;
+        if (i < n)
+            k1_update(b, px[j], py[j], i, acc);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        double v = b.v[k];
+        long long id = b.i[k];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double w = __shfl_xor_sync(FULL, v, off);
+            const long long jj = __shfl_xor_sync(FULL, id, off);
+            reduce_pair(k, v, id, w, jj);
+        }
+        if (lane == 0) {
+            s_v[warp][k] = v;
+            s_i[warp][k] = id;
+        }
+    }
+    const int nf = __syncthreads_or(acc != acc);
+    if (tid < 8) {
+        const int k = tid;
+        double bv = s_v[0][k];
+        long long bi = s_i[0][k];
+        for (int w = 1; w < NW; w++)
+            reduce_pair(k, bv, bi, s_v[w][k], s_i[w][k]);
+        s_pv[k] = bv;
+        s_pi[k] = bi;
+        if (k == 0)
+            s_nf = nf;
+    }
+    cluster.sync(); // every CTA's partial is in its shared memory
+    if (r == 0) {
+        if (tid < 8) {
+            const int k = tid;
+            double bv = chf::slot_is_max(k) ? -CH_INF : CH_INF;
+            long long bi = LLONG_MAX;
+            int anynf = 0;
+            for (int q = 0; q < KC_CTAS; q++) {
+                reduce_pair(k, bv, bi, *cluster.map_shared_rank(&s_pv[k], q), *cluster.map_shared_rank(&s_pi[k], q));
+                anynf |= *cluster.map_shared_rank(&s_nf, q);
+            }
+            s_e.idx[k] = bi;
+            s_e.x[k] = (double)xy[2 * bi];
+            s_e.y[k] = (double)xy[2 * bi + 1];
+            if (k == 0)
+                s_nf = anynf;
+        }
+        __syncthreads();
+        build_octagon_cta(s_e, flags, s_o);
+        load_soct(so, &s_o);
+    }
+    cluster.sync(); // CTA 0's octagon is ready
+    if (r != 0) {   // copy CTA 0's SOct
+        const unsigned *src = (const unsigned *)cluster.map_shared_rank(&so, 0);
+        unsigned *dst = (unsigned *)&so;
+        for (int q = tid; q < (int)(sizeof(SOct) / 4); q += KC_THREADS)
+            dst[q] = src[q];
+    }
+    __syncthreads();
+    // ---- octagon test + stable compaction (groups (j, warp) of 32 points) ----
+    unsigned m[KC_P];
+#pragma unroll
+    for (int j = 0; j < KC_P; j++) {
+        const long long i = base + (long long)j * KC_THREADS + tid;
+        const bool kp = i < n && (so.degenerate || keep_point(so, px[j], py[j]));
+        m[j] = __ballot_sync(FULL, kp);
+        if (lane == 0)
+            s_cnt[j * NW + warp] = __popc(m[j]);
+    }
+    __syncthreads();
+    constexpr int GPL = KC_P * NW / 32; // scan groups per lane
+    if (warp == 0) {
+        int c[GPL], run = 0;
+#pragma unroll
+        for (int t = 0; t < GPL; t++) {
+            c[t] = s_cnt[lane * GPL + t];
+            run += c[t];
+        }
+        int inc = run;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(FULL, inc, off);
+            if (lane >= off)
+                inc += v;
+        }
+        int ex = inc - run;
+#pragma unroll
+        for (int t = 0; t < GPL; t++) {
+            s_pre[lane * GPL + t] = ex;
+            ex += c[t];
+        }
+        if (lane == 31)
+            s_tot = inc;
+    }
+    cluster.sync(); // every CTA's survivor total is known
+    long long off = 0, total = 0;
+    for (int q = 0; q < KC_CTAS; q++) {
+        const int t = *cluster.map_shared_rank(&s_tot, q);
+        off += q < r ? t : 0;
+        total += t;
+    }
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < KC_P; j++) {
+        const int pre = s_pre[j * NW + warp];
+        if ((m[j] >> lane) & 1u)
+            out[off + pre + __popc(m[j] & lt)] = base + (long long)j * KC_THREADS + tid;
+    }
+    if (r == 0) {   // publish (the same workspace fields K1 / K2 write)
+        const unsigned *src = (const unsigned *)&s_o;
+        unsigned *dst = (unsigned *)&hdr->oct;
+        for (int q = tid; q < (int)(sizeof(ch_octagon) / 4); q += KC_THREADS)
+            dst[q] = src[q];
+        const unsigned *se = (const unsigned *)&s_e;
+        unsigned *de = (unsigned *)&hdr->ext;
+        for (int q = tid; q < (int)(sizeof(ch_extremes) / 4); q += KC_THREADS)
+            de[q] = se[q];
+        if (tid == 0) {
+            hdr->result.count = total;
+            hdr->result.nonfinite = s_nf;
+            hdr->result.degenerate = s_o.degenerate;
+            if (d_count)
+                *d_count = total;
+        }
+    }
+    cluster.sync(); // no CTA leaves while another may still read its shared memory
+}
+
 // ===================================================================== K4 ==
 __global__ void __launch_bounds__(K4_THREADS)
 k4_octagon_bits(const double *__restrict__ xy, long long n, const ch_octagon *__restrict__ oct,
@@ -1959,6 +2138,18 @@ ch_status filter_async_impl(const T *d_xy, int64_t n, int flags, int64_t *d_surv
         k5_small_filter<T><<<1, KS_THREADS, 0, (cudaStream_t)stream>>>(d_xy, n, flags, hdr_of(d_ws),
                                                                        (long long *)d_survivors, (long long *)d_count);
         return cuda_check("k5_small_filter");
+    }
+    if (n <= KC_MAX_N && !(flags & CH_NO_CLUSTER)) {
+        ch_status s = check_points(d_xy, n);
+        if (s != CH_OK)
+            return s;
+        if (!d_survivors)
+            return fail(CH_ERR_INVALID_ARG, "d_survivors is NULL");
+        if ((s = check_ws(d_ws, ws_bytes, n)) != CH_OK)
+            return s;
+        k6_cluster_filter<T><<<KC_CTAS, KC_THREADS, 0, (cudaStream_t)stream>>>(
+            d_xy, n, flags, hdr_of(d_ws), (long long *)d_survivors, (long long *)d_count);
+        return cuda_check("k6_cluster_filter");
     }
     ch_status s = extremes8_impl(d_xy, n, 0, flags, nullptr, nullptr, nullptr, d_ws, ws_bytes, stream);
     if (s != CH_OK)

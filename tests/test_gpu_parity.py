@@ -688,9 +688,9 @@ def test_parity_beyond_2pow31_points_sampled():
 
 @pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
 def test_small_n_single_kernel_equals_two_kernels(dist):
-    """K5 (one CTA, n <= 4096) against K1 + K2 and the oracle, f64 and f32,
-    all predicate modes."""
-    for n in (1, 5, 1023, 1024, 1025, 4095, 4096):
+    """K5 (one CTA, n <= 4096) and K6 (one 8-CTA cluster, n <= 32768)
+    against K1 + K2 and the oracle, f64 and f32, all predicate modes."""
+    for n in (1, 5, 1023, 1024, 1025, 4095, 4096, 4097, 10_000, 16_383, 32_768, 32_769):
         for storage in ("f64", "f32"):
             xy_d = synth.points(dist, n, seed=n, device=DEV)
             if storage == "f32":
@@ -698,7 +698,7 @@ def test_small_n_single_kernel_equals_two_kernels(dist):
             xy = xy_d.double().cpu().numpy()
             for mode in (False, True, "exact"):
                 ws = chf.Workspace(n)
-                k5 = chf.filter(xy_d, ws, plain=mode).cpu().numpy()          # K5
+                k5 = chf.filter(xy_d, ws, plain=mode).cpu().numpy()          # K5 / K6
                 ws2 = chf.Workspace(n)
                 chf.extremes8_async(xy_d, ws2, plain=mode)
                 out = chf.filter_compact(xy_d, ws2)                          # K1 + K2
