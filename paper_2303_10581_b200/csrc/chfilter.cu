@@ -1626,7 +1626,7 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
     __shared__ long long s_i[NW][8];
     __shared__ double s_pv[8];     // this CTA's partial extremes
     __shared__ long long s_pi[8];
-    __shared__ int s_nf;
+    __shared__ int s_nf, s_nfall; // this CTA's / (CTA 0) the cluster's non-finite flag
     __shared__ ch_extremes s_e;    // CTA 0
     __shared__ ch_octagon s_o;     // CTA 0
     __shared__ SOct so;
@@ -1692,13 +1692,14 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
             int anynf = 0;
             for (int q = 0; q < KC_CTAS; q++) {
                 reduce_pair(k, bv, bi, *cluster.map_shared_rank(&s_pv[k], q), *cluster.map_shared_rank(&s_pi[k], q));
-                anynf |= *cluster.map_shared_rank(&s_nf, q);
+                if (k == 0)
+                    anynf |= *cluster.map_shared_rank(&s_nf, q);
             }
             s_e.idx[k] = bi;
             s_e.x[k] = (double)xy[2 * bi];
             s_e.y[k] = (double)xy[2 * bi + 1];
             if (k == 0)
-                s_nf = anynf;
+                s_nfall = anynf;
         }
         __syncthreads();
         build_octagon_cta(s_e, flags, s_o);
@@ -1772,7 +1773,7 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
             de[q] = se[q];
         if (tid == 0) {
             hdr->result.count = total;
-            hdr->result.nonfinite = s_nf;
+            hdr->result.nonfinite = s_nfall;
             hdr->result.degenerate = s_o.degenerate;
             if (d_count)
                 *d_count = total;

@@ -183,12 +183,15 @@ def test_host_octagon_argument_path():
 
 
 def test_nonfinite_detected():
-    for bad in (np.nan, np.inf, -np.inf):
-        xy = synth.points("normal", 20_000, seed=0).numpy()
-        xy[12345, 1] = bad
-        with pytest.raises(chf.CHError) as ei:
-            chf.filter(torch.tensor(xy, device=DEV))
-        assert ei.value.status == 3
+    # 20 000: K6 (the flag of CTA 1 reaches CTA 0 through shared memory);
+    # 3 000: K5; 100 000: K1 + K2
+    for n, at in ((20_000, 12_345), (3_000, 2_999), (100_000, 77_777)):
+        for bad in (np.nan, np.inf, -np.inf):
+            xy = synth.points("normal", n, seed=0).numpy()
+            xy[at, 1] = bad
+            with pytest.raises(chf.CHError) as ei:
+                chf.filter(torch.tensor(xy, device=DEV))
+            assert ei.value.status == 3, (n, bad)
     chf.filter(synth.points("normal", 1000, seed=0, device=DEV))   # workspace state recovers
 
 
