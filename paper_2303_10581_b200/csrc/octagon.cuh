@@ -190,9 +190,12 @@ CH_HD bool box_candidate(const ch_extremes &e, int t, double b[4])
     const double y0 = dmax(e.y[5], e.y[7]), y1 = dmin(e.y[1], e.y[3]);
     if (!(x0 < x1 && y0 < y1))
         return false;
-    const double shrink[BOX_CANDIDATES] = {0.0, 0x1p-40, 0x1p-24, 0x1p-12, 0x1p-6, 0x1p-3, 0x1p-2};
-    const double wx = CH_MUL(CH_SUB(x1, x0), shrink[t]);
-    const double wy = CH_MUL(CH_SUB(y1, y0), shrink[t]);
+    // shrink factors 0, 2^-40, 2^-24, 2^-12, 2^-6, 2^-3, 2^-2 (a select chain:
+    // a table indexed at run time would live in local memory on the device)
+    const double shrink = t == 0 ? 0.0 : t == 1 ? 0x1p-40 : t == 2 ? 0x1p-24 : t == 3 ? 0x1p-12
+                        : t == 4 ? 0x1p-6 : t == 5 ? 0x1p-3 : 0x1p-2;
+    const double wx = CH_MUL(CH_SUB(x1, x0), shrink);
+    const double wy = CH_MUL(CH_SUB(y1, y0), shrink);
     b[0] = CH_ADD(x0, wx);
     b[1] = CH_SUB(x1, wx);
     b[2] = CH_ADD(y0, wy);
