@@ -763,3 +763,42 @@ def test_back_to_back_k2_and_steps_same_workspace():
         torch.cuda.synchronize()
         for o in outs:
             assert np.array_equal(o[: int(cnt.item())].cpu().numpy(), want), dist
+
+
+def test_randomized_sweep_against_oracle():
+    """A seeded sweep over sizes (every path: K5, K6, K1 + K2), storages,
+    predicate modes and point-set shapes -- Gaussian, ring, integer grids with
+    heavy ties and collinear runs, a few points far out, a tiny-scale and a
+    huge-scale copy -- each compared with the oracle element by element."""
+    rng = np.random.default_rng(2026)
+    shapes = ("normal", "ring", "grid", "outliers", "tiny", "huge")
+    for case in range(48):
+        n = int(rng.choice([1, 2, 3, 7, 100, 4096, 4097, 9_999, 32_768, 32_769, 65_537, 150_001]))
+        shape = shapes[case % len(shapes)]
+        if shape == "normal":
+            xy = rng.normal(0.5, 0.3, size=(n, 2))
+        elif shape == "ring":
+            t = rng.uniform(0, 2 * np.pi, n)
+            r = rng.uniform(0.2, 0.25, n)
+            xy = np.stack([r * np.cos(t), r * np.sin(t)], 1)
+        elif shape == "grid":
+            xy = rng.integers(-5, 6, size=(n, 2)).astype(np.float64)
+        elif shape == "outliers":
+            xy = rng.normal(0, 1, size=(n, 2))
+            k = max(1, n // 1000)
+            xy[rng.integers(0, n, k)] *= 50.0
+        elif shape == "tiny":
+            xy = rng.normal(0, 1, size=(n, 2)) * 1e-30
+        else:
+            xy = rng.normal(0, 1, size=(n, 2)) * 1e30
+        storage = "f32" if case % 3 == 2 else "f64"
+        if storage == "f32":
+            xy = xy.astype(np.float32).astype(np.float64)
+        mode = (False, True, "exact")[case % 3 if shape != "huge" else 0]
+        xy_d = torch.tensor(xy, device=DEV, dtype=torch.float32 if storage == "f32" else torch.float64)
+        got = chf.filter(xy_d, plain=mode).cpu().numpy()
+        if mode == "exact":
+            want, _ = oracle.filter_compact_exact(xy)
+        else:
+            want, _ = oracle.filter_compact(xy, certified=not mode)
+        assert np.array_equal(got, want), (case, n, shape, storage, mode)
