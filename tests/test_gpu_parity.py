@@ -802,3 +802,32 @@ def test_randomized_sweep_against_oracle():
         else:
             want, _ = oracle.filter_compact(xy, certified=not mode)
         assert np.array_equal(got, want), (case, n, shape, storage, mode)
+
+
+def test_device_hull_randomized_sweep():
+    """The device hull on seeded sets with many chunk boundaries (up to
+    ~300 chunks: every merge path -- three, two and one levels per copy) and
+    hard shapes: integer grids (duplicates, collinear runs, vertical columns),
+    points on a circle (nearly all on the hull), rings, subsets of candidates.
+    Each equals the oracle's exact hull."""
+    rng = np.random.default_rng(77)
+    for case in range(24):
+        n = int(rng.choice([3, 511, 512, 513, 4_097, 30_001, 150_000]))
+        kind = case % 4
+        if kind == 0:
+            xy = rng.integers(-20, 21, size=(n, 2)).astype(np.float64)
+        elif kind == 1:
+            t = rng.uniform(0, 2 * np.pi, n)
+            xy = np.stack([np.cos(t), np.sin(t)], 1)
+        elif kind == 2:
+            t = rng.uniform(0, 2 * np.pi, n)
+            r = rng.uniform(0.9, 1.0, n)
+            xy = np.stack([r * np.cos(t), r * np.sin(t)], 1)
+        else:
+            xy = rng.normal(0, 1, size=(n, 2))
+            xy[:, 0] = np.round(xy[:, 0], 1)   # many equal x: vertical ties
+        d = torch.tensor(xy, device=DEV)
+        ids = np.sort(rng.choice(n, size=max(1, n - n // 7), replace=False)) if case % 2 else np.arange(n)
+        got = chf.hull_gpu(d, torch.tensor(ids, dtype=torch.int64, device=DEV))
+        want = oracle.hull(xy, ids)
+        assert np.array_equal(got, want), (case, n, kind)
