@@ -457,7 +457,8 @@ def _peer_worker(rank, world, port, n, dist_name, storage, steps, q):
 @pytest.mark.parametrize("world,n,dist_name,storage", [(2, 1_000_003, "displaced", "f64"),
                                                        (3, 777_777, "circle", "f32"),
                                                        (3, 2, "normal", "f64"),
-                                                       (4, 100_003, "displaced", "f64")])
+                                                       (4, 100_003, "displaced", "f64"),
+                                                       (8, 200_003, "displaced", "f64")])
 def test_peer_exchange_multirank_single_gpu(world, n, dist_name, storage):
     """The fused exchange (ch_filter_step_peer: K1 stores its extremes record
     into every peer's cudaIpc-mapped buffer, K3 acquires them, K2 stores its
