@@ -202,7 +202,8 @@ ch_status ch_filter_f32(const float *d_xy, int64_t n, int flags, int64_t *d_surv
 ch_status ch_read_result(const void *d_ws, ch_result *h_res, void *stream);
 
 /* One filter step on device-resident input: ch_extremes8 + ch_filter_compact
- * (two kernels, no host round trip in between; one kernel, K5, for n <= 4096)
+ * (two kernels, no host round trip in between; one launch -- K5, or K6 -- for
+ * n <= 32768, see ch_filter_async)
  * + ch_read_result. */
 ch_status ch_filter(const double *d_xy, int64_t n, int flags, int64_t *d_survivors,
                     int64_t *h_count, void *d_ws, size_t ws_bytes, void *stream);
@@ -220,7 +221,7 @@ ch_status ch_filter_async_f32(const float *d_xy, int64_t n, int flags, int64_t *
 
 /* The step of ch_filter_async captured once into a CUDA graph, then replayed
  * with one launch per step (Blackwell: a graph launch costs one host call
- * for the whole K1 + K2 or K5 sequence, the point of the latency-bound C1
+ * for the whole K1 + K2, K5 or K6 sequence, the point of the latency-bound C1
  * config).  Capture happens on a private stream; the arguments (pointers,
  * n, flags) are baked into the graph, so the caller keeps the buffers alive
  * and unchanged in place until ch_graph_destroy.  *out receives an opaque
