@@ -33,6 +33,9 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef CH_K1_UNROLL_F
+#define CH_K1_UNROLL_F 6 // K1 wide loads (2 points each) per thread per chunk, float32 storage (8 spills at 80 registers)
+#endif
 #ifndef CH_K1_MINB_F
 #define CH_K1_MINB_F 3 // K1 CTAs per SM for float32 storage
 #endif
@@ -67,7 +70,7 @@ template <> struct PtTraits<double> {
 };
 template <> struct PtTraits<float> {
     using V2 = float2;
-    static constexpr int K1_UNROLL = 8;
+    static constexpr int K1_UNROLL = CH_K1_UNROLL_F;
     static constexpr int K1_MINB = CH_K1_MINB_F;
     static constexpr int K2_NP = CH_K2_NP_F;
     static constexpr int K2_STAGES = CH_K2_STAGES;
