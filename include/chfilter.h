@@ -201,6 +201,12 @@ ch_status ch_filter_f32(const float *d_xy, int64_t n, int flags, int64_t *d_surv
  * CH_ERR_NONFINITE if the last pass saw a non-finite coordinate. */
 ch_status ch_read_result(const void *d_ws, ch_result *h_res, void *stream);
 
+/* Synchronize `stream` and copy the eight extremes and the octagon (Algorithm
+ * 1 line 1) that the last step on this workspace built on the
+ * device (K1's last CTA, K3, K5 or K6) to the host.  Either pointer may be
+ * NULL.  Unspecified before the first step. */
+ch_status ch_read_octagon(const void *d_ws, ch_extremes *h_ext, ch_octagon *h_oct, void *stream);
+
 /* One filter step on device-resident input: ch_extremes8 + ch_filter_compact
  * (two kernels, no host round trip in between; one launch -- K5, or K6 -- for
  * n <= 32768, see ch_filter_async)
@@ -209,7 +215,7 @@ ch_status ch_filter(const double *d_xy, int64_t n, int flags, int64_t *d_survivo
                     int64_t *h_count, void *d_ws, size_t ws_bytes, void *stream);
 
 /* The same step without synchronizing: the count goes to *d_count (device,
- * nullable) and to the workspace result.  For n <= 4096 the whole step runs
+ * nullable) and to the workspace result.  For n <= 2048 the whole step runs
  * as ONE single-CTA kernel (K5); for n <= 32768 (the latency-bound C1 case)
  * as ONE launch of an 8-CTA thread-block cluster (K6: extremes combined and
  * the octagon shared through distributed shared memory); above, K1 + K2.

@@ -165,6 +165,14 @@ def read_result(ws: Workspace, stream=None) -> Result:
     return r
 
 
+def read_octagon(ws: Workspace, stream=None):
+    """(Extremes, Octagon) the last step on `ws` built on the device."""
+    lib = _lib.load()
+    e, o = Extremes(), Octagon()
+    _lib.check(lib.ch_read_octagon(ws.ptr, ctypes.byref(e), ctypes.byref(o), _stream(stream)), "ch_read_octagon")
+    return e, o
+
+
 def filter(xy: torch.Tensor, ws: Workspace | None = None, plain: bool = False, out: torch.Tensor | None = None,
            stream=None) -> torch.Tensor:
     """One filter step (K1 + K2 + count readback): the survivor indices, in
@@ -183,7 +191,7 @@ def filter(xy: torch.Tensor, ws: Workspace | None = None, plain: bool = False, o
 
 def filter_async(xy: torch.Tensor, ws: Workspace, out: torch.Tensor, count: torch.Tensor | None = None,
                  plain: bool = False, stream=None):
-    """One filter step without synchronizing (K5 for n <= 4096, else K1 + K2);
+    """One filter step without synchronizing (K5 for n <= 2048, K6 for n <= 32768, else K1 + K2);
     the count goes to `count` (device int64[1]) and the workspace result."""
     lib = _lib.load()
     xy = _points(xy)

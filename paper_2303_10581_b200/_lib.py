@@ -66,6 +66,7 @@ SIGNATURES = {
     "ch_filter_compact_f32": (ctypes.c_int, [P, I64, I64, ctypes.POINTER(Octagon), P, P, P, SZ, P]),
     "ch_filter_f32": (ctypes.c_int, [P, I64, ctypes.c_int, P, ctypes.POINTER(I64), P, SZ, P]),
     "ch_read_result": (ctypes.c_int, [P, ctypes.POINTER(Result), P]),
+    "ch_read_octagon": (ctypes.c_int, [P, ctypes.POINTER(Extremes), ctypes.POINTER(Octagon), P]),
     "ch_filter": (ctypes.c_int, [P, I64, ctypes.c_int, P, ctypes.POINTER(I64), P, SZ, P]),
     "ch_filter_async": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, SZ, P]),
     "ch_filter_async_f32": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, SZ, P]),

@@ -369,26 +369,157 @@ __device__ __forceinline__ void reduce_pair(int k, double &v, long long &i, doub
     }
 }
 
+// The same decision as reduce_pair (chf::slot_better: better key, else --
+// equal or unordered -- the lower index), written as selects so that the
+// eight keys' chains interleave (K5, K6).
+template <int K>
+__device__ __forceinline__ void reduce_pair_sel(double &v, long long &i, double w, long long j)
+{
+    const bool gt = chf::slot_is_max(K) ? (w > v) : (w < v);
+    const bool lt = chf::slot_is_max(K) ? (w < v) : (w > v);
+    const bool take = gt | (!lt & (j < i));
+    v = take ? w : v;
+    i = take ? j : i;
+}
+__device__ __forceinline__ void best_init(Best &b)
+{
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        b.v[k] = chf::slot_is_max(k) ? -CH_INF : CH_INF;
+        b.i[k] = LLONG_MAX;
+    }
+}
+// One point into a thread's running extremes (points visited in increasing
+// index order: equal keys keep the earlier, i.e. lower, index).
+__device__ __forceinline__ void best_point(Best &b, double x, double y, long long gi)
+{
+    const double s = __dadd_rn(x, y), d = __dsub_rn(x, y);
+    reduce_pair_sel<0>(b.v[0], b.i[0], x, gi);
+    reduce_pair_sel<1>(b.v[1], b.i[1], s, gi);
+    reduce_pair_sel<2>(b.v[2], b.i[2], y, gi);
+    reduce_pair_sel<3>(b.v[3], b.i[3], d, gi);
+    reduce_pair_sel<4>(b.v[4], b.i[4], x, gi);
+    reduce_pair_sel<5>(b.v[5], b.i[5], s, gi);
+    reduce_pair_sel<6>(b.v[6], b.i[6], y, gi);
+    reduce_pair_sel<7>(b.v[7], b.i[7], d, gi);
+}
+template <int K0>
+__device__ __forceinline__ void best_merge4(Best &b, const double (&w)[4], const long long (&j)[4])
+{
+    reduce_pair_sel<K0 + 0>(b.v[K0 + 0], b.i[K0 + 0], w[0], j[0]);
+    reduce_pair_sel<K0 + 1>(b.v[K0 + 1], b.i[K0 + 1], w[1], j[1]);
+    reduce_pair_sel<K0 + 2>(b.v[K0 + 2], b.i[K0 + 2], w[2], j[2]);
+    reduce_pair_sel<K0 + 3>(b.v[K0 + 3], b.i[K0 + 3], w[3], j[3]);
+}
+template <int K0>
+__device__ __forceinline__ void best_shfl4(Best &b, int off)
+{
+    double w[4];
+    long long j[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        w[k] = __shfl_xor_sync(FULL, b.v[K0 + k], off);
+        j[k] = __shfl_xor_sync(FULL, b.i[K0 + k], off);
+    }
+    best_merge4<K0>(b, w, j);
+}
+// Butterfly over `width` lanes (a power of two), four keys' chains at a time.
+__device__ __forceinline__ void best_warp(Best &b, int width = 32)
+{
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        if (off >= width)
+            continue;
+        best_shfl4<0>(b, off);
+        best_shfl4<4>(b, off);
+    }
+}
+
+#ifdef CH_TRACE // developer build only (CH_NVCC_EXTRA=-DCH_TRACE): phase clocks of K5 / K6
+__device__ long long g_trace[32];
+#define CH_TR(k) do { if (threadIdx.x == 0 && blockIdx.x == 0) g_trace[k] = clock64(); } while (0)
+#else
+#define CH_TR(k) do { } while (0)
+#endif
+
+// chf::octagon_vertices on warp 0, lane k holding slot k: a slot is dropped
+// iff it equals the previous SLOT (numeric ==; equal to the last kept vertex
+// exactly when it equals the previous slot, == being transitive and a dropped
+// slot equal to the kept one), and consecutive kept vertices differ, so at
+// most one trailing vertex can equal the first.  Same fields as the serial
+// function.  Called by the 32 lanes of one warp.
+__device__ __forceinline__ void octagon_vertices_warp(const ch_extremes &e, int flags, ch_octagon &o /*shared*/)
+{
+    const int lane = threadIdx.x & 31;
+    const int k = lane & 7;
+    const double x = e.x[k], y = e.y[k];
+    const double xp = __shfl_sync(FULL, x, (k + 7) & 7), yp = __shfl_sync(FULL, y, (k + 7) & 7);
+    const bool keep = k == 0 || !(x == xp && y == yp);
+    const unsigned mask = __ballot_sync(FULL, keep && lane < 8);
+    const int nv0 = __popc(mask);
+    const int last = 31 - __clz(mask);
+    const double xl = __shfl_sync(FULL, x, last), yl = __shfl_sync(FULL, y, last);
+    const double x0 = __shfl_sync(FULL, x, 0), y0 = __shfl_sync(FULL, y, 0);
+    const int nv = nv0 - ((nv0 > 1 && xl == x0 && yl == y0) ? 1 : 0);
+    const int degenerate = nv < 3;
+    if (lane < 8) {
+        const int pos = __popc(mask & ((1u << k) - 1u)); // kept vertices before slot k
+        if (keep) { // (a dropped trailing vertex keeps its coordinates, index -1)
+            o.vidx[pos] = pos < nv ? e.idx[k] : -1;
+            o.vx[pos] = x;
+            o.vy[pos] = y;
+        }
+        if (k >= nv0) {
+            o.vidx[k] = -1;
+            o.vx[k] = o.vy[k] = 0.0;
+        }
+        o.ex[k] = o.ey[k] = o.thr[k] = 0.0;
+        o.f32_a[k] = o.f32_b[k] = o.f32_cin[k] = o.f32_cout[k] = 0.0f;
+        const int sv = __popc(mask & ((2u << k) - 1u)) - 1; // slot k's kept vertex
+        o.guess_edge[k] = (!degenerate && sv < nv) ? sv : 0;
+    }
+    if (lane == 0) {
+        o.nv = nv;
+        o.degenerate = degenerate;
+        o.has_box = 0;
+        o.plain = (flags & CH_PLAIN) ? 1 : 0;
+        o.exact = (!o.plain && (flags & CH_EXACT)) ? 1 : 0;
+        o.has_f32 = 0;
+        o.bbox[0] = e.x[4]; // xmin (L)
+        o.bbox[1] = e.x[0]; // xmax (R)
+        o.bbox[2] = e.y[6]; // ymin (B)
+        o.bbox[3] = e.y[2]; // ymax (T)
+        o.box[0] = CH_INF;
+        o.box[1] = -CH_INF;
+        o.box[2] = CH_INF;
+        o.box[3] = -CH_INF;
+        o.cx = __dmul_rn(0.5, __dadd_rn(o.bbox[0], o.bbox[1]));
+        o.cy = __dmul_rn(0.5, __dadd_rn(o.bbox[2], o.bbox[3]));
+    }
+}
+
 // The octagon (DESIGN R5, R4) built by a whole CTA from extremes in shared
-// memory: thread 0 assembles the vertices, one thread per edge computes
-// ex, ey, T_k and the fp32 constants, one thread per (box candidate, edge,
-// corner) validates the accept box, and thread 0 keeps the first candidate
-// valid at every corner.  Same functions, same result as the serial
+// memory: warp 0 assembles the vertices (octagon_vertices_warp), one thread
+// per edge computes ex, ey, T_k and the fp32 constants, one thread per (box
+// candidate, edge, corner) validates the accept box, and warp 0 keeps the
+// first candidate valid at every corner.  Same result as the serial
 // chf::build_octagon (the host path).  Called by every thread of the CTA.
 __device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o /*shared*/)
 {
     __shared__ int s_bad[chf::BOX_CANDIDATES];
     const int tid = threadIdx.x;
-    if (tid == 0)
-        chf::octagon_vertices(e, flags, o);
+    if (tid < 32)
+        octagon_vertices_warp(e, flags, o);
     if (tid < chf::BOX_CANDIDATES)
         s_bad[tid] = 0;
     __syncthreads();
+    CH_TR(21);
     if (o.degenerate)
         return;
     if (tid < o.nv)
         chf::octagon_edge(o, tid);
     __syncthreads();
+    CH_TR(22);
     for (int q = tid; q < chf::BOX_CANDIDATES * 32; q += blockDim.x) {
         const int t = q >> 5, k = (q >> 2) & 7, corner = q & 3;
         double b[4];
@@ -396,19 +527,20 @@ __device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o
             s_bad[t] = 1;
     }
     __syncthreads();
-    if (tid == 0) {
-        o.has_f32 = chf::f32_domain_ok(o) ? 1 : 0;
-        for (int t = 0; t < chf::BOX_CANDIDATES; t++) {
-            double b[4];
-            if (!s_bad[t] && chf::box_candidate(e, t, b)) {
-                o.box[0] = b[0];
-                o.box[1] = b[1];
-                o.box[2] = b[2];
-                o.box[3] = b[3];
-                o.has_box = 1;
-                break;
-            }
+    CH_TR(23);
+    if (tid < 32) { // the first candidate valid everywhere (lane t: candidate t)
+        double b[4];
+        const bool ok = tid < chf::BOX_CANDIDATES && !s_bad[tid] && chf::box_candidate(e, tid, b);
+        const unsigned okm = __ballot_sync(FULL, ok);
+        if (okm && tid == __ffs(okm) - 1) {
+            o.box[0] = b[0];
+            o.box[1] = b[1];
+            o.box[2] = b[2];
+            o.box[3] = b[3];
+            o.has_box = 1;
         }
+        if (tid == 0)
+            o.has_f32 = chf::f32_domain_ok(o) ? 1 : 0;
     }
     __syncthreads();
 }
@@ -458,10 +590,13 @@ __device__ void k1_finalize(const T *__restrict__ xy, long long index_base, int 
         long long bi = s_i[0][k];
         for (int w = 1; w < K1_THREADS / 32; w++)
             reduce_pair(k, bv, bi, s_v[w][k], s_i[w][k]);
+        // no finite candidate at all (every point NaN: the status will be
+        // CH_ERR_NONFINITE): keep the sentinel, read nothing
         const long long loc = bi - index_base;
+        const bool any = bi != LLONG_MAX;
         s_e.idx[k] = bi;
-        s_e.x[k] = (double)xy[2 * loc];
-        s_e.y[k] = (double)xy[2 * loc + 1];
+        s_e.x[k] = any ? (double)xy[2 * loc] : __longlong_as_double(0x7ff8000000000000LL);
+        s_e.y[k] = any ? (double)xy[2 * loc + 1] : __longlong_as_double(0x7ff8000000000000LL);
     }
     __syncthreads();
     build_octagon_cta(s_e, flags, s_o);
@@ -796,9 +931,10 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
 
 // Survivor mask for NP points of one thread (bit i = point i), bit-identical
 // to "not (forall k: D_k > T_k)" for every valid point (R4), without the
-// fp32 certificates: K2's path for caller-supplied octagons, degenerate or
-// out-of-domain ones, and the partial last sub-tile (full sub-tiles of
-// octagons built from the data take consume_cert).  Stages, each skipped
+// fp32 certificates: K5 and K6 (the small-input steps), and K2's path for
+// caller-supplied octagons, degenerate or out-of-domain ones, and the
+// partial last sub-tile (full sub-tiles of octagons built from the data take
+// consume_cert).  Stages, each skipped
 // when no lane of the warp needs it (warp-uniform branches):
 //  1. the certified accept box (4 DSETP): inside => discarded (proof at
 //     chf::box_corner_ok);
@@ -808,8 +944,9 @@ __device__ __forceinline__ bool keep_point(const SOct &s, double x, double y)
 //  3. fp64 D_k on every edge for every undecided point.
 template <typename C, int NP>
 __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], const C (&py)[NP],
-                                             unsigned valid, int &guess_mode)
+                                             unsigned valid, int &guess_mode, int np = NP)
 {
+    // np (warp-uniform): only points [0, np) can be valid; the rest are skipped
     static_assert(NP <= 32, "one mask bit per point");
     unsigned und = 0;
 #pragma unroll
@@ -830,6 +967,8 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
         // 2'. the guessed edge of the point's octant: D_g <= T_g => kept
 #pragma unroll
         for (int i = 0; i < NP; i++) {
+            if (i >= np)
+                break;
             double dx = __dsub_rn((double)px[i], s.cx), dy = __dsub_rn((double)py[i], s.cy);
             bool c = fabs(dx) >= fabs(dy);
             int oct = dy >= 0.0 ? (dx >= 0.0 ? (c ? 0 : 1) : (c ? 3 : 2))
@@ -852,6 +991,8 @@ __device__ __forceinline__ unsigned classify(const SOct &s, const C (&px)[NP], c
             const double ax = s.e[k].ax, ay = s.e[k].ay, ex = s.e[k].ex, ey = s.e[k].ey, thr = s.e[k].thr;
 #pragma unroll
             for (int i = 0; i < NP; i++) {
+                if (i >= np)
+                    break;
                 double D = chf::edge_det(ax, ay, ex, ey, (double)px[i], (double)py[i]);
                 disc &= ~((D > thr ? 0u : 1u) << i);
             }
@@ -1454,15 +1595,18 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
 // results as K1 + K2 (same functions, same order of decisions).
 constexpr int KS_THREADS = 512;
 constexpr int KS_BATCH = 8;
-constexpr long long KS_MAX_N = 4096;  // measured crossover vs K1 + K2 (profiles/r01_small_n.txt)
+#ifndef CH_KS_MAX_N
+#define CH_KS_MAX_N 2048
+#endif
+constexpr long long KS_MAX_N = CH_KS_MAX_N; // K5 / K6 crossover (profiles/r01_small_n.txt)
 
 template <typename T>
 __global__ void __launch_bounds__(KS_THREADS, 1)
 k5_small_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hdr, long long *__restrict__ out,
                 long long *d_count)
 {
-    constexpr int B = KS_BATCH;                 // points per thread per batch
-    constexpr long long BP = (long long)B * KS_THREADS;
+    constexpr int B = KS_BATCH;                 // point slots per thread
+    static_assert(KS_MAX_N <= (long long)B * KS_THREADS, "K5 holds every point in registers");
     constexpr int NW = KS_THREADS / 32;
     __shared__ double s_v[NW][8];
     __shared__ long long s_i[NW][8];
@@ -1473,121 +1617,123 @@ k5_small_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hdr,
     __shared__ ch_octagon s_o;
     __shared__ SOct so;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const long long nb = (n + BP - 1) / BP;
-    // ---- extremes: batches high -> low, points loaded first, then walked
-    //      downward (">=" ties keep the lowest index) ----
+    const int P = (int)((n + KS_THREADS - 1) / KS_THREADS); // slots in use (block-uniform)
+    CH_TR(0);
+    // ---- the points, once, into registers (point j * KS_THREADS + tid);
+    //      extremes walking upward (equal keys keep the lower index) ----
+    double px[B], py[B];
+#pragma unroll
+    for (int j = 0; j < B; j++) {
+        const long long i = (long long)j * KS_THREADS + tid;
+        px[j] = py[j] = 0.0;
+        if (j < P && i < n)
+            ld1pt(xy, i, px[j], py[j]);
+    }
     Best bst;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        bst.v[k] = chf::slot_is_max(k) ? -CH_INF : CH_INF;
-        bst.i[k] = LLONG_MAX;
-    }
+    best_init(bst);
     double acc = 0.0;
-    for (long long bi = nb - 1; bi >= 0; bi--) {
-        double px[B], py[B];
+    unsigned valid = 0;
 #pragma unroll
-        for (int j = 0; j < B; j++) {
-            const long long i = bi * BP + (long long)j * KS_THREADS + tid;
-            px[j] = py[j] = 0.0;
-            if (i < n)
-                ld1pt(xy, i, px[j], py[j]);
-        }
-#pragma unroll
-        for (int j = B - 1; j >= 0; j--) {
-            const long long i = bi * BP + (long long)j * KS_THREADS + tid;
-            if (i < n)
-                k1_update(bst, px[j], py[j], i, acc);
+    for (int j = 0; j < B; j++) {
+        if (j >= P)
+            break;
+        const long long i = (long long)j * KS_THREADS + tid;
+        if (i < n) {
+            best_point(bst, px[j], py[j], i);
+            acc = __fma_rn(px[j], 0.0, acc);
+            acc = __fma_rn(py[j], 0.0, acc);
+            valid |= 1u << j;
         }
     }
+    CH_TR(1);
+    best_warp(bst);
+    if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-        double v = bst.v[k];
-        long long id = bst.i[k];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const double w = __shfl_xor_sync(FULL, v, off);
-            const long long j = __shfl_xor_sync(FULL, id, off);
-            reduce_pair(k, v, id, w, j);
-        }
-        if (lane == 0) {
-            s_v[warp][k] = v;
-            s_i[warp][k] = id;
+        for (int k = 0; k < 8; k++) {
+            s_v[warp][k] = bst.v[k];
+            s_i[warp][k] = bst.i[k];
         }
     }
     const int nf = __syncthreads_or(acc != acc);
-    if (tid < 8) {
-        const int k = tid;
-        double bv = s_v[0][k];
-        long long bi = s_i[0][k];
-        for (int w = 1; w < NW; w++)
-            reduce_pair(k, bv, bi, s_v[w][k], s_i[w][k]);
-        s_e.idx[k] = bi;
-        s_e.x[k] = (double)xy[2 * bi];
-        s_e.y[k] = (double)xy[2 * bi + 1];
+    CH_TR(2);
+    if (warp == 0) { // the NW warp results, one per lane, in one butterfly
+        Best c;
+        best_init(c);
+        if (lane < NW) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                c.v[k] = s_v[lane][k];
+                c.i[k] = s_i[lane][k];
+            }
+        }
+        best_warp(c, NW);
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                s_e.idx[k] = c.i[k];
+                s_e.x[k] = (double)xy[2 * c.i[k]];
+                s_e.y[k] = (double)xy[2 * c.i[k] + 1];
+            }
+        }
     }
     __syncthreads();
+    CH_TR(3);
     build_octagon_cta(s_e, flags, s_o);
+    CH_TR(4);
     load_soct(so, &s_o);
     __syncthreads();
-    // ---- octagon test + stable compaction: per batch, groups (j, warp) of
-    //      32 consecutive points, block scan of their popcounts ----
-    long long base_out = 0;
-    for (long long bi = 0; bi < nb; bi++) {
-        double px[B], py[B];
+    CH_TR(5);
+    // ---- octagon test + stable compaction: groups (j, warp) of 32
+    //      consecutive points, block scan of their popcounts ----
+    int guess_mode = 0; // adaptive: see classify()
+    const unsigned keep = so.degenerate ? valid : classify<double, B>(so, px, py, valid, guess_mode, P);
+    CH_TR(6);
+    unsigned m[B];
 #pragma unroll
-        for (int j = 0; j < B; j++) {
-            const long long i = bi * BP + (long long)j * KS_THREADS + tid;
-            px[j] = py[j] = 0.0;
-            if (i < n)
-                ld1pt(xy, i, px[j], py[j]);
-        }
-        unsigned m[B];
-#pragma unroll
-        for (int j = 0; j < B; j++) {
-            const long long i = bi * BP + (long long)j * KS_THREADS + tid;
-            const bool k = i < n && (so.degenerate || keep_point(so, px[j], py[j]));
-            m[j] = __ballot_sync(FULL, k);
-            if (lane == 0)
-                s_cnt[j * NW + warp] = __popc(m[j]);
-        }
-        __syncthreads();
-        // exclusive prefix of the B * NW group counts (index order: j, warp),
-        // one warp scan: lane l owns groups [GPL*l, GPL*l + GPL)
-        if (warp == 0) {
-            int c[GPL], run = 0;
-#pragma unroll
-            for (int t = 0; t < GPL; t++) {
-                c[t] = s_cnt[lane * GPL + t];
-                run += c[t];
-            }
-            int inc = run;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int v = __shfl_up_sync(FULL, inc, off);
-                if (lane >= off)
-                    inc += v;
-            }
-            int ex = inc - run;
-#pragma unroll
-            for (int t = 0; t < GPL; t++) {
-                s_pre[lane * GPL + t] = ex;
-                ex += c[t];
-            }
-            if (lane == 31)
-                s_tot = inc;
-        }
-        __syncthreads();
-        const int tot = s_tot;
-        const unsigned lt = lanemask_lt();
-#pragma unroll
-        for (int j = 0; j < B; j++) {
-            const int pre = s_pre[j * NW + warp];
-            if ((m[j] >> lane) & 1u)
-                out[base_out + pre + __popc(m[j] & lt)] = bi * BP + (long long)j * KS_THREADS + tid;
-        }
-        base_out += tot;
-        __syncthreads();
+    for (int j = 0; j < B; j++) {
+        m[j] = __ballot_sync(FULL, (keep >> j) & 1u);
+        if (lane == 0)
+            s_cnt[j * NW + warp] = __popc(m[j]);
     }
+    __syncthreads();
+    // exclusive prefix of the B * NW group counts (index order: j, warp),
+    // one warp scan: lane l owns groups [GPL*l, GPL*l + GPL)
+    if (warp == 0) {
+        int c[GPL], run = 0;
+#pragma unroll
+        for (int t = 0; t < GPL; t++) {
+            c[t] = s_cnt[lane * GPL + t];
+            run += c[t];
+        }
+        int inc = run;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(FULL, inc, off);
+            if (lane >= off)
+                inc += v;
+        }
+        int ex = inc - run;
+#pragma unroll
+        for (int t = 0; t < GPL; t++) {
+            s_pre[lane * GPL + t] = ex;
+            ex += c[t];
+        }
+        if (lane == 31)
+            s_tot = inc;
+    }
+    __syncthreads();
+    CH_TR(7);
+    const long long base_out = s_tot;
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < B; j++) {
+        if (j >= P)
+            break;
+        const int pre = s_pre[j * NW + warp];
+        if ((m[j] >> lane) & 1u)
+            out[pre + __popc(m[j] & lt)] = (long long)j * KS_THREADS + tid;
+    }
+    CH_TR(8);
     // ---- publish (the same workspace fields K1/K2 write) ----
     const unsigned *src = (const unsigned *)&s_o;
     unsigned *dst = (unsigned *)&hdr->oct;
@@ -1609,11 +1755,13 @@ k5_small_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hdr,
 // ===================================================================== K6 ==
 // Mid-small inputs (KS_MAX_N < n <= KC_MAX_N, e.g. the C1 config): the whole
 // step in ONE launch of one 8-CTA thread-block cluster, each point read once
-// into registers.  Extremes per CTA (k1_update, shuffles), combined by CTA 0
-// through distributed shared memory; CTA 0 builds the octagon
-// (build_octagon_cta) and every CTA copies it from CTA 0's shared memory; the
-// octagon test and a stable compaction whose CTA offsets are read from the
-// other CTAs' shared memory.  Same decisions as K1 + K2 (same functions).
+// into registers.  CTA r holds points [r P T, (r + 1) P T) (T threads, P =
+// ceil(n / 8T) slots per thread, so every CTA has work).  Extremes per CTA
+// (selects, butterflies), pushed into CTA 0's shared memory; CTA 0 builds the
+// octagon (build_octagon_cta) and pushes it into every CTA's shared memory;
+// the octagon test, and a stable compaction whose per-CTA totals are pushed
+// to every CTA.  Only remote STORES cross the cluster, each followed by one
+// cluster barrier (release / acquire).  Same decisions as K1 + K2.
 constexpr int KC_CTAS = 8, KC_THREADS = 512, KC_P = 8;
 constexpr long long KC_MAX_N = (long long)KC_CTAS * KC_THREADS * KC_P;
 
@@ -1627,102 +1775,132 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
     constexpr int NW = KC_THREADS / 32;
     __shared__ double s_v[NW][8];
     __shared__ long long s_i[NW][8];
-    __shared__ double s_pv[8];     // this CTA's partial extremes
-    __shared__ long long s_pi[8];
-    __shared__ int s_nf, s_nfall; // this CTA's / (CTA 0) the cluster's non-finite flag
-    __shared__ ch_extremes s_e;    // CTA 0
-    __shared__ ch_octagon s_o;     // CTA 0
-    __shared__ SOct so;
-    __shared__ int s_cnt[KC_P * NW], s_pre[KC_P * NW], s_tot;
+    __shared__ double s_cv[KC_CTAS][8];     // CTA 0: every CTA's extremes (pushed)
+    __shared__ long long s_ci[KC_CTAS][8];
+    __shared__ int s_cnf[KC_CTAS];          // CTA 0: every CTA's non-finite flag (pushed)
+    __shared__ int s_nfall;                 // CTA 0: the cluster's
+    __shared__ ch_extremes s_e;             // CTA 0
+    __shared__ ch_octagon s_o;              // CTA 0
+    __shared__ SOct so;                     // every CTA (pushed by CTA 0)
+    __shared__ int s_cnt[KC_P * NW], s_pre[KC_P * NW];
+    __shared__ int s_tots[KC_CTAS];         // every CTA's survivor total (pushed)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r = (int)cluster.block_rank();
-    const long long base = (long long)r * KC_THREADS * KC_P;
-    // ---- the points, once, into registers; extremes walking downward ----
+    const int P = (int)((n + KC_CTAS * KC_THREADS - 1) / (KC_CTAS * KC_THREADS)); // 1..KC_P
+    const long long base = (long long)r * P * KC_THREADS;
+    // shared memory of another CTA may be written only once that CTA runs:
+    // arrive now, wait before the first remote store
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    CH_TR(10);
+    // ---- the points, once, into registers; extremes walking upward ----
     double px[KC_P], py[KC_P];
 #pragma unroll
     for (int j = 0; j < KC_P; j++) {
         const long long i = base + (long long)j * KC_THREADS + tid;
         px[j] = py[j] = 0.0;
-        if (i < n)
+        if (j < P && i < n)
             ld1pt(xy, i, px[j], py[j]);
     }
-    Best b;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        b.v[k] = chf::slot_is_max(k) ? -CH_INF : CH_INF;
-        b.i[k] = LLONG_MAX;
-    }
+    Best bst;
+    best_init(bst);
     double acc = 0.0;
+    unsigned valid = 0;
+    CH_TR(11);
 #pragma unroll
-    for (int j = KC_P - 1; j >= 0; j--) {
+    for (int j = 0; j < KC_P; j++) {
+        if (j >= P)
+            break;
         const long long i = base + (long long)j * KC_THREADS + tid;
-        if (i < n)
-            k1_update(b, px[j], py[j], i, acc);
-    }
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        double v = b.v[k];
-        long long id = b.i[k];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const double w = __shfl_xor_sync(FULL, v, off);
-            const long long jj = __shfl_xor_sync(FULL, id, off);
-            reduce_pair(k, v, id, w, jj);
+        if (i < n) {
+            best_point(bst, px[j], py[j], i);
+            acc = __fma_rn(px[j], 0.0, acc);
+            acc = __fma_rn(py[j], 0.0, acc);
+            valid |= 1u << j;
         }
-        if (lane == 0) {
-            s_v[warp][k] = v;
-            s_i[warp][k] = id;
+    }
+    best_warp(bst);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            s_v[warp][k] = bst.v[k];
+            s_i[warp][k] = bst.i[k];
         }
     }
     const int nf = __syncthreads_or(acc != acc);
-    if (tid < 8) {
-        const int k = tid;
-        double bv = s_v[0][k];
-        long long bi = s_i[0][k];
-        for (int w = 1; w < NW; w++)
-            reduce_pair(k, bv, bi, s_v[w][k], s_i[w][k]);
-        s_pv[k] = bv;
-        s_pi[k] = bi;
-        if (k == 0)
-            s_nf = nf;
-    }
-    cluster.sync(); // every CTA's partial is in its shared memory
-    if (r == 0) {
-        if (tid < 8) {
-            const int k = tid;
-            double bv = chf::slot_is_max(k) ? -CH_INF : CH_INF;
-            long long bi = LLONG_MAX;
-            int anynf = 0;
-            for (int q = 0; q < KC_CTAS; q++) {
-                reduce_pair(k, bv, bi, *cluster.map_shared_rank(&s_pv[k], q), *cluster.map_shared_rank(&s_pi[k], q));
-                if (k == 0)
-                    anynf |= *cluster.map_shared_rank(&s_nf, q);
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); // every CTA of the cluster runs
+    CH_TR(12);
+    if (warp == 0) { // this CTA's extremes -> CTA 0's shared memory
+        Best c;
+        best_init(c);
+        if (lane < NW) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                c.v[k] = s_v[lane][k];
+                c.i[k] = s_i[lane][k];
             }
-            s_e.idx[k] = bi;
-            s_e.x[k] = (double)xy[2 * bi];
-            s_e.y[k] = (double)xy[2 * bi + 1];
-            if (k == 0)
+        }
+        best_warp(c, NW);
+        if (lane == 0) {
+            double *rv = cluster.map_shared_rank(&s_cv[r][0], 0);
+            long long *ri = cluster.map_shared_rank(&s_ci[r][0], 0);
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                rv[k] = c.v[k];
+                ri[k] = c.i[k];
+            }
+            *cluster.map_shared_rank(&s_cnf[r], 0) = nf;
+        }
+    }
+    cluster.sync(); // CTA 0 holds every CTA's partial
+    CH_TR(13);
+    if (r == 0) {
+        if (warp == 0) {
+            Best c;
+            best_init(c);
+            if (lane < KC_CTAS) {
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    c.v[k] = s_cv[lane][k];
+                    c.i[k] = s_ci[lane][k];
+                }
+            }
+            best_warp(c, KC_CTAS);
+            const int anynf = __any_sync(FULL, lane < KC_CTAS && s_cnf[lane]);
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    s_e.idx[k] = c.i[k];
+                    s_e.x[k] = (double)xy[2 * c.i[k]];
+                    s_e.y[k] = (double)xy[2 * c.i[k] + 1];
+                }
                 s_nfall = anynf;
+            }
         }
         __syncthreads();
+        CH_TR(14);
         build_octagon_cta(s_e, flags, s_o);
         load_soct(so, &s_o);
+        __syncthreads();
+        CH_TR(15);
+        // push the SOct into the other CTAs' shared memory
+        constexpr int WORDS = (int)(sizeof(SOct) / 4);
+        const unsigned *src = (const unsigned *)&so;
+        for (int q = tid; q < (KC_CTAS - 1) * WORDS; q += KC_THREADS) {
+            const int dstc = 1 + q / WORDS, w = q % WORDS;
+            unsigned *dst = (unsigned *)cluster.map_shared_rank(&so, dstc);
+            dst[w] = src[w];
+        }
     }
-    cluster.sync(); // CTA 0's octagon is ready
-    if (r != 0) {   // copy CTA 0's SOct
-        const unsigned *src = (const unsigned *)cluster.map_shared_rank(&so, 0);
-        unsigned *dst = (unsigned *)&so;
-        for (int q = tid; q < (int)(sizeof(SOct) / 4); q += KC_THREADS)
-            dst[q] = src[q];
-    }
-    __syncthreads();
+    cluster.sync(); // every CTA has the octagon
+    CH_TR(16);
     // ---- octagon test + stable compaction (groups (j, warp) of 32 points) ----
+    int guess_mode = 0;
+    const unsigned keep = so.degenerate ? valid : classify<double, KC_P>(so, px, py, valid, guess_mode, P);
+    CH_TR(17);
     unsigned m[KC_P];
 #pragma unroll
     for (int j = 0; j < KC_P; j++) {
-        const long long i = base + (long long)j * KC_THREADS + tid;
-        const bool kp = i < n && (so.degenerate || keep_point(so, px[j], py[j]));
-        m[j] = __ballot_sync(FULL, kp);
+        m[j] = __ballot_sync(FULL, (keep >> j) & 1u);
         if (lane == 0)
             s_cnt[j * NW + warp] = __popc(m[j]);
     }
@@ -1748,19 +1926,25 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
             s_pre[lane * GPL + t] = ex;
             ex += c[t];
         }
-        if (lane == 31)
-            s_tot = inc;
+        const int tot = __shfl_sync(FULL, inc, 31);
+        if (lane < KC_CTAS) // this CTA's total -> every CTA
+            *cluster.map_shared_rank(&s_tots[r], lane) = tot;
     }
-    cluster.sync(); // every CTA's survivor total is known
+    cluster.sync(); // every CTA's survivor total is known everywhere (last remote access)
+    CH_TR(18);
     long long off = 0, total = 0;
+#pragma unroll
     for (int q = 0; q < KC_CTAS; q++) {
-        const int t = *cluster.map_shared_rank(&s_tot, q);
+        const int t = s_tots[q];
         off += q < r ? t : 0;
         total += t;
     }
     const unsigned lt = lanemask_lt();
+    CH_TR(19);
 #pragma unroll
     for (int j = 0; j < KC_P; j++) {
+        if (j >= P)
+            break;
         const int pre = s_pre[j * NW + warp];
         if ((m[j] >> lane) & 1u)
             out[off + pre + __popc(m[j] & lt)] = base + (long long)j * KC_THREADS + tid;
@@ -1782,7 +1966,7 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
                 *d_count = total;
         }
     }
-    cluster.sync(); // no CTA leaves while another may still read its shared memory
+    CH_TR(20);
 }
 
 // ===================================================================== K4 ==
@@ -2005,6 +2189,15 @@ extern "C" {
 
 int ch_abi_version(void) { return CH_ABI_VERSION; }
 
+#ifdef CH_TRACE
+int ch_debug_trace(long long *h, int n)
+{
+    if (n > 32)
+        n = 32;
+    return cudaMemcpyFromSymbol(h, g_trace, n * sizeof(long long)) == cudaSuccess ? n : -1;
+}
+#endif
+
 int ch_occupancy(int kernel)
 {
     const DevInfo d = dev_info();
@@ -2058,6 +2251,19 @@ ch_status ch_octagon_build(const ch_extremes *ext, int flags, ch_octagon *out)
         return fail(CH_ERR_INVALID_ARG, "NULL argument");
     chf::build_octagon(*ext, flags, *out);
     return CH_OK;
+}
+
+ch_status ch_read_octagon(const void *d_ws, ch_extremes *h_ext, ch_octagon *h_oct, void *stream)
+{
+    if (!d_ws)
+        return fail(CH_ERR_INVALID_ARG, "NULL workspace");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (h_ext)
+        cudaMemcpyAsync(h_ext, &((const WsHeader *)d_ws)->ext, sizeof(ch_extremes), cudaMemcpyDeviceToHost, st);
+    if (h_oct)
+        cudaMemcpyAsync(h_oct, &((const WsHeader *)d_ws)->oct, sizeof(ch_octagon), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return cuda_check("read octagon");
 }
 
 ch_status ch_read_result(const void *d_ws, ch_result *h_res, void *stream)

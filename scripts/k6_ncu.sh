@@ -1,0 +1,10 @@
+set -x
+mkdir -p gpurun_out/k6
+for d in normal circle; do
+ for n in 4000 10000; do
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv python scripts/k6_prof.py $d $n 10 > gpurun_out/k6/dur_${d}_${n}.csv 2>&1
+ done
+ ncu --set full --import-source on --clock-control none -k regex:k6 -s 3 -c 1 -o gpurun_out/k6/full_${d}_1e4 python scripts/k6_prof.py $d 10000 5 > /dev/null 2>&1
+done
+ncu --set full --import-source on --clock-control none -k regex:k5 -s 3 -c 1 -o gpurun_out/k6/full_k5_normal_4e3 python scripts/k6_prof.py normal 4000 5 > /dev/null 2>&1
+ls gpurun_out/k6

@@ -3,7 +3,7 @@ set -x
 cat > /tmp/san.py <<'PY'
 import sys; sys.path.insert(0, ".")
 import numpy as np, torch, oracle, synth, paper_2303_10581_b200 as chf
-for dist, n in (("displaced", 300_001), ("circle", 70_000), ("normal", 200_003), ("displaced", 5), ("circle", 10_000), ("normal", 4_100)):
+for dist, n in (("displaced", 300_001), ("circle", 70_000), ("normal", 200_003), ("displaced", 5), ("circle", 10_000), ("normal", 4_100), ("displaced", 30_000), ("normal", 1_000)):
     xy = synth.points(dist, n, seed=1, device="cuda")
     ws = chf.Workspace(n)
     s = chf.filter(xy, ws).cpu().numpy()

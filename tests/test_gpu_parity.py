@@ -63,7 +63,7 @@ def test_golden_on_gpu(ex):
 
 
 # ------------------------------------------------- sizes and distributions --
-SIZES = [1, 2, 3, 31, 511, 512, 4095, 4096, 4097, 10_000, 123_457, 1_000_003]
+SIZES = [1, 2, 3, 31, 511, 512, 2048, 2049, 4095, 4096, 4097, 10_000, 123_457, 1_000_003]
 
 
 @pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
@@ -193,6 +193,72 @@ def test_nonfinite_detected():
                 chf.filter(torch.tensor(xy, device=DEV))
             assert ei.value.status == 3, (n, bad)
     chf.filter(synth.points("normal", 1000, seed=0, device=DEV))   # workspace state recovers
+
+
+def _bits(v):
+    import struct as _st
+    if isinstance(v, float):
+        return _st.pack("<d", v)
+    if hasattr(v, "__len__"):
+        return tuple(_bits(x) for x in v)
+    return v
+
+
+def _octagon_special_inputs(rng):
+    """Point sets whose octagons exercise the assembly: coinciding slots,
+    a trailing vertex equal to the first, +-0 coordinates, nv < 3."""
+    sq = [(0.0, 0.0), (1.0, 0.0), (1.0, 1.0), (0.0, 1.0)]
+    yield "square", sq
+    yield "triangle", [(0.0, 0.0), (2.0, 0.0), (1.0, 3.0)]
+    yield "triangle_left", [(0.0, 1.0), (3.0, 0.0), (3.0, 2.0)]
+    yield "diamond", [(1.0, 0.0), (2.0, 1.0), (1.0, 2.0), (0.0, 1.0)]
+    yield "signed_zero", [(-0.0, 1.0), (0.0, -1.0), (1.0, 0.0), (-1.0, -0.0), (0.0, 0.0)]
+    yield "segment", [(0.0, 0.0), (1.0, 1.0)]
+    yield "one_point", [(0.5, 0.25)]
+    yield "horizontal", [(float(i), 3.0) for i in range(5)]
+    for t in range(6):
+        yield f"random{t}", [tuple(p) for p in rng.normal(size=(int(rng.integers(3, 12)), 2))]
+
+
+@pytest.mark.parametrize("n", [3_000, 20_000, 100_000])
+def test_device_octagon_equals_host_build(n):
+    """The octagon K5 (n = 3000), K6 (20 000) and K1's last CTA (100 000)
+    build on the device -- every field, the unused entries included -- equals
+    chf::build_octagon on the host from the same extremes, and the extremes
+    equal the oracle's.  The special points are placed first, the rest of the
+    input is drawn strictly inside their hull (or repeats them)."""
+    rng = np.random.default_rng(7)
+    for name, pts in _octagon_special_inputs(rng):
+        pts = np.array(pts, dtype=np.float64)
+        m = len(pts)
+        if m >= 3:
+            w = rng.dirichlet(np.ones(m) * 5, size=n - m)   # convex combinations: inside the hull
+            fill = w @ pts
+        else:
+            fill = pts[rng.integers(0, m, size=n - m)]
+        xy = np.concatenate([pts, fill])
+        ws = chf.Workspace(n)
+        out = torch.empty(n, dtype=torch.int64, device=DEV)
+        chf.filter_async(torch.tensor(xy, device=DEV), ws, out)
+        e, o = chf.read_octagon(ws)
+        want_idx = oracle.extremes8(xy)
+        assert list(e.idx) == list(want_idx), name
+        h = chf.octagon_build(e)
+        for f, _ in chf.Octagon._fields_:
+            assert _bits(getattr(o, f)) == _bits(getattr(h, f)), (name, n, f, getattr(o, f), getattr(h, f))
+
+
+def test_all_nonfinite_input():
+    """Every point non-finite (no slot can hold a finite key): the status is
+    CH_ERR_NONFINITE on every path and no extreme index leaves the array."""
+    for n in (1, 3_000, 20_000, 100_000):
+        for bad in (np.nan, np.inf, -np.inf):
+            xy = np.full((n, 2), bad)
+            with pytest.raises(chf.CHError) as ei:
+                chf.filter(torch.tensor(xy, device=DEV))
+            assert ei.value.status == 3, (n, bad)
+            torch.cuda.synchronize()
+    chf.filter(synth.points("normal", 1000, seed=0, device=DEV))
 
 
 def test_determinism_and_workspace_reuse():
@@ -692,9 +758,9 @@ def test_parity_beyond_2pow31_points_sampled():
 
 @pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
 def test_small_n_single_kernel_equals_two_kernels(dist):
-    """K5 (one CTA, n <= 4096) and K6 (one 8-CTA cluster, n <= 32768)
+    """K5 (one CTA, n <= 2048) and K6 (one 8-CTA cluster, n <= 32768)
     against K1 + K2 and the oracle, f64 and f32, all predicate modes."""
-    for n in (1, 5, 1023, 1024, 1025, 4095, 4096, 4097, 10_000, 16_383, 32_768, 32_769):
+    for n in (1, 5, 1023, 1024, 1025, 2047, 2048, 2049, 4095, 4096, 4097, 10_000, 16_383, 32_768, 32_769):
         for storage in ("f64", "f32"):
             xy_d = synth.points(dist, n, seed=n, device=DEV)
             if storage == "f32":
@@ -718,7 +784,7 @@ def test_small_n_single_kernel_equals_two_kernels(dist):
 @pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
 def test_graph_replay_equals_oracle(dist):
     """ch_filter_graph_create / ch_graph_launch: the captured step (K5 for
-    n <= 4096, K1 + K2 above), replayed several times, gives the oracle's
+    n <= 2048, K6 to 32768, K1 + K2 above), replayed several times, gives the oracle's
     survivors every time, f64 and f32."""
     for n in (4096, 10_000, 300_007):
         for storage in ("f64", "f32"):
