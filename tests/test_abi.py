@@ -64,6 +64,7 @@ def test_argument_validation_without_gpu():
     st = lib.ch_filter_compact(P(1 << 20), 100, 0, None, None, None, ws, nbytes, None)
     assert st == 1                                            # NULL survivors
     assert b"NULL" in lib.ch_last_error()
+    assert lib.ch_read_octagon(None, None, None, None) == 1   # NULL workspace
 
 
 @pytest.mark.parametrize("ex", load_golden(), ids=[g["name"] for g in load_golden()])
