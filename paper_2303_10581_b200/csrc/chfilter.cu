@@ -543,6 +543,7 @@ __device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o
             o.has_f32 = chf::f32_domain_ok(o) ? 1 : 0;
     }
     __syncthreads();
+    CH_TR(24);
 }
 
 template <typename T>
