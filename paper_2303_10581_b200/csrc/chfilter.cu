@@ -506,7 +506,8 @@ __device__ __forceinline__ void octagon_vertices_warp(const ch_extremes &e, int 
 // chf::build_octagon (the host path).  Called by every thread of the CTA.
 __device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o /*shared*/)
 {
-    __shared__ int s_bad[chf::BOX_CANDIDATES];
+    __shared__ int s_bad[chf::BOX_CANDIDATES], s_cand[chf::BOX_CANDIDATES];
+    __shared__ double s_box[chf::BOX_CANDIDATES][4];
     const int tid = threadIdx.x;
     if (tid < 32)
         octagon_vertices_warp(e, flags, o);
@@ -523,24 +524,31 @@ __device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o
     for (int q = tid; q < chf::BOX_CANDIDATES * 32; q += blockDim.x) {
         const int t = q >> 5, k = (q >> 2) & 7, corner = q & 3;
         double b[4];
-        if (k < o.nv && (!chf::box_candidate(e, t, b) || !chf::box_corner_ok(o, k, b, corner)))
+        const bool cand = chf::box_candidate(e, t, b);
+        if ((q & 31) == 0) { // one thread per candidate keeps it for the pick
+            s_cand[t] = cand;
+            s_box[t][0] = b[0];
+            s_box[t][1] = b[1];
+            s_box[t][2] = b[2];
+            s_box[t][3] = b[3];
+        }
+        if (k < o.nv && (!cand || !chf::box_corner_ok(o, k, b, corner)))
             s_bad[t] = 1;
     }
     __syncthreads();
     CH_TR(23);
     if (tid < 32) { // the first candidate valid everywhere (lane t: candidate t)
-        double b[4];
-        const bool ok = tid < chf::BOX_CANDIDATES && !s_bad[tid] && chf::box_candidate(e, tid, b);
+        const bool ok = tid < chf::BOX_CANDIDATES && s_cand[tid] && !s_bad[tid];
         const unsigned okm = __ballot_sync(FULL, ok);
         if (okm && tid == __ffs(okm) - 1) {
-            o.box[0] = b[0];
-            o.box[1] = b[1];
-            o.box[2] = b[2];
-            o.box[3] = b[3];
+            o.box[0] = s_box[tid][0];
+            o.box[1] = s_box[tid][1];
+            o.box[2] = s_box[tid][2];
+            o.box[3] = s_box[tid][3];
             o.has_box = 1;
         }
-        if (tid == 0)
-            o.has_f32 = chf::f32_domain_ok(o) ? 1 : 0;
+    } else if (tid == 32) { // (another warp: runs alongside the pick)
+        o.has_f32 = chf::f32_domain_ok(o) ? 1 : 0;
     }
     __syncthreads();
     CH_TR(24);
@@ -854,20 +862,23 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.guess[t] = o->guess_edge[t];
         s.fab[t] = make_float4(o->f32_a[t], o->f32_a[t], o->f32_b[t], o->f32_b[t]);
         s.fc[t] = make_float4(o->f32_cin[t], o->f32_cin[t], o->f32_cout[t], o->f32_cout[t]);
-    } else if (t == 8) {
-        s.box[0] = o->box[0];
-        s.box[1] = o->box[1];
-        s.box[2] = o->box[2];
-        s.box[3] = o->box[3];
-        s.boxf[0] = chf::f32_up(o->box[0]);
-        s.boxf[1] = chf::f32_down(o->box[1]);
-        s.boxf[2] = chf::f32_up(o->box[2]);
-        s.boxf[3] = chf::f32_down(o->box[3]);
-        auto dup = [](float v) { return ((unsigned long long)__float_as_uint(v) << 32) | __float_as_uint(v); };
-        s.nbx0 = dup(-s.boxf[0]);
-        s.bx1 = dup(s.boxf[1]);
-        s.nby0 = dup(-s.boxf[2]);
-        s.by1 = dup(s.boxf[3]);
+    } else if (t < 12) { // one float bound of the accept box each (threads 8..11)
+        const int j = t - 8;
+        const double bj = o->box[j];
+        const float f = (j & 1) ? chf::f32_down(bj) : chf::f32_up(bj);
+        s.box[j] = bj;
+        s.boxf[j] = f;
+        const float g = (j & 1) ? f : -f; // the x0 / y0 bounds are stored negated
+        const unsigned long long d = ((unsigned long long)__float_as_uint(g) << 32) | __float_as_uint(g);
+        if (j == 0)
+            s.nbx0 = d;
+        else if (j == 1)
+            s.bx1 = d;
+        else if (j == 2)
+            s.nby0 = d;
+        else
+            s.by1 = d;
+    } else if (t == 12) {
         s.cx = o->cx;
         s.cy = o->cy;
         s.nv = o->nv;
@@ -1595,7 +1606,7 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
 // compaction -- so no grid combine, no look-back, no second launch.  Same
 // results as K1 + K2 (same functions, same order of decisions).
 constexpr int KS_THREADS = 512;
-constexpr int KS_BATCH = 8;
+constexpr int KS_BATCH = 4;
 #ifndef CH_KS_MAX_N
 #define CH_KS_MAX_N 2048
 #endif
