@@ -517,11 +517,15 @@ __device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o
     CH_TR(21);
     if (o.degenerate)
         return;
-    if (tid < o.nv)
-        chf::octagon_edge(o, tid);
-    __syncthreads();
+    // the edges (items BOX_CANDIDATES * 32 + k) and the box validation (one
+    // item per candidate, edge and corner, recomputing its edge) side by side
     CH_TR(22);
-    for (int q = tid; q < chf::BOX_CANDIDATES * 32; q += blockDim.x) {
+    for (int q = tid; q < chf::BOX_CANDIDATES * 32 + 8; q += blockDim.x) {
+        if (q >= chf::BOX_CANDIDATES * 32) {
+            if (q - chf::BOX_CANDIDATES * 32 < o.nv)
+                chf::octagon_edge(o, q - chf::BOX_CANDIDATES * 32);
+            continue;
+        }
         const int t = q >> 5, k = (q >> 2) & 7, corner = q & 3;
         double b[4];
         const bool cand = chf::box_candidate(e, t, b);
@@ -532,7 +536,7 @@ __device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o
             s_box[t][2] = b[2];
             s_box[t][3] = b[3];
         }
-        if (k < o.nv && (!cand || !chf::box_corner_ok(o, k, b, corner)))
+        if (k < o.nv && (!cand || !chf::box_corner_ok_core(o, k, b, corner)))
             s_bad[t] = 1;
     }
     __syncthreads();

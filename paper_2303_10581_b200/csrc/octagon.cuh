@@ -96,18 +96,26 @@ CH_HD bool f32_domain_ok(const ch_octagon &o)
 
 // Edge k of an octagon whose vertices and bbox are set: ex, ey, T_k (R4)
 // and the fp32 pre-filter constants.
-CH_HD void octagon_edge(ch_octagon &o, int k)
+// ex, ey, S_k and T_k of edge k (R4), from the vertices and the bbox only.
+CH_HD void edge_core(const ch_octagon &o, int k, double &ex, double &ey, double &S, double &T)
 {
     const int k1 = (k + 1 == o.nv) ? 0 : k + 1;
     const double ax = o.vx[k], ay = o.vy[k];
-    const double ex = CH_SUB(o.vx[k1], ax);
-    const double ey = CH_SUB(o.vy[k1], ay);
-    o.ex[k] = ex;
-    o.ey[k] = ey;
+    ex = CH_SUB(o.vx[k1], ax);
+    ey = CH_SUB(o.vy[k1], ay);
     const double X = dmax(CH_SUB(o.bbox[1], ax), CH_SUB(ax, o.bbox[0]));
     const double Y = dmax(CH_SUB(o.bbox[3], ay), CH_SUB(ay, o.bbox[2]));
-    const double S = CH_ADD(CH_MUL(dabs(ex), Y), CH_MUL(dabs(ey), X));
-    const double T = o.plain ? 0.0 : CH_MUL(S, 0x1p-50); // exact power-of-two scaling
+    S = CH_ADD(CH_MUL(dabs(ex), Y), CH_MUL(dabs(ey), X));
+    T = o.plain ? 0.0 : CH_MUL(S, 0x1p-50); // exact power-of-two scaling
+}
+
+CH_HD void octagon_edge(ch_octagon &o, int k)
+{
+    const double ax = o.vx[k], ay = o.vy[k];
+    double ex, ey, S, T;
+    edge_core(o, k, ex, ey, S, T);
+    o.ex[k] = ex;
+    o.ey[k] = ey;
     o.thr[k] = T;
     // fp32 pre-filter constants (used only if f32_domain_ok)
     const double Xm = dmax(dabs(o.bbox[0]), dabs(o.bbox[1]));
@@ -209,6 +217,18 @@ CH_HD bool box_corner_ok(const ch_octagon &o, int k, const double b[4], int corn
     const double x = (corner & 1) ? b[1] : b[0];
     const double y = (corner & 2) ? b[3] : b[2];
     return edge_det(o.vx[k], o.vy[k], o.ex[k], o.ey[k], x, y) > o.thr[k];
+}
+
+// The same test with the edge recomputed (edge_core: the same operations, so
+// the same values as o.ex / o.ey / o.thr): lets the device validate the box
+// while other threads are still storing the edges.
+CH_HD bool box_corner_ok_core(const ch_octagon &o, int k, const double b[4], int corner)
+{
+    const double x = (corner & 1) ? b[1] : b[0];
+    const double y = (corner & 2) ? b[3] : b[2];
+    double ex, ey, S, T;
+    edge_core(o, k, ex, ey, S, T);
+    return edge_det(o.vx[k], o.vy[k], ex, ey, x, y) > T;
 }
 
 // Serial assembly (host, and tests): vertices, every edge, the fp32 domain
