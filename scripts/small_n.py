@@ -39,8 +39,8 @@ def main():
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     lines = ["# one filter step at small n, 1x B200, us per step (CUDA events, back-to-back, inputs resident)",
-             f"{'workload':16s} {'K5 us':>9s} {'K1+K2 us':>9s} {'graph us':>9s}  (graph: ch_graph_launch of the "
-             f"ch_filter_async step; K5 for n <= 4096, else K1 + K2)"]
+             f"{'workload':16s} {'step us':>9s} {'K1+K2 us':>9s} {'graph us':>9s}  (graph: ch_graph_launch of the "
+             f"ch_filter_async step; K5 for n <= 2048, K6 for n <= 32768, else K1 + K2)"]
     print(lines[0], flush=True)
     for dist in a.dists:
         for nf in a.sizes:
