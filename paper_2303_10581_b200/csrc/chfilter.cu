@@ -403,36 +403,80 @@ __device__ __forceinline__ void best_point(Best &b, double x, double y, long lon
     reduce_pair_sel<6>(b.v[6], b.i[6], y, gi);
     reduce_pair_sel<7>(b.v[7], b.i[7], d, gi);
 }
-template <int K0>
-__device__ __forceinline__ void best_merge4(Best &b, const double (&w)[4], const long long (&j)[4])
+// Max-oriented pairs (v, i): a min-slot key is carried negated (exact), so
+// that one merge rule serves every key -- the larger value, else (equal or
+// unordered) the lower index: chf::slot_better's decision on the original key.
+__device__ __forceinline__ void max_merge(double &v, long long &i, double w, long long j)
 {
-    reduce_pair_sel<K0 + 0>(b.v[K0 + 0], b.i[K0 + 0], w[0], j[0]);
-    reduce_pair_sel<K0 + 1>(b.v[K0 + 1], b.i[K0 + 1], w[1], j[1]);
-    reduce_pair_sel<K0 + 2>(b.v[K0 + 2], b.i[K0 + 2], w[2], j[2]);
-    reduce_pair_sel<K0 + 3>(b.v[K0 + 3], b.i[K0 + 3], w[3], j[3]);
+    const bool take = (w > v) | (!(w < v) & (j < i));
+    v = take ? w : v;
+    i = take ? j : i;
 }
-template <int K0>
-__device__ __forceinline__ void best_shfl4(Best &b, int off)
+__device__ __forceinline__ void max_xor(double &v, long long &i, int off)
 {
-    double w[4];
-    long long j[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        w[k] = __shfl_xor_sync(FULL, b.v[K0 + k], off);
-        j[k] = __shfl_xor_sync(FULL, b.i[K0 + k], off);
-    }
-    best_merge4<K0>(b, w, j);
+    const double w = __shfl_xor_sync(FULL, v, off);
+    const long long j = __shfl_xor_sync(FULL, i, off);
+    max_merge(v, i, w, j);
 }
-// Butterfly over `width` lanes (a power of two), four keys' chains at a time.
-__device__ __forceinline__ void best_warp(Best &b, int width = 32)
+// The key lane l holds after best_warp_rs: bits 4, 3, 2 of the lane.
+__device__ __forceinline__ int rs_key(int lane) { return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1); }
+// Reduce-scatter butterfly over the warp: each level a lane sends the half
+// of its keys its partner keeps (16: four keys, 8: two, 4: one), then two
+// plain levels; lane l ends with the warp's best for key rs_key(l)
+// (max-oriented).  9 merges and 36 shuffles instead of 40 and 160.
+__device__ __forceinline__ void best_warp_rs(const Best &b, double &ov, long long &oi)
 {
+    const int lane = threadIdx.x & 31;
+    double v[8];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        if (off >= width)
-            continue;
-        best_shfl4<0>(b, off);
-        best_shfl4<4>(b, off);
+    for (int k = 0; k < 8; k++)
+        v[k] = chf::slot_is_max(k) ? b.v[k] : -b.v[k];
+    const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+    double v4[4];
+    long long i4[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        v4[j] = h4 ? v[4 + j] : v[j];
+        i4[j] = h4 ? b.i[4 + j] : b.i[j];
+        const double w = __shfl_xor_sync(FULL, h4 ? v[j] : v[4 + j], 16);
+        const long long jj = __shfl_xor_sync(FULL, h4 ? b.i[j] : b.i[4 + j], 16);
+        max_merge(v4[j], i4[j], w, jj);
     }
+    double v2[2];
+    long long i2[2];
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+        v2[j] = h3 ? v4[2 + j] : v4[j];
+        i2[j] = h3 ? i4[2 + j] : i4[j];
+        const double w = __shfl_xor_sync(FULL, h3 ? v4[j] : v4[2 + j], 8);
+        const long long jj = __shfl_xor_sync(FULL, h3 ? i4[j] : i4[2 + j], 8);
+        max_merge(v2[j], i2[j], w, jj);
+    }
+    ov = h2 ? v2[1] : v2[0];
+    oi = h2 ? i2[1] : i2[0];
+    {
+        const double w = __shfl_xor_sync(FULL, h2 ? v2[0] : v2[1], 4);
+        const long long jj = __shfl_xor_sync(FULL, h2 ? i2[0] : i2[1], 4);
+        max_merge(ov, oi, w, jj);
+    }
+    max_xor(ov, oi, 2);
+    max_xor(ov, oi, 1);
+}
+// Warp 0 combines R rows of 8 max-oriented pairs (s_v[r][k], s_i[r][k]):
+// lane l takes key l & 7 of rows l >> 3, (l >> 3) + 4, ...; then two
+// butterfly levels; lanes 0..7 end with key = lane.  Called by warp 0.
+template <int R>
+__device__ __forceinline__ void rows_combine(const double (*s_v)[8], const long long (*s_i)[8], double &ov,
+                                             long long &oi)
+{
+    const int lane = threadIdx.x & 31, k = lane & 7;
+    ov = -CH_INF;
+    oi = LLONG_MAX;
+#pragma unroll
+    for (int r = lane >> 3; r < R; r += 4)
+        max_merge(ov, oi, s_v[r][k], s_i[r][k]);
+    max_xor(ov, oi, 8);
+    max_xor(ov, oi, 16);
 }
 
 #ifdef CH_TRACE // developer build only (CH_NVCC_EXTRA=-DCH_TRACE): phase clocks of K5 / K6
@@ -1662,34 +1706,25 @@ k5_small_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hdr,
         }
     }
     CH_TR(1);
-    best_warp(bst);
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            s_v[warp][k] = bst.v[k];
-            s_i[warp][k] = bst.i[k];
+    {
+        double wv;
+        long long wi;
+        best_warp_rs(bst, wv, wi);
+        if ((lane & 3) == 0) {
+            s_v[warp][rs_key(lane)] = wv;
+            s_i[warp][rs_key(lane)] = wi;
         }
     }
     const int nf = __syncthreads_or(acc != acc);
     CH_TR(2);
-    if (warp == 0) { // the NW warp results, one per lane, in one butterfly
-        Best c;
-        best_init(c);
-        if (lane < NW) {
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-                c.v[k] = s_v[lane][k];
-                c.i[k] = s_i[lane][k];
-            }
-        }
-        best_warp(c, NW);
-        if (lane == 0) {
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-                s_e.idx[k] = c.i[k];
-                s_e.x[k] = (double)xy[2 * c.i[k]];
-                s_e.y[k] = (double)xy[2 * c.i[k] + 1];
-            }
+    if (warp == 0) { // the NW warp results; lane k < 8 ends with key k
+        double cv;
+        long long ci;
+        rows_combine<NW>(s_v, s_i, cv, ci);
+        if (lane < 8) {
+            s_e.idx[lane] = ci;
+            s_e.x[lane] = (double)xy[2 * ci];
+            s_e.y[lane] = (double)xy[2 * ci + 1];
         }
     }
     __syncthreads();
@@ -1834,63 +1869,44 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
             valid |= 1u << j;
         }
     }
-    best_warp(bst);
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            s_v[warp][k] = bst.v[k];
-            s_i[warp][k] = bst.i[k];
+    {
+        double wv;
+        long long wi;
+        best_warp_rs(bst, wv, wi);
+        if ((lane & 3) == 0) {
+            s_v[warp][rs_key(lane)] = wv;
+            s_i[warp][rs_key(lane)] = wi;
         }
     }
     const int nf = __syncthreads_or(acc != acc);
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); // every CTA of the cluster runs
     CH_TR(12);
-    if (warp == 0) { // this CTA's extremes -> CTA 0's shared memory
-        Best c;
-        best_init(c);
-        if (lane < NW) {
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-                c.v[k] = s_v[lane][k];
-                c.i[k] = s_i[lane][k];
-            }
-        }
-        best_warp(c, NW);
-        if (lane == 0) {
-            double *rv = cluster.map_shared_rank(&s_cv[r][0], 0);
-            long long *ri = cluster.map_shared_rank(&s_ci[r][0], 0);
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-                rv[k] = c.v[k];
-                ri[k] = c.i[k];
-            }
-            *cluster.map_shared_rank(&s_cnf[r], 0) = nf;
+    if (warp == 0) { // this CTA's extremes (lane k < 8: key k) -> CTA 0's shared memory
+        double cv;
+        long long ci;
+        rows_combine<NW>(s_v, s_i, cv, ci);
+        if (lane < 8) {
+            *cluster.map_shared_rank(&s_cv[r][lane], 0) = cv;
+            *cluster.map_shared_rank(&s_ci[r][lane], 0) = ci;
+            if (lane == 0)
+                *cluster.map_shared_rank(&s_cnf[r], 0) = nf;
         }
     }
     cluster.sync(); // CTA 0 holds every CTA's partial
     CH_TR(13);
     if (r == 0) {
         if (warp == 0) {
-            Best c;
-            best_init(c);
-            if (lane < KC_CTAS) {
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    c.v[k] = s_cv[lane][k];
-                    c.i[k] = s_ci[lane][k];
-                }
-            }
-            best_warp(c, KC_CTAS);
+            double cv;
+            long long ci;
+            rows_combine<KC_CTAS>(s_cv, s_ci, cv, ci);
             const int anynf = __any_sync(FULL, lane < KC_CTAS && s_cnf[lane]);
-            if (lane == 0) {
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    s_e.idx[k] = c.i[k];
-                    s_e.x[k] = (double)xy[2 * c.i[k]];
-                    s_e.y[k] = (double)xy[2 * c.i[k] + 1];
-                }
-                s_nfall = anynf;
+            if (lane < 8) {
+                s_e.idx[lane] = ci;
+                s_e.x[lane] = (double)xy[2 * ci];
+                s_e.y[lane] = (double)xy[2 * ci + 1];
             }
+            if (lane == 0)
+                s_nfall = anynf;
         }
         __syncthreads();
         CH_TR(14);
