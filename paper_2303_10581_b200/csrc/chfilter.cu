@@ -1915,11 +1915,12 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
         __syncthreads();
         CH_TR(15);
         // push the SOct into the other CTAs' shared memory
-        constexpr int WORDS = (int)(sizeof(SOct) / 4);
-        const unsigned *src = (const unsigned *)&so;
+        static_assert(sizeof(SOct) % 16 == 0 && alignof(SOct) >= 16, "SOct is pushed as 16-byte words");
+        constexpr int WORDS = (int)(sizeof(SOct) / 16);
+        const uint4 *src = (const uint4 *)&so;
         for (int q = tid; q < (KC_CTAS - 1) * WORDS; q += KC_THREADS) {
             const int dstc = 1 + q / WORDS, w = q % WORDS;
-            unsigned *dst = (unsigned *)cluster.map_shared_rank(&so, dstc);
+            uint4 *dst = (uint4 *)cluster.map_shared_rank(&so, dstc);
             dst[w] = src[w];
         }
     }
