@@ -95,8 +95,14 @@ typedef struct {
  * proves D_k > thr[k]; h = fma(a, fl32(x), fma(b, fl32(y), cout)) <= -0
  * proves D_k < thr[k]; otherwise D_k is evaluated in fp64.  Valid only for
  * points inside bbox, so the kernels use it only with octagons they built
- * themselves (has_f32 is cleared on a caller-supplied octagon).  It never
- * changes a result. */
+ * themselves from the same points (has_f32 is cleared on a caller-supplied
+ * octagon; a workspace octagon is tagged with the (pointer, n, index_base) it
+ * was built from, and K2 uses its fp32 stage only on those points).  It never
+ * changes a result.
+ * A caller-supplied octagon (h_oct != NULL below) is validated on the host:
+ * nv outside [0, 8] or degenerate != (nv < 3) is CH_ERR_INVALID_ARG; its box
+ * is kept only if every corner passes every edge test (else no box is used);
+ * guess_edge entries outside [0, nv) become 0. */
 typedef struct {
     int32_t nv;
     int32_t degenerate;
@@ -256,7 +262,8 @@ ch_status ch_graph_destroy(ch_graph *g);
  *   K2's last CTA stores the survivor count into every peer's slot[rank]
  *   (a7), read back on the host by ch_peer_counts.
  * Banks alternate with the step epoch (a rank can run at most one step ahead
- * of a peer's reads).  Waits time out after ~60 s (CH_ERR_PEER from the next
+ * of a peer's reads).  Waits time out after 60 s (or $CH_PEER_TIMEOUT_MS at
+ * ch_peer_create) with CH_ERR_PEER from the next
  * ch_read_result / ch_peer_counts) instead of hanging.
  *   ch_peer_create: allocates the buffer, writes its IPC handle (64 bytes,
  *     ch_peer_handle_bytes()) to h_handle.  ch_peer_open: takes the world

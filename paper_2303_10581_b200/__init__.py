@@ -46,6 +46,22 @@ def _points(xy: torch.Tensor) -> torch.Tensor:
     return xy
 
 
+def _points64(xy: torch.Tensor, what: str) -> torch.Tensor:
+    """float64 points only: the hull and gather entry points read const double*."""
+    xy = _points(xy)
+    if xy.dtype != torch.float64:
+        raise TypeError(f"{what} takes float64 points (got {xy.dtype}); widen float32 storage with .double()")
+    return xy
+
+
+def _ids(idx: torch.Tensor, xy: torch.Tensor, what: str) -> torch.Tensor:
+    if not isinstance(idx, torch.Tensor) or idx.dtype != torch.int64 or idx.dim() != 1 or not idx.is_contiguous():
+        raise TypeError(f"{what}: indices must be a contiguous 1-D int64 tensor")
+    if idx.device != xy.device:
+        raise ValueError(f"{what}: indices must be on the points' device")
+    return idx
+
+
 def _plain(plain: bool) -> int:
     """Predicate flags: True / "plain" -> CH_PLAIN, "exact" -> CH_EXACT,
     False / "certified" -> CH_CERTIFIED (DESIGN R4, f3)."""
@@ -244,7 +260,10 @@ def filter_host(h_xy: torch.Tensor, ws: Workspace, d_staging: torch.Tensor, d_ou
 
 
 def gather_points(xy: torch.Tensor, idx: torch.Tensor, index_base: int = 0, stream=None) -> torch.Tensor:
+    """The coordinates of points idx - index_base of xy (device, [m, 2] float64)."""
     lib = _lib.load()
+    xy = _points64(xy, "gather_points")
+    idx = _ids(idx, xy, "gather_points")
     m = idx.shape[0]
     out = torch.empty(m, 2, dtype=torch.float64, device=xy.device)
     _lib.check(lib.ch_gather_points(_ptr(xy), index_base, _ptr(idx), m, _ptr(out), _stream(stream)),
@@ -268,7 +287,8 @@ def hull_gpu(xy: torch.Tensor, surv: torch.Tensor, stream=None) -> np.ndarray:
     """f1: exact strict hull of the survivors `surv` (int64 device indices
     into xy) computed on the device; returns the hull ids (host)."""
     lib = _lib.load()
-    xy = _points(xy)
+    xy = _points64(xy, "hull_gpu")
+    surv = _ids(surv, xy, "hull_gpu")
     m = int(surv.shape[0])
     tb = int(lib.ch_hull_gpu_temp_bytes(m))
     tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=xy.device)
@@ -284,7 +304,8 @@ def hull_gpu_async(xy: torch.Tensor, surv: torch.Tensor, tmp: torch.Tensor | Non
     (the ids valid up to the count).  `tmp`: uint8 device scratch of
     ch_hull_gpu_temp_bytes(len(surv)) bytes (allocated if None)."""
     lib = _lib.load()
-    xy = _points(xy)
+    xy = _points64(xy, "hull_gpu_async")
+    surv = _ids(surv, xy, "hull_gpu_async")
     m = int(surv.shape[0])
     tb = int(lib.ch_hull_gpu_temp_bytes(m))
     if tmp is None or tmp.numel() < tb:

@@ -18,6 +18,7 @@
 #include <chrono>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -114,7 +115,9 @@ struct WsHeader {
     unsigned k2_exit;
     unsigned epoch;
     unsigned peer_timeout; // K3's wait for a peer's record timed out (CH_ERR_PEER)
-    unsigned pad_[3];
+    unsigned tag_valid;    // the octagon below was built from the points (tag_xy, tag_n, tag_base)
+    unsigned pad_[2];
+    long long tag_xy, tag_n, tag_base;
     ch_result result;
     ch_extremes ext;
     ch_octagon oct;
@@ -193,6 +196,18 @@ __device__ __forceinline__ unsigned lanemask_lt()
     return m;
 }
 
+// The workspace octagon's data tag: the octagon in the header was built from
+// the points (xy, n, index_base) by K1 / K5 / K6 (or K3, from records whose
+// bbox contains that shard's).  K2 trusts the fp32 certificates (whose error
+// bound needs every point inside the octagon's bbox) only for those points.
+__device__ __forceinline__ void set_tag(WsHeader *hdr, const void *xy, long long n, long long index_base)
+{
+    hdr->tag_xy = (long long)xy;
+    hdr->tag_n = n;
+    hdr->tag_base = index_base;
+    hdr->tag_valid = 1;
+}
+
 // --------------------------------------------------- peer exchange (a4, a7) --
 // Exchange buffer of one rank: [2 banks][CH_MAX_PEERS slots][PEER_SLOT words];
 // slot s holds what rank s sent: words 0..23 its ch_extremes record, 24 the
@@ -204,6 +219,7 @@ struct PeerPush {
     unsigned long long *base[CH_MAX_PEERS]; // every rank's buffer, as mapped in this process
     int world, rank;                        // world == 0: no peer exchange
     unsigned long long epoch;               // step number (>= 1), bank = epoch & 1
+    unsigned long long timeout_ns;          // K3's wait for a record (CH_PEER_TIMEOUT_MS, default 60 s)
     __device__ __forceinline__ unsigned long long *slot(int peer, int of) const
     {
         return base[peer] + ((size_t)(epoch & 1) * CH_MAX_PEERS + of) * PEER_SLOT;
@@ -603,7 +619,7 @@ __device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o
 }
 
 template <typename T>
-__device__ void k1_finalize(const T *__restrict__ xy, long long index_base, int flags,
+__device__ void k1_finalize(const T *__restrict__ xy, long long n, long long index_base, int flags,
                             WsHeader *hdr, const Partial *parts, int nparts, void *ext_out, const PeerPush &pp)
 {
     // Called by every thread of the last CTA.
@@ -675,6 +691,8 @@ __device__ void k1_finalize(const T *__restrict__ xy, long long index_base, int 
     if (tid == 0) {
         hdr->result.nonfinite = s_nf;
         hdr->result.degenerate = s_o.degenerate;
+        hdr->peer_timeout = 0; // a new step
+        set_tag(hdr, xy, n, index_base);
         hdr->k1_ticket = 0; // ready for the next call (stream order)
     }
     if (pp.world > 0) // a4 fused: this rank's record into every peer's buffer
@@ -777,7 +795,7 @@ k1_extremes8(const T *__restrict__ xy, long long n, long long index_base, int fl
     __syncthreads();
     if (s_last) {
         __threadfence();
-        k1_finalize(xy, index_base, flags, hdr, parts, gridDim.x, ext_out, pp);
+        k1_finalize(xy, n, index_base, flags, hdr, parts, gridDim.x, ext_out, pp);
     }
 }
 
@@ -789,7 +807,10 @@ __device__ void combine_records(const ch_extremes *all, int world, int flags, Ws
 {
     __shared__ ch_extremes s_e;
     __shared__ ch_octagon s_o;
+    __shared__ double s_lb[4]; // the bbox of the octagon K1 built from this rank's shard
     const int tid = threadIdx.x;
+    if (tid < 4)
+        s_lb[tid] = hdr->oct.bbox[tid];
     if (tid < 8) {
         const int k = tid;
         double bv = chf::slot_is_max(k) ? -CH_INF : CH_INF;
@@ -814,6 +835,7 @@ __device__ void combine_records(const ch_extremes *all, int world, int flags, Ws
     }
     __syncthreads();
     build_octagon_cta(s_e, flags, s_o);
+    __syncthreads(); // s_lb read before the header is overwritten
     const unsigned *src = (const unsigned *)&s_o;
     unsigned *dst = (unsigned *)&hdr->oct;
     for (int i = tid; i < (int)(sizeof(ch_octagon) / 4); i += blockDim.x)
@@ -822,21 +844,32 @@ __device__ void combine_records(const ch_extremes *all, int world, int flags, Ws
     unsigned *de = (unsigned *)&hdr->ext;
     for (int i = tid; i < (int)(sizeof(ch_extremes) / 4); i += blockDim.x)
         de[i] = se[i];
-    if (tid == 0)
+    if (tid == 0) {
         hdr->result.degenerate = s_o.degenerate;
+        // the shard's points lie in its own bbox; the fp32 certificates stay
+        // valid for them iff that bbox lies in the combined one
+        const bool inside = s_lb[0] >= s_o.bbox[0] && s_lb[1] <= s_o.bbox[1] && s_lb[2] >= s_o.bbox[2] &&
+                            s_lb[3] <= s_o.bbox[3];
+        if (!inside)
+            hdr->tag_valid = 0;
+    }
 }
 
 __global__ void __launch_bounds__(256) k3_combine8(const ch_extremes *__restrict__ all, int world, int flags,
                                                    WsHeader *hdr)
 {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // K2's producer may start (PDL)
+    if (threadIdx.x == 0)
+        hdr->peer_timeout = 0;
     combine_records(all, world, flags, hdr);
 }
 
 // K3 of the fused exchange: acquire the W epoch flags of this rank's own
 // exchange buffer (the peers' K1s store their records there), then combine.
-// A wait longer than ~60 s sets hdr->peer_timeout (CH_ERR_PEER) and
-// combines what is there rather than hanging.
+// A wait longer than pp.timeout_ns (60 s unless CH_PEER_TIMEOUT_MS) sets
+// hdr->peer_timeout (CH_ERR_PEER) and combines the records that arrived,
+// the late ones as empty shards, rather than hanging.  Every K3 rewrites
+// peer_timeout, so a late record fails only its own step.
 __global__ void __launch_bounds__(256) k3_combine8_peer(const PeerPush pp, int flags, WsHeader *hdr)
 {
     __shared__ ch_extremes s_all[CH_MAX_PEERS];
@@ -850,19 +883,23 @@ __global__ void __launch_bounds__(256) k3_combine8_peer(const PeerPush pp, int f
         const unsigned long long *slot = pp.slot(pp.rank, tid); // own buffer, sender tid
         const unsigned long long t0 = globaltimer_ns();
         while (ld_acquire_sys(slot + PEER_REC_FLAG) != pp.epoch) {
-            if (globaltimer_ns() - t0 > 60000000000ull) {
+            if (globaltimer_ns() - t0 > pp.timeout_ns) {
                 s_late = 1;
                 break;
             }
             __nanosleep(100);
         }
         unsigned long long *dst = (unsigned long long *)&s_all[tid];
+        const bool late = ld_acquire_sys(slot + PEER_REC_FLAG) != pp.epoch;
+        // a record that did not arrive counts as an empty shard (idx -1): the
+        // octagon is then built from input points of the other shards only
+        // (still hull-safe), and the step reports CH_ERR_PEER
         for (int w = 0; w < 24; w++)
-            dst[w] = *(const volatile unsigned long long *)(slot + w);
+            dst[w] = late ? (w < 8 ? ~0ull : 0ull) : *(const volatile unsigned long long *)(slot + w);
     }
     __syncthreads();
-    if (tid == 0 && s_late)
-        hdr->peer_timeout = 1;
+    if (tid == 0)
+        hdr->peer_timeout = s_late;
     combine_records(s_all, pp.world, flags, hdr);
 }
 
@@ -897,7 +934,9 @@ struct SOct {
     int guess[8];
 };
 
-__device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict__ o)
+// f32_ok: the points being tested are the ones the octagon was built from
+// (the data tag), so the fp32 certificates' bbox assumption holds.
+__device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict__ o, bool f32_ok = true)
 {
     const int t = threadIdx.x;
     if (t < 8) {
@@ -931,7 +970,7 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.cy = o->cy;
         s.nv = o->nv;
         s.degenerate = o->degenerate;
-        s.has_f32 = o->has_f32;
+        s.has_f32 = f32_ok ? o->has_f32 : 0;
         s.exact = o->exact;
     }
 }
@@ -957,11 +996,14 @@ __device__ __forceinline__ bool edge_inside(const SOct &s, int k, int exact, dou
     const double D = __dsub_rn(l, r);
     if (!exact)
         return D > e.thr;
-    const double eb = __dmul_rn((3.0 + 16.0 * 0x1p-53) * 0x1p-53, __dadd_rn(fabs(l), fabs(r)));
-    if (D > eb)
-        return true;
-    if (-D > eb)
-        return false;
+    const double sum = __dadd_rn(fabs(l), fabs(r));
+    const double eb = __dmul_rn((3.0 + 16.0 * 0x1p-53) * 0x1p-53, sum);
+    if (sum >= 0x1p-900) { // (below: the products may have underflowed; exact_stage scales)
+        if (D > eb)
+            return true;
+        if (-D > eb)
+            return false;
+    }
     const int k1 = k + 1 < s.nv ? k + 1 : 0; // the edge's end point: the next vertex
     return exact_stage(e.ax, e.ay, s.e[k1].ax, s.e[k1].ay, x, y) > 0;
 }
@@ -1316,7 +1358,7 @@ __global__ void __launch_bounds__(K2_THREADS, CH_K2_MINB)
 k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
                   const ch_octagon *__restrict__ oct, WsHeader *hdr,
                   unsigned long long *status, long long *__restrict__ out,
-                  long long *d_count, unsigned nsuper, int subs, const PeerPush pp)
+                  long long *d_count, unsigned nsuper, int subs, long long nstatus, const PeerPush pp)
 {
     extern __shared__ __align__(128) unsigned char dsm[];
     using V2 = typename PtTraits<T>::V2;
@@ -1356,7 +1398,8 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
         // K3); everything that reads it or publishes results waits for that
         // grid here.  The producer only streams points, so it starts at once.
         asm volatile("griddepcontrol.wait;" ::: "memory");
-        load_soct(so, oct);
+        load_soct(so, oct,
+                  hdr->tag_valid && hdr->tag_xy == (long long)xy && hdr->tag_n == n && hdr->tag_base == index_base);
         bar_sync(K2_BAR_BASE + 5, K2_CTHREADS + 32); // consumers + publisher: `so` is ready
     }
 
@@ -1627,13 +1670,27 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
     }
     __syncthreads();
     // exit protocol: the last CTA to leave resets the counters, bumps the epoch
+    __shared__ int s_exit_last;
     if (tid == 0) {
         __threadfence();
-        unsigned e = atomicAdd(&hdr->k2_exit, 1u);
-        if (e == gridDim.x - 1) {
+        s_exit_last = atomicAdd(&hdr->k2_exit, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    const unsigned next_epoch = (s_epoch + 1) & ST_EPOCH_MASK;
+    if (s_exit_last && next_epoch == 0) {
+        // the epoch wraps (every 2^22 launches): clear every status word of
+        // the workspace, so that none written 2^22 launches ago can pass for
+        // one of the coming launches
+        for (long long q = tid; q < nstatus; q += K2_THREADS)
+            status[q] = 0ull;
+        __threadfence();
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (s_exit_last) {
             hdr->k2_claim = 0;
             hdr->k2_exit = 0;
-            hdr->epoch = (s_epoch + 1) & ST_EPOCH_MASK;
+            hdr->epoch = next_epoch;
             if (nsuper == 0) {
                 hdr->result.count = 0;
                 if (d_count)
@@ -1798,6 +1855,8 @@ k5_small_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hdr,
         hdr->result.count = base_out;
         hdr->result.nonfinite = nf;
         hdr->result.degenerate = s_o.degenerate;
+        hdr->peer_timeout = 0;
+        set_tag(hdr, xy, n, 0);
         if (d_count)
             *d_count = base_out;
     }
@@ -1995,6 +2054,8 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
             hdr->result.count = total;
             hdr->result.nonfinite = s_nfall;
             hdr->result.degenerate = s_o.degenerate;
+            hdr->peer_timeout = 0;
+            set_tag(hdr, xy, n, 0);
             if (d_count)
                 *d_count = total;
         }
@@ -2146,16 +2207,54 @@ ch_status launch_k1(const T *d_xy, long long n, long long index_base, int flags,
     return cuda_check("k1_extremes8");
 }
 
+// A caller-supplied octagon (ch_filter_compact / ch_octagon_filter with
+// h_oct != NULL) defines the predicate by its vertices, edges and thresholds
+// (D_k > thr[k] on every edge, R4).  The shortcuts the kernels take are
+// re-derived here, never trusted: nv must lie in [0, 8] and agree with
+// `degenerate` (else CH_ERR_INVALID_ARG); the accept box is kept only if
+// every corner passes every edge (chf::box_corner_ok, the proof at
+// octagon.cuh), else it is replaced by the empty box; guessed edges outside
+// [0, nv) become 0; the fp32 certificates are off (their bound needs the
+// points inside the octagon's bbox).
+ch_status sanitize_octagon(const ch_octagon &in, ch_octagon &o)
+{
+    o = in;
+    if (o.nv < 0 || o.nv > 8)
+        return fail(CH_ERR_INVALID_ARG, "octagon: nv outside [0, 8]");
+    if ((o.degenerate != 0) != (o.nv < 3))
+        return fail(CH_ERR_INVALID_ARG, "octagon: degenerate must be (nv < 3)");
+    o.degenerate = o.nv < 3;
+    o.plain = o.plain ? 1 : 0;
+    o.exact = (!o.plain && o.exact) ? 1 : 0;
+    o.has_f32 = 0;
+    for (int k = 0; k < 8; k++)
+        if (o.guess_edge[k] < 0 || o.guess_edge[k] >= (o.nv > 0 ? o.nv : 1))
+            o.guess_edge[k] = 0;
+    bool box_ok = o.has_box && !o.degenerate && o.box[0] <= o.box[1] && o.box[2] <= o.box[3];
+    for (int k = 0; k < o.nv && box_ok; k++)
+        for (int c = 0; c < 4 && box_ok; c++)
+            box_ok = chf::box_corner_ok(o, k, o.box, c);
+    if (!box_ok) {
+        o.has_box = 0;
+        o.box[0] = o.box[2] = CH_INF;
+        o.box[1] = o.box[3] = -CH_INF;
+    }
+    return CH_OK;
+}
+
 ch_status stage_octagon(const ch_octagon *h_oct, void *d_ws, cudaStream_t st, const ch_octagon **d_oct)
 {
     WsHeader *h = hdr_of(d_ws);
     if (h_oct) {
-        cudaMemcpyAsync(&h->oct, h_oct, sizeof(ch_octagon), cudaMemcpyHostToDevice, st);
+        ch_octagon o;
+        ch_status s = sanitize_octagon(*h_oct, o);
+        if (s != CH_OK)
+            return s;
+        // (pageable source: the copy is staged before cudaMemcpyAsync returns)
+        cudaMemcpyAsync(&h->oct, &o, sizeof(ch_octagon), cudaMemcpyHostToDevice, st);
         cudaMemsetAsync(&h->result.nonfinite, 0, sizeof(int32_t), st); // no K1 pass: nothing checked
-        // the fp32 pre-filter's error bound assumes every point lies in the
-        // octagon's bbox, which only holds for octagons built from the data
-        cudaMemsetAsync(&h->oct.has_f32, 0, sizeof(int32_t), st);
-        ch_status s = cuda_check("octagon upload");
+        cudaMemsetAsync(&h->tag_valid, 0, sizeof(unsigned), st);      // not built from the data
+        s = cuda_check("octagon upload");
         if (s != CH_OK)
             return s;
     }
@@ -2170,9 +2269,10 @@ template <typename T>
 // K2 on the same workspace must see that K2's exit protocol, so by default
 // K2 is serialized normally.
 ch_status launch_k2(const T *d_xy, long long n, long long index_base, const ch_octagon *d_oct,
-                    long long *d_surv, long long *d_count, void *d_ws, cudaStream_t st,
+                    long long *d_surv, long long *d_count, void *d_ws, size_t ws_bytes, cudaStream_t st,
                     const PeerPush &pp = PeerPush{}, bool pdl = false)
 {
+    const long long nstatus = (long long)((ws_bytes - WS_HEADER - WS_PARTIALS) / sizeof(unsigned long long));
     DevInfo di = dev_info();
     long long resident = (long long)di.sms * (sizeof(T) == 8 ? di.k2_per_sm_d : di.k2_per_sm_f);
     constexpr long long K2_SUB = k2_sub<T>();
@@ -2195,7 +2295,7 @@ ch_status launch_k2(const T *d_xy, long long n, long long index_base, const ch_o
     cfg.numAttrs = pdl ? 1 : 0;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, k2_filter_compact<T>, d_xy, (long long)n, (long long)index_base, d_oct,
                                              hdr_of(d_ws), status_of(d_ws), (long long *)d_surv, (long long *)d_count,
-                                             (unsigned)nsuper, (int)subs, pp);
+                                             (unsigned)nsuper, (int)subs, nstatus, pp);
     if (e != cudaSuccess)
         return fail(CH_ERR_CUDA, std::string("k2_filter_compact: ") + cudaGetErrorString(e));
     return cuda_check("k2_filter_compact");
@@ -2361,8 +2461,8 @@ ch_status filter_compact_impl(const T *d_xy, int64_t n, int64_t index_base, cons
     const ch_octagon *d_oct;
     if ((s = stage_octagon(h_oct, d_ws, st, &d_oct)) != CH_OK)
         return s;
-    return launch_k2(d_xy, n, index_base, d_oct, (long long *)d_survivors, (long long *)d_count, d_ws, st,
-                     PeerPush{}, after_k1 && !h_oct);
+    return launch_k2(d_xy, n, index_base, d_oct, (long long *)d_survivors, (long long *)d_count, d_ws, ws_bytes,
+                     st, PeerPush{}, after_k1 && !h_oct);
 }
 
 // One step, asynchronous: K5 (one CTA, one launch) for small n, else K1 + K2.
@@ -2587,6 +2687,7 @@ struct ch_peer {
     unsigned long long *base[CH_MAX_PEERS] = {};   // every rank's, mapped here
     bool opened[CH_MAX_PEERS] = {};
     unsigned long long epoch = 0;                  // steps issued
+    unsigned long long timeout_ms = 60000;         // waits for a peer's record / count
 };
 
 namespace {
@@ -2610,6 +2711,7 @@ ch_status step_peer(ch_peer *p, const T *d_xy, int64_t n_local, int64_t index_ba
     pp.world = p->world;
     pp.rank = p->rank;
     pp.epoch = ++p->epoch;
+    pp.timeout_ns = p->timeout_ms * 1000000ull;
     if (n_local > 0) {
         if ((s = launch_k1(d_xy, n_local, index_base, flags, nullptr, d_ws, st, pp)) != CH_OK)
             return s;
@@ -2620,8 +2722,8 @@ ch_status step_peer(ch_peer *p, const T *d_xy, int64_t n_local, int64_t index_ba
     if ((s = cuda_check("k3_combine8_peer")) != CH_OK)
         return s;
     if (n_local > 0)
-        return launch_k2(d_xy, n_local, index_base, &hdr_of(d_ws)->oct, (long long *)d_survivors, nullptr, d_ws, st,
-                         pp, true); // K3 (peer) just before
+        return launch_k2(d_xy, n_local, index_base, &hdr_of(d_ws)->oct, (long long *)d_survivors, nullptr, d_ws,
+                         ws_bytes, st, pp, true); // K3 (peer) just before
     k_peer_push<<<1, 32, 0, st>>>(pp, 1);
     return cuda_check("k_peer_push");
 }
@@ -2638,6 +2740,8 @@ ch_status ch_peer_create(int rank, int world, ch_peer **out, void *h_handle)
     ch_peer *p = new ch_peer();
     p->rank = rank;
     p->world = world;
+    if (const char *t = getenv("CH_PEER_TIMEOUT_MS")) // tests: a short timeout
+        p->timeout_ms = std::max(1ull, strtoull(t, nullptr, 10));
     if (cudaMalloc((void **)&p->d_buf, PEER_BUF_BYTES) != cudaSuccess ||
         cudaMemset(p->d_buf, 0, PEER_BUF_BYTES) != cudaSuccess) {
         delete p;
@@ -2722,7 +2826,7 @@ ch_status ch_peer_counts(ch_peer *p, int64_t *h_counts, void *stream)
             all = all && buf[(size_t)r * PEER_SLOT + PEER_CNT_FLAG] == p->epoch;
         if (all)
             break;
-        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(p->timeout_ms))
             return fail(CH_ERR_PEER, "peer exchange timed out (a rank's count did not arrive)");
         std::this_thread::sleep_for(std::chrono::microseconds(50));
     }

@@ -8,15 +8,27 @@
 // terms (two_prod via FMA), summed into a non-overlapping expansion
 // (Grow-Expansion with zero elimination); the sign is that of the largest
 // component.  Same arithmetic on host and device (explicitly rounded ops).
+//
+// Underflow: two_prod is exact only while a product stays above
+// about 2^-969, and Shewchuk's bound assumes no underflow.  So stage 1 decides
+// only when |l| + |r| >= 2^-900, and stage 2 first scales the eight exact
+// difference components by one power of two (the determinant is bilinear, so
+// its sign is unchanged) so that the largest lies in [2^479, 2^480).  Stage 2
+// is then exact whenever the nonzero components span at most 2^963, e.g. for
+// every input whose coordinates are all tiny (|x| ~ 1e-160 and below).
 #pragma once
 
 #include "octagon.cuh"
 
 #ifdef __CUDA_ARCH__
 #define CH_FMA(a, b, c) __fma_rn((a), (b), (c))
+#define CH_ILOGB(a) ilogb(a)
+#define CH_LDEXP(a, e) ldexp((a), (e))
 #else
 #include <cmath>
 #define CH_FMA(a, b, c) std::fma((a), (b), (c))
+#define CH_ILOGB(a) std::ilogb(a)
+#define CH_LDEXP(a, e) std::ldexp((a), (e))
 #endif
 
 namespace chf {
@@ -63,6 +75,17 @@ CH_HD int orient_sign_exact_stage(double ax, double ay, double bx, double by, do
     two_diff(py, ay, q1, q0);
     two_diff(by, ay, r1, r0);
     two_diff(px, ax, s1, s0);
+    // scale every component by 2^(479 - ilogb(max)): exact (a power of two,
+    // no overflow), sign-preserving (bilinear determinant)
+    const double m = dmax(dmax(dmax(dabs(p1), dabs(q1)), dmax(dabs(r1), dabs(s1))),
+                          dmax(dmax(dabs(p0), dabs(q0)), dmax(dabs(r0), dabs(s0))));
+    if (m == 0.0)
+        return 0;
+    if (m < 0x1p479) {
+        const int sh = 479 - CH_ILOGB(m);
+        p1 = CH_LDEXP(p1, sh), p0 = CH_LDEXP(p0, sh), q1 = CH_LDEXP(q1, sh), q0 = CH_LDEXP(q0, sh);
+        r1 = CH_LDEXP(r1, sh), r0 = CH_LDEXP(r0, sh), s1 = CH_LDEXP(s1, sh), s0 = CH_LDEXP(s0, sh);
+    }
     const double pa[4] = {p1, p1, p0, p0}, qa[4] = {q1, q0, q1, q0};
     const double ra[4] = {r1, r1, r0, r0}, sa[4] = {s1, s0, s1, s0};
     double h[34];
@@ -88,11 +111,14 @@ CH_HD int orient_sign(double ax, double ay, double bx, double by, double px, dou
     const double l = CH_MUL(CH_SUB(bx, ax), CH_SUB(py, ay));
     const double r = CH_MUL(CH_SUB(by, ay), CH_SUB(px, ax));
     const double det = CH_SUB(l, r);
-    const double eb = CH_MUL((3.0 + 16.0 * 0x1p-53) * 0x1p-53, CH_ADD(dabs(l), dabs(r)));
-    if (det > eb)
-        return 1;
-    if (-det > eb)
-        return -1;
+    const double sum = CH_ADD(dabs(l), dabs(r));
+    const double eb = CH_MUL((3.0 + 16.0 * 0x1p-53) * 0x1p-53, sum);
+    if (sum >= 0x1p-900) { // (below: the products may have underflowed)
+        if (det > eb)
+            return 1;
+        if (-det > eb)
+            return -1;
+    }
     return orient_sign_exact_stage(ax, ay, bx, by, px, py);
 }
 

@@ -11,85 +11,15 @@
 #include <numeric>
 #include <vector>
 
+#include "exact.cuh"
+
+// The exact orientation is exact.cuh's chf::orient_sign (the same
+// adaptive predicate the device hull and CH_EXACT use), compiled for the host.
 namespace chh {
-
-// Knuth two-sum / two-diff and an FMA-based exact product.
-static inline void two_sum(double a, double b, double &s, double &e)
+static inline int orient_sign(double ax, double ay, double bx, double by, double cx, double cy)
 {
-    s = a + b;
-    double bb = s - a;
-    e = (a - (s - bb)) + (b - bb);
+    return chf::orient_sign(ax, ay, bx, by, cx, cy);
 }
-static inline void two_diff(double a, double b, double &s, double &e)
-{
-    s = a - b;
-    double bb = a - s;
-    e = (a - (s + bb)) + (bb - b);
-}
-static inline void two_prod(double a, double b, double &p, double &e)
-{
-    p = a * b;
-    e = std::fma(a, b, -p);
-}
-
-// Add b into the non-overlapping expansion h[0..len) (increasing magnitude),
-// dropping zero components; returns the new length.
-static inline int expansion_add(double *h, int len, double b)
-{
-    double q = b;
-    int o = 0;
-    for (int i = 0; i < len; i++) {
-        double s, e;
-        two_sum(q, h[i], s, e);
-        q = s;
-        if (e != 0.0)
-            h[o++] = e;
-    }
-    if (q != 0.0 || o == 0)
-        h[o++] = q;
-    return o;
-}
-
-// sign((b - a) x (c - a)).  Stage 1: fp64 with Shewchuk's first error bound
-// (3 + 16 eps) eps (|l| + |r|).  Stage 2 (rare): the differences are split
-// exactly (two_diff), so det = (p1 + p0)(q1 + q0) - (r1 + r0)(s1 + s0) is a
-// sum of eight exact products, accumulated exactly.
-static int orient_sign(double ax, double ay, double bx, double by, double cx, double cy)
-{
-    double l = (bx - ax) * (cy - ay);
-    double r = (by - ay) * (cx - ax);
-    double det = l - r;
-    const double eps = 0x1p-53;
-    const double bound = (3.0 + 16.0 * eps) * eps;
-    double sum = std::fabs(l) + std::fabs(r);
-    if (std::fabs(det) > bound * sum)
-        return (det > 0) - (det < 0);
-    if (l == 0.0 && r == 0.0)
-        return 0;
-    double p1, p0, q1, q0, r1, r0, s1, s0;
-    two_diff(bx, ax, p1, p0);
-    two_diff(cy, ay, q1, q0);
-    two_diff(by, ay, r1, r0);
-    two_diff(cx, ax, s1, s0);
-    double h[40];
-    int len = 0;
-    const double pf[4][2] = {{p1, q1}, {p1, q0}, {p0, q1}, {p0, q0}};
-    const double nf[4][2] = {{r1, s1}, {r1, s0}, {r0, s1}, {r0, s0}};
-    for (int t = 0; t < 4; t++) {
-        double p, e;
-        two_prod(pf[t][0], pf[t][1], p, e);
-        len = expansion_add(h, len, p);
-        len = expansion_add(h, len, e);
-        two_prod(nf[t][0], nf[t][1], p, e);
-        len = expansion_add(h, len, -p);
-        len = expansion_add(h, len, -e);
-    }
-    for (int i = len - 1; i >= 0; i--)
-        if (h[i] != 0.0)
-            return (h[i] > 0) - (h[i] < 0);
-    return 0;
-}
-
 } // namespace chh
 
 extern "C" int ch_internal_orient_sign(double ax, double ay, double bx, double by, double cx, double cy)

@@ -31,6 +31,7 @@ import torch
 import torch.distributed as dist
 
 from . import Workspace, _fn, _lib, _plain, _points, _ptr, _stream, combine8, extremes8_async, filter_compact
+from ._lib import CHError
 
 EXT_WORDS = 24  # ch_extremes = int64 idx[8] + double x[8] + double y[8]
 
@@ -86,6 +87,16 @@ def exclusive_offsets(count: torch.Tensor, group=None, out: torch.Tensor | None 
     if out is None:
         out = torch.empty(world, dtype=torch.int64, device=count.device)
     return _all_gather_flat(out, count.reshape(1), group)
+
+
+def agree_status(status: int, group=None) -> int:
+    """The worst (largest) ch_status over the ranks, known to every rank, so
+    that a non-finite coordinate or a late peer seen by one rank makes every
+    rank raise instead of some ranks returning a result built from it."""
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([int(status)], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return int(t.item())
 
 
 def offsets_from_counts(counts, rank: int) -> tuple[int, int]:
@@ -150,6 +161,12 @@ class PeerExchange:
         _lib.check(_lib.load().ch_peer_counts(self._h, c, _stream(stream)), "ch_peer_counts")
         return list(c)
 
+    def counts_status(self, stream=None) -> tuple[int, list[int]]:
+        """(ch_status, counts) without raising (the caller agrees on it first)."""
+        c = (ctypes.c_int64 * self.world)()
+        st = _lib.load().ch_peer_counts(self._h, c, _stream(stream))
+        return st, list(c)
+
     def close(self):
         if getattr(self, "_h", None):
             _lib.load().ch_peer_destroy(self._h)
@@ -204,13 +221,30 @@ class DistFilter:
             filter_compact(xy, self.ws, index_base=self.lo, out=self.out, count=self.count)
         exclusive_offsets(self.count, self.group, out=self.counts)
 
+    def _check_all_ranks(self, st_local: int):
+        """This rank's workspace status (non-finite input, late peer) combined
+        with every other rank's: all ranks raise, or none does."""
+        lib = _lib.load()
+        res = _lib.Result()
+        st = lib.ch_read_result(self.ws.ptr, ctypes.byref(res), _stream(None))
+        if st_local != _lib.CH_OK:
+            st = st_local
+        worst = agree_status(st, self.group)
+        if worst != _lib.CH_OK:
+            detail = (lib.ch_last_error() or b"").decode() if st != _lib.CH_OK else "reported by another rank"
+            raise CHError(worst, "DistFilter.step", f"{lib.ch_status_str(worst).decode()}: {detail}")
+
     def result(self):
-        """(local survivor indices (device view), offset, total) -- synchronizes."""
+        """(local survivor indices (device view), offset, total) -- synchronizes.
+        Raises CHError on every rank if any rank saw a non-finite coordinate
+        or a peer exchange timeout."""
         if self.peer is not None:
-            c = self.peer.counts()
+            st, c = self.peer.counts_status()
+            self._check_all_ranks(st)
             self.counts.copy_(torch.tensor(c, dtype=torch.int64))
             off, total = offsets_from_counts(c, self.rank)
             return self.out[: c[self.rank]], off, total
+        self._check_all_ranks(_lib.CH_OK)
         off, total = offsets_from_counts(self.counts, self.rank)
         cnt = int(self.counts[self.rank].item())
         return self.out[:cnt], off, total

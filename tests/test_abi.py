@@ -132,3 +132,51 @@ def test_host_orient_exact():
         c = a + rng.random() * (b - a)
         c[0] = np.nextafter(c[0], [-np.inf, np.inf][rng.integers(2)])
         assert chf.orient_sign(a, b, c) == orient_exact(a, b, c)
+
+
+def test_caller_octagon_is_validated_before_any_cuda_call():
+    """a caller-supplied octagon with nv outside [0, 8] or an
+    inconsistent `degenerate` flag is rejected on the host (the kernels index
+    eight edge slots); pointers are never dereferenced."""
+    lib = chf._lib.load()
+    P = ctypes.c_void_p
+    ws = P(1 << 20)
+    nbytes = lib.ch_workspace_bytes(100)
+    base = oracle.octagon(np.array([[0, 0], [2, 0], [2, 2], [0, 2], [1, 1]], dtype=np.float64))
+    e = chf.Extremes()
+    for k, i in enumerate([1, 2, 2, 3, 0, 0, 0, 1]):
+        e.idx[k] = i
+    pts = [(0, 0), (2, 0), (2, 2), (0, 2)]
+    for k, i in enumerate([1, 2, 2, 3, 0, 0, 0, 1]):
+        e.x[k], e.y[k] = pts[i]
+    o = chf.octagon_build(e)
+    assert o.nv == base["nv"] == 4
+    for nv, deg in ((9, 0), (-1, 1), (4, 1), (2, 0)):
+        bad = chf.Octagon.from_buffer_copy(o)
+        bad.nv, bad.degenerate = nv, deg
+        st = lib.ch_filter_compact(P(1 << 20), 100, 0, ctypes.byref(bad), P(1 << 21), None, ws, nbytes, None)
+        assert st == 1, (nv, deg)
+        st = lib.ch_octagon_filter(P(1 << 20), 100, ctypes.byref(bad), P(1 << 21), ws, nbytes, None)
+        assert st == 1, (nv, deg)
+
+
+def test_host_orient_exact_tiny_magnitudes():
+    """ADVICE r1: products of coordinate differences below ~2^-969 underflow;
+    the exact stage scales the differences by a power of two (sign-preserving,
+    the determinant is bilinear).  Expected signs follow from scale invariance:
+    det((1,1),(1,1+2^-52)) = 2^-52 > 0 at every scale s."""
+    for s in (2.0 ** -300, 2.0 ** -540, 2.0 ** -600, 2.0 ** -1000):
+        a, b, c = (0.0, 0.0), (s, s), (s, s * (1 + 2.0 ** -52))
+        assert chf.orient_sign(a, b, c) == 1, s
+        assert chf.orient_sign(a, c, b) == -1, s
+        assert chf.orient_sign(a, b, (2 * s, 2 * s)) == 0, s
+
+
+def test_host_hull_golden_scaled_tiny():
+    """The golden hulls are invariant under scaling by a power of two; at
+    2^-540 every product of coordinate differences underflows."""
+    for s in (2.0 ** -470, 2.0 ** -540, 2.0 ** -700):
+        for ex in load_golden():
+            xy = np.array(ex["points"], dtype=np.float64) * s
+            sv = np.array(ex["survivors"], dtype=np.int64)
+            assert list(chf.hull_points(xy[sv], sv)) == ex["hull"], (ex["name"], s)
