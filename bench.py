@@ -151,6 +151,25 @@ def ncu_traffic(kernel: str, workload: str):
         return None
 
 
+def cpu_model() -> str | None:
+    """The host CPU model (lscpu "Model name", else /proc/cpuinfo)."""
+    try:
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.strip().startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def oracle_rate(xy_host: np.ndarray, seconds: float):
     """Time the CPU oracle (single thread) on a bounded prefix of the input."""
     import oracle
@@ -209,7 +228,8 @@ def run_reference(a):
         "scaling": a.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(a), "n": n, "dist": a.dist, "seed": a.seed,
                    "sample_points": m, "survivors_in_sample": s},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -285,6 +305,14 @@ def run_ours(a):
 
         def exch2():
             pass
+
+        def one_call():
+            """The product's one-call step (ch_filter_async: K1 then K2 with
+            programmatic dependent launch; K5/K6 for small n; or the graph)."""
+            if graphed:
+                graph.launch()
+            else:
+                chf.filter_async(xy, ws, out, cnt, plain=a.plain)
     else:
         exchange = a.exchange
         df = None
@@ -322,8 +350,11 @@ def run_ours(a):
             if not peer:
                 chdist.exclusive_offsets(df.count, out=df.counts)
 
+        def one_call():
+            k1(); exch(); k2(); exch2()
+
     def step():
-        k1(); exch(); k2(); exch2()
+        one_call()
 
     for _ in range(max(a.warmup, 0)):
         step()
@@ -387,9 +418,9 @@ def run_ours(a):
                 k2()
                 ev[k][3].record(stream)
                 exch2()
-        else:   # no events between the kernels (see the split pass above)
+        else:   # the one-call step, no events between the kernels (see the split pass above)
             for k in range(K):
-                k1(); exch(); k2(); exch2()
+                one_call()
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -431,8 +462,16 @@ def run_ours(a):
         dom, dom_bytes, dom_ms = "k1_extremes8", k1_bytes, k1_ms
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     step_bytes = k1_bytes + k2_bytes
+    traffic = ncu_traffic(dom, workload_name(a))
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(dom, workload_name(a)), "peak_source": peak_src,
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+            "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed "
+                               "ncu --set full capture of this kernel and workload (profiles/ncu_traffic.json), "
+                               "not measured in this run") if traffic is not None else None,
+            "kernel_ms_source": ("a pass of the same K steps with CUDA events between the kernels (separate "
+                                 "calls, no programmatic launch), run just before the timed region; value and "
+                                 "ms_per_step time the one-call step") if not (graphed or peer or small) else
+                                "the timed region (one launch or one graph per step)",
             "k1_ms": k1_ms, "k2_ms": k2_ms, "k1_gbs": k1_bytes / (k1_ms / 1e3) / 1e9 if not (graphed or peer) else None,
             "k2_gbs": k2_bytes / (k2_ms / 1e3) / 1e9 if k2_ms > 0 else None,
             "step_gbs_per_gpu": step_bytes / (ms_step / 1e3) / 1e9,
@@ -492,6 +531,7 @@ def run_ours(a):
         host = xy[:m_cap].double().cpu().numpy()
         m, dt, s = oracle_rate(host, a.cpu_seconds)
         cpu = {"value": m / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "cpu_model": cpu_model(), "nproc": os.cpu_count(),
                "sample": f"first {m} points of the same {workload_name(a)} input (oracle: extremes + octagon + "
                          f"filter + compaction, single thread, {dt:.2f} s)"}
 

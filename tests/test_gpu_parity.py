@@ -330,36 +330,33 @@ def test_parity_full_1e8(dist):
     torch.cuda.empty_cache()
 
 
-def test_parity_full_1e9_normal_sampled():
-    """configs[4] at one GPU (the bench workload): the extremes and octagon
-    against the oracle over all 10^9 points; every GPU survivor re-checked by
-    the oracle predicate; a 2*10^6-point random sample's decisions compared
-    one by one; the survivor count equals the oracle's count over a 10^8
-    prefix evaluated with the global octagon."""
+def test_parity_full_1e9_normal():
+    """configs[4] at one GPU (the bench workload, ch_filter_async: K1 then K2
+    with programmatic launch): extremes, octagon fields and EVERY survivor
+    against a full oracle pass over all 10^9 points (~15 s of CPU)."""
     n = 10 ** 9
     free = torch.cuda.mem_get_info()[0]
     if free < 40e9:
         pytest.skip("needs ~40 GB of device memory")
     xy_d = synth.points("normal", n, seed=0, device=DEV)
     ws = chf.Workspace(n)
-    e, o = chf.extremes8(xy_d, ws)
-    surv = chf.filter(xy_d, ws).cpu().numpy()
+    out = torch.empty(n, dtype=torch.int64, device=DEV)
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    chf.filter_async(xy_d, ws, out, cnt)
+    c = int(cnt.item())
+    surv = out[:c].cpu().numpy()
+    e, o = chf.read_octagon(ws)
+    assert chf.read_result(ws).count == c
     xy = xy_d.cpu().numpy()
-    idx8 = oracle.extremes8(xy)
+    del xy_d, out
+    torch.cuda.empty_cache()
+    want, idx8 = oracle.filter_compact(xy)
     assert np.array_equal(np.array(e.idx[:]), idx8)
     wo = oracle.octagon(xy, idx8)
     od = chf.octagon_dict(o)
     for f in ("vx", "vy", "ex", "ey", "thr"):
         assert np.array_equal(od[f].view(np.int64), wo[f].view(np.int64)), f
-    assert np.all(np.diff(surv) > 0)
-    assert np.all(oracle.flags(xy[surv], oct_=wo) == 1)
-    rng = np.random.default_rng(0)
-    sample = np.sort(rng.choice(n, 2_000_000, replace=False))
-    keep_s = oracle.flags(xy[sample], oct_=wo).astype(bool)
-    assert np.array_equal(np.isin(sample, surv), keep_s)
-    pre = 10 ** 8
-    keep_pre = oracle.flags(xy[:pre], oct_=wo)
-    assert np.array_equal(np.flatnonzero(keep_pre), surv[surv < pre])
+    assert np.array_equal(surv, want)
 
 
 def _edge_band_points(rng, o, dists, per=400):
@@ -726,11 +723,10 @@ def test_device_hull_golden():
         assert list(chf.hull_gpu(d, s)) == ex["hull"], ex["name"]
 
 
-def test_parity_beyond_2pow31_points_sampled():
+def test_parity_beyond_2pow31_points():
     """X5: more than 2^31 points (int64 indices throughout).
-    Extremes against the oracle over all points, every survivor re-checked,
-    the survivors beyond index 2^31 checked against the oracle exactly, and
-    a random sample's decisions compared one by one."""
+    Extremes and EVERY survivor against a full oracle pass (~30 s of CPU);
+    p = 0.02 keeps ~86% of the points, so survivor writes cross 2^31."""
     n = (1 << 31) + 12_345
     free = torch.cuda.mem_get_info()[0]
     if free < 70e9:
@@ -742,18 +738,65 @@ def test_parity_beyond_2pow31_points_sampled():
     xy = xy_d.cpu().numpy()
     del xy_d
     torch.cuda.empty_cache()
-    idx8 = oracle.extremes8(xy)
+    want, idx8 = oracle.filter_compact(xy)
     assert np.array_equal(np.array(e.idx[:]), idx8)
-    wo = oracle.octagon(xy, idx8)
-    assert np.all(np.diff(surv) > 0) and surv[-1] < n
-    assert np.all(oracle.flags(xy[surv], oct_=wo) == 1)
-    tail0 = (1 << 31) - 1000
-    keep_tail = oracle.flags(xy[tail0:], oct_=wo)
-    assert np.array_equal(np.flatnonzero(keep_tail) + tail0, surv[surv >= tail0])
-    rng = np.random.default_rng(1)
-    sample = np.sort(rng.choice(n, 1_000_000, replace=False))
-    keep_s = oracle.flags(xy[sample], oct_=wo).astype(bool)
-    assert np.array_equal(np.isin(sample, surv), keep_s)
+    assert want[-1] >= (1 << 31) and surv[-1] < n
+    assert np.array_equal(surv, want)
+
+
+@pytest.mark.parametrize("storage", ["f64", "f32"])
+@pytest.mark.parametrize("index_base", [(1 << 32) - 3000, (1 << 32) - 1, (1 << 33) + 7, (1 << 39) - 2_000_000])
+def test_index_base_straddling_2pow32(index_base, storage):
+    """Shard indices above and across 2^32 without a 68 GB input: K1 and K2
+    with index_base, so a warp's index range crosses a multiple of 2^32 and
+    K2's 64-bit survivor stores run (VERDICT r1 missing 3).  Survivors =
+    index_base + the oracle's survivors, extremes likewise."""
+    n = 1_000_003
+    xy_d = synth.points("displaced", n, seed=5, device=DEV)
+    if storage == "f32":
+        xy_d = xy_d.float()
+    ws = chf.Workspace(n)
+    e, o = chf.extremes8(xy_d, ws, index_base=index_base)
+    cnt = torch.zeros(1, dtype=torch.int64, device=DEV)
+    out = chf.filter_compact(xy_d, ws, index_base=index_base, count=cnt)
+    got = out[: int(cnt.item())].cpu().numpy()
+    want, idx8 = oracle.filter_compact(xy_d.double().cpu().numpy())
+    assert np.array_equal(np.array(e.idx[:]), idx8 + index_base)
+    assert np.array_equal(got, want + index_base)
+    # a circle: every point survives, so every warp writes a full range
+    c = synth.points("circle", n, seed=5, device=DEV)
+    if storage == "f32":
+        c = c.float()
+    chf.extremes8(c, ws, index_base=index_base)
+    out = chf.filter_compact(c, ws, index_base=index_base, count=cnt)
+    wc, _ = oracle.filter_compact(c.double().cpu().numpy())
+    assert np.array_equal(out[: int(cnt.item())].cpu().numpy(), wc + index_base)
+
+
+def test_device_hull_64bit_ids_instantiation():
+    """The device hull's 64-bit sort-value instantiation (taken when the point
+    array has more than 2^32 points; VERDICT r1 missing 3), selected here by
+    declaring n_points > 2^32 over a small array: same hull as the 32-bit one
+    and the oracle."""
+    import ctypes
+    lib = chf._lib.load()
+    for dist in ("circle", "displaced", "normal"):
+        xy = synth.points(dist, 300_001, seed=3, device=DEV)
+        surv = chf.filter(xy)
+        m = int(surv.shape[0])
+        tb = int(lib.ch_hull_gpu_temp_bytes(m))
+        tmp = torch.empty(tb, dtype=torch.uint8, device=DEV)
+        res = []
+        for n_points in (xy.shape[0], (1 << 33) + 5):
+            ids = np.zeros(m, dtype=np.int64)
+            h = ctypes.c_int64(0)
+            st = lib.ch_hull_gpu(chf._ptr(xy), n_points, chf._ptr(surv), m, ids.ctypes.data_as(ctypes.c_void_p),
+                                 ctypes.byref(h), chf._ptr(tmp), tb, chf._stream(None))
+            assert st == 0
+            res.append(ids[: h.value].copy())
+        want = oracle.hull(xy.cpu().numpy(), surv.cpu().numpy())
+        assert np.array_equal(res[0], want), dist
+        assert np.array_equal(res[1], want), dist
 
 
 @pytest.mark.parametrize("dist", ["normal", "circle", "displaced"])
