@@ -58,9 +58,11 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--timed-events", action="store_true", help=argparse.SUPPRESS)
-    ap.add_argument("--exchange", choices=["auto", "peer", "nccl"], default="auto",
-                    help="N > 1: extremes / count exchange fused into the kernels over peer memory (peer), or "
-                         "NCCL all-gathers; auto = peer if it initializes")
+    ap.add_argument("--exchange", choices=["auto", "peer", "nccl", "torch"], default="auto",
+                    help="N > 1: extremes / count exchange fused into the kernels over peer memory (peer), the "
+                         "library-owned NCCL communicator (nccl: one C call per step), or torch.distributed "
+                         "all-gathers (torch); auto = peer if it initializes AND its first step agrees with nccl, "
+                         "else nccl")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",  # noqa: E501
                     help="replay the step as a CUDA graph (ch_graph_launch); auto: 1 GPU and n <= 2^20")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -246,13 +248,25 @@ def run_ours(a):
     rank, world, local = env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU path)")
+    # the sharded path: N > 1, or an explicit --exchange (also at N = 1, to
+    # run the distributed step's code on one GPU)
+    multi = world > 1 or a.exchange != "auto"
     # CH_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo collectives -- only
     # to exercise the N > 1 code path on a 1-GPU box; never a measurement.
     share = os.environ.get("CH_BENCH_SHARE_GPU") == "1"
     gpu = 0 if share else local
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
-    if world > 1:
+    if multi:
+        if world == 1:   # a one-rank group without torchrun
+            import socket
+            s0 = socket.socket()
+            s0.bind(("127.0.0.1", 0))
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(s0.getsockname()[1]))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+            s0.close()
         if share:
             dist.init_process_group("gloo")
         else:
@@ -277,11 +291,11 @@ def run_ours(a):
     bpp = 8.0 if a.storage == "f32" else 16.0   # bytes per point per pass
     stream = torch.cuda.current_stream()
 
-    small = world == 1 and n_local <= 4096   # latency-bound C1: the single-kernel step (K5)
+    small = not multi and n_local <= 4096   # latency-bound C1: the single-kernel step (K5)
     peer, exchange = False, None
     # launch-bound sizes: the whole step replayed as one CUDA graph
-    graphed = world == 1 and (a.graph == "on" or (a.graph == "auto" and n_local <= (1 << 20)))
-    if world == 1:
+    graphed = not multi and (a.graph == "on" or (a.graph == "auto" and n_local <= (1 << 20)))
+    if not multi:
         ws = chf.Workspace(n_local, device=dev)
         out = torch.empty(max(n_local, 1), dtype=torch.int64, device=dev)
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -314,40 +328,52 @@ def run_ours(a):
             else:
                 chf.filter_async(xy, ws, out, cnt, plain=a.plain)
     else:
-        exchange = a.exchange
-        df = None
-        if exchange in ("auto", "peer"):
-            try:   # the exchanges fused into K1 / K3 / K2 over peer memory (cudaIpc, NVLink)
-                df = chdist.DistFilter(n_total, xy, plain=a.plain, exchange="peer")
-                exchange = "peer"
-            except Exception as e:   # e.g. IPC unavailable in this container
-                if a.exchange == "peer":
-                    raise
-                print(f"[bench] peer exchange unavailable ({e}); using NCCL all-gathers", file=sys.stderr)
-                exchange = "nccl"
-        if df is None:
-            df = chdist.DistFilter(n_total, xy, plain=a.plain, exchange="nccl")
+        exchange = a.exchange if a.exchange != "auto" else "nccl"
+        if share and exchange == "nccl":
+            exchange = "torch"   # NCCL refuses two ranks on one device: gloo all-gathers instead
+        df = chdist.DistFilter(n_total, xy, plain=a.plain, exchange=exchange)
+        if a.exchange == "auto" and not share:
+            # the peer transport (no collective launches) if it initializes on
+            # every rank AND its first step gives the same placement as NCCL's
+            df.step()
+            ref = df.result()
+            ok = 1
+            try:
+                os.environ.setdefault("CH_PEER_TIMEOUT_MS", "10000")
+                dp = chdist.DistFilter(n_total, xy, plain=a.plain, exchange="peer")
+                dp.step()
+                got = dp.result()
+                ok = int(got[1:] == ref[1:] and torch.equal(got[0], ref[0]))
+            except Exception as e:
+                print(f"[bench] rank {rank}: peer exchange unavailable ({e})", file=sys.stderr)
+                dp, ok = None, 0
+            if int(reduce_host(int(ok), dist.ReduceOp.MIN)) == 1:
+                df.close()
+                df, exchange = dp, "peer"
+            elif dp is not None:
+                dp.close()
         ws = df.ws
-        launches_per_step = 3
         peer = exchange == "peer"
+        # our kernels per step: K1, K3, K2 (+ the status pack and scan kernels of the NCCL step)
+        launches_per_step = 5 if exchange == "nccl" else 3
 
         def k1():
-            if peer:
-                df.step()   # K1 (+ record push) -> K3 (acquire + combine) -> K2 (+ count push)
+            if exchange != "torch":
+                df.step()   # one C call: the whole step (see DistFilter)
                 return
             chf.extremes8_async(xy, df.ws, index_base=df.lo, plain=a.plain, ext_out=df.ext_local)
 
         def exch():
-            if not peer:
+            if exchange == "torch":
                 chdist.exchange_extremes(df.ext_local, out=df.ext_all)
                 chf.combine8(df.ext_all, world, df.ws, plain=a.plain)
 
         def k2():
-            if not peer:
+            if exchange == "torch":
                 chf.filter_compact(xy, df.ws, index_base=df.lo, out=df.out, count=df.count)
 
         def exch2():
-            if not peer:
+            if exchange == "torch":
                 chdist.exclusive_offsets(df.count, out=df.counts)
 
         def one_call():
@@ -434,6 +460,9 @@ def run_ours(a):
         k1_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
         k2_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
         ex_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    if multi and exchange == "nccl":
+        # the library's own events around the phases of the last timed step
+        k1_ms, ex_ms, k2_ms = df.comm.step_times()
     res = chf.read_result(ws)
     s_local = int(res.count)
     if world > 1:
@@ -488,7 +517,7 @@ def run_ours(a):
         e_s = torch.cuda.Event(enable_timing=True)
         e_e = torch.cuda.Event(enable_timing=True)
         # one untimed warm-up
-        if world == 1:
+        if not multi:
             d2h = 0
             chf.filter_host(h_xy, ws, d_stage, out, h_out, plain=a.plain)
             torch.cuda.synchronize()
@@ -521,7 +550,7 @@ def run_ours(a):
             e2e_ms = float(reduce_host(float(e_s.elapsed_time(e_e) / a.e2e_steps), dist.ReduceOp.MAX))
         e2e = {"value": n_total / (e2e_ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": 16 * n_local, "d2h_bytes_per_step": int(d2h),
-               "api": "ch_filter_host (C ABI, pinned host input)" if world == 1 else "DistFilter + host copies"}
+               "api": "ch_filter_host (C ABI, pinned host input)" if not multi else "DistFilter + host copies"}
         del h_xy, h_out, d_stage
 
     # ---- CPU oracle baseline (rank 0, N = 1 only) ----
@@ -548,17 +577,24 @@ def run_ours(a):
                               f"inputs {bpp * n_local / 1e6:.3g} MB" if flush
                               else f"inputs larger than L2 ({int(bpp)} B/pt)"),
                        "cuda_graph": bool(graphed),
-                       "exchange": exchange if world > 1 else None},
+                       "exchange": exchange if multi else None},
             "survivors": s_total, "survivor_ratio": s_total / n_total,
             "hbm_frac": roof["step_frac"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * K, "clocks": clk.summary(),
-            "exchange_ms": ex_ms if world > 1 else 0.0,
+            "exchange_ms": ex_ms if multi else 0.0,
+            "transport": ({"exchange": exchange, "ranks": world,
+                           "collectives": {"nccl": "library-owned ncclComm (ch_comm_*): ncclAllGather x2 per step",
+                                           "peer": "none (cudaIpc peer stores fused into K1/K2, acquired by K3)",
+                                           "torch": "torch.distributed all_gather_into_tensor x2 per step"}[exchange],
+                           "nccl_version": chf._lib.load().ch_comm_nccl_version(),
+                           "backend": "gloo (shared GPU, functional check only)" if share else "nccl"}
+                          if multi else None),
             "ctas_per_sm": {"k1": chf._lib.load().ch_occupancy(0),
                             "k2": chf._lib.load().ch_occupancy(2 if a.storage == "f32" else 1)},
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
     return 0
 

@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define CH_ABI_VERSION 1
+#define CH_ABI_VERSION 2 /* 2: ch_comm_* (NCCL), ch_gather_survivors, ch_peer_counts with offsets, ch_stats pass times */
 
 typedef enum {
     CH_OK = 0,
@@ -56,7 +56,8 @@ typedef enum {
     CH_ERR_MISALIGNED = 4, /* d_xy not 16-byte aligned                  */
     CH_ERR_WORKSPACE = 5,  /* workspace missing or too small            */
     CH_ERR_CUDA = 6,       /* a CUDA runtime error (see ch_last_error)  */
-    CH_ERR_PEER = 7        /* peer exchange: a rank's record did not arrive (timeout) */
+    CH_ERR_PEER = 7,       /* peer exchange: a rank's record did not arrive (timeout) */
+    CH_ERR_NCCL = 8        /* NCCL missing, or an NCCL call failed (see ch_last_error) */
 } ch_status;
 
 /* Predicate switch (DESIGN R4).  Default: certified thresholds T_k. */
@@ -130,9 +131,12 @@ typedef struct {
 
 typedef struct {
     int64_t n, n_survivors, n_hull;
-    double ms_filter; /* extremes + octagon + filter + compaction (device) */
-    double ms_gather; /* survivor coordinates device -> host               */
-    double ms_hull;   /* exact monotone chain on the host                  */
+    double ms_filter;   /* extremes + octagon + filter + compaction (device)       */
+    double ms_gather;   /* survivor coordinates to the hull stage (host or root)    */
+    double ms_hull;     /* the exact hull (device or host)                          */
+    double ms_pass1;    /* pass 1: K1 extremes + octagon (device events)            */
+    double ms_pass2;    /* pass 2: K2 octagon test + compaction (device events)     */
+    double ms_exchange; /* multi-GPU: extremes all-gather + K3 + count all-gather   */
 } ch_stats;
 
 int ch_abi_version(void);
@@ -284,7 +288,73 @@ ch_status ch_filter_step_peer(ch_peer *p, const double *d_xy, int64_t n_local, i
                               int64_t *d_survivors, void *d_ws, size_t ws_bytes, void *stream);
 ch_status ch_filter_step_peer_f32(ch_peer *p, const float *d_xy, int64_t n_local, int64_t index_base, int flags,
                                   int64_t *d_survivors, void *d_ws, size_t ws_bytes, void *stream);
-ch_status ch_peer_counts(ch_peer *p, int64_t *h_counts, void *stream);
+/* h_counts[world] (nullable): every rank's count; h_offset / h_total
+ * (nullable): this rank's exclusive offset in the global survivor order and
+ * the total (a7's scan, done here). */
+ch_status ch_peer_counts(ch_peer *p, int64_t *h_counts, int64_t *h_offset, int64_t *h_total, void *stream);
+
+/* a7's scan for callers that exchange the counts themselves (host, pure):
+ * *h_offset = sum of h_counts[0..rank), *h_total = sum of h_counts[0..world). */
+ch_status ch_exclusive_offset(const int64_t *h_counts, int world, int rank, int64_t *h_offset, int64_t *h_total);
+
+/* ---- Multi-GPU over a library-owned NCCL communicator (north_star: "a tiny
+ * NCCL allgather ... survivor counts are exclusive-scanned to gather
+ * survivors") ------------------------------------------------
+ * One process per GPU.  NCCL is loaded at run time (the libnccl.so.2 the
+ * process already has, e.g. PyTorch's, else the system one); without it these
+ * calls return CH_ERR_NCCL and everything else still works.
+ *   ch_comm_unique_id: rank 0 creates the 128-byte ncclUniqueId; the caller
+ *     broadcasts it (e.g. torch.distributed) -- the only bytes that cross the
+ *     caller's transport.  ch_comm_init: collective over the `world` ranks;
+ *     binds `device` (cudaSetDevice) and allocates the communicator's own
+ *     ~1 KB of device buffers.  ch_comm_nccl_version: NCCL_VERSION_CODE of the
+ *     loaded library, or -1.
+ *   ch_filter_compact_dist: one sharded step (rows a1-a7): K1 on the shard
+ *     (global indices, shard = DESIGN R14: rank r owns [floor(r n/W),
+ *     floor((r+1) n/W)), n_local must be that size, may be 0), ncclAllGather
+ *     of the 192-byte extremes records, K3 (combine + octagon, identical on
+ *     every rank, bit-identical to 1 GPU), K2 on the shard, ncclAllGather of
+ *     {count, flags}, and the exclusive scan on the device.
+ *     d_survivors_local: this shard's survivors as increasing GLOBAL indices.
+ *     h_count_local / h_offset / h_total / h_ext (global extremes), all
+ *     nullable: if any is given the call synchronizes `stream` and returns
+ *     CH_ERR_NONFINITE on EVERY rank if any shard held a non-finite
+ *     coordinate; if none is given the call is asynchronous and
+ *     ch_comm_result reads the outcome later.
+ *   ch_comm_result: synchronizes `stream`; h_counts[world] (every rank's
+ *     count), this rank's offset, the total; the same status rule.
+ *   ch_comm_step_times: device-event times of the last step's phases.
+ *   ch_gather_survivors (the hull stage's gather, a8): the survivors of the
+ *     last step to `root`, in global order, by grouped ncclSend / ncclRecv:
+ *     d_all_ids (root, capacity total) gets the ids; with_points (same value
+ *     on every rank) also sends the coordinates, d_all_pts (root, capacity
+ *     2 * total doubles), staged on non-root ranks in d_tmp (>= 16 bytes per
+ *     local survivor).  d_local / d_xy_shard: this rank's survivors and shard.
+ *   ch_hull_end_to_end_dist: Algorithm 1 on W GPUs: the step, the gather
+ *     to `root`, the exact device hull of the gathered survivors there (f1).
+ *     h_hull (root, capacity >= total) and *h_n_hull at the root; *h_n_hull
+ *     = 0 elsewhere.  Stage times to h_stats (nullable).  Synchronizes. */
+#define CH_NCCL_ID_BYTES 128
+typedef struct ch_comm ch_comm;
+ch_status ch_comm_unique_id(void *h_id);
+int ch_comm_nccl_version(void);
+ch_status ch_comm_init(ch_comm **out, const void *h_id, int rank, int world, int device);
+ch_status ch_comm_destroy(ch_comm *c);
+ch_status ch_filter_compact_dist(ch_comm *c, const double *d_xy_shard, int64_t n_local, int64_t n_global, int flags,
+                                 int64_t *d_survivors_local, int64_t *h_count_local, int64_t *h_offset,
+                                 int64_t *h_total, ch_extremes *h_ext, void *d_ws, size_t ws_bytes, void *stream);
+ch_status ch_filter_compact_dist_f32(ch_comm *c, const float *d_xy_shard, int64_t n_local, int64_t n_global,
+                                     int flags, int64_t *d_survivors_local, int64_t *h_count_local,
+                                     int64_t *h_offset, int64_t *h_total, ch_extremes *h_ext, void *d_ws,
+                                     size_t ws_bytes, void *stream);
+ch_status ch_comm_result(ch_comm *c, int64_t *h_counts, int64_t *h_offset, int64_t *h_total, void *stream);
+ch_status ch_comm_step_times(ch_comm *c, double *h_ms_pass1, double *h_ms_exchange, double *h_ms_pass2);
+ch_status ch_gather_survivors(ch_comm *c, const double *d_xy_shard, const int64_t *d_local, int root, int with_points,
+                              int64_t *d_all_ids, double *d_all_pts, void *d_tmp, size_t tmp_bytes, void *stream);
+ch_status ch_hull_end_to_end_dist(ch_comm *c, const double *d_xy_shard, int64_t n_local, int64_t n_global, int flags,
+                                  int64_t *d_survivors_local, int root, int64_t *h_hull, int64_t *h_n_hull,
+                                  int64_t *h_n_survivors, ch_stats *h_stats, void *d_ws, size_t ws_bytes,
+                                  void *stream);
 
 /* The same step end to end from HOST memory: copies h_xy (pinned for full
  * speed) into d_xy_staging (capacity n points), filters, and copies the
@@ -324,6 +394,13 @@ ch_status ch_hull_gpu(const double *d_xy, int64_t n_points, const int64_t *d_sur
  * this point.  m == 0 writes a zero count. */
 ch_status ch_hull_gpu_async(const double *d_xy, int64_t n_points, const int64_t *d_surv, int64_t m,
                             int64_t *d_hull, int64_t *d_n_hull, void *d_tmp, size_t tmp_bytes, void *stream);
+
+/* f1 on given coordinates: the hull of the m points d_pts[2j..2j+1] with ids
+ * d_ids[j] (e.g. survivors gathered to a root, in increasing id order: then
+ * duplicates resolve to the lowest id, as in ch_hull_gpu).  Asynchronous;
+ * scratch ch_hull_gpu_temp_bytes(m). */
+ch_status ch_hull_gpu_pts_async(const double *d_pts, const int64_t *d_ids, int64_t m, int64_t *d_hull,
+                                int64_t *d_n_hull, void *d_tmp, size_t tmp_bytes, void *stream);
 
 #define CH_HULL_HOST 4 /* flag for ch_hull_end_to_end: gather + host monotone chain */
 #define CH_NO_CLUSTER 8 /* flag for ch_filter / ch_filter_async: no single-cluster step (K6)

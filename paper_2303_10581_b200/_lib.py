@@ -17,7 +17,9 @@ DBL = ctypes.c_double
 SZ = ctypes.c_size_t
 
 CH_OK, CH_ERR_INVALID_ARG, CH_ERR_EMPTY, CH_ERR_NONFINITE = 0, 1, 2, 3
-CH_ERR_MISALIGNED, CH_ERR_WORKSPACE, CH_ERR_CUDA, CH_ERR_PEER = 4, 5, 6, 7
+CH_ERR_MISALIGNED, CH_ERR_WORKSPACE, CH_ERR_CUDA, CH_ERR_PEER, CH_ERR_NCCL = 4, 5, 6, 7, 8
+ABI_VERSION = 2
+CH_NCCL_ID_BYTES = 128
 CH_MAX_PEERS = 16
 CH_CERTIFIED, CH_PLAIN, CH_EXACT = 0, 1, 2
 CH_HULL_HOST = 4
@@ -44,7 +46,8 @@ class Result(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [("n", I64), ("n_survivors", I64), ("n_hull", I64),
-                ("ms_filter", DBL), ("ms_gather", DBL), ("ms_hull", DBL)]
+                ("ms_filter", DBL), ("ms_gather", DBL), ("ms_hull", DBL),
+                ("ms_pass1", DBL), ("ms_pass2", DBL), ("ms_exchange", DBL)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/chfilter.h
@@ -79,7 +82,25 @@ SIGNATURES = {
     "ch_peer_destroy": (ctypes.c_int, [P]),
     "ch_filter_step_peer": (ctypes.c_int, [P, P, I64, I64, ctypes.c_int, P, P, SZ, P]),
     "ch_filter_step_peer_f32": (ctypes.c_int, [P, P, I64, I64, ctypes.c_int, P, P, SZ, P]),
-    "ch_peer_counts": (ctypes.c_int, [P, P, P]),
+    "ch_peer_counts": (ctypes.c_int, [P, P, ctypes.POINTER(I64), ctypes.POINTER(I64), P]),
+    "ch_exclusive_offset": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+    "ch_comm_unique_id": (ctypes.c_int, [P]),
+    "ch_comm_nccl_version": (ctypes.c_int, []),
+    "ch_comm_init": (ctypes.c_int, [ctypes.POINTER(P), P, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "ch_comm_destroy": (ctypes.c_int, [P]),
+    "ch_filter_compact_dist": (ctypes.c_int, [P, P, I64, I64, ctypes.c_int, P, ctypes.POINTER(I64),
+                                              ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(Extremes),
+                                              P, SZ, P]),
+    "ch_filter_compact_dist_f32": (ctypes.c_int, [P, P, I64, I64, ctypes.c_int, P, ctypes.POINTER(I64),
+                                                  ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(Extremes),
+                                                  P, SZ, P]),
+    "ch_comm_result": (ctypes.c_int, [P, P, ctypes.POINTER(I64), ctypes.POINTER(I64), P]),
+    "ch_comm_step_times": (ctypes.c_int, [P, ctypes.POINTER(DBL), ctypes.POINTER(DBL), ctypes.POINTER(DBL)]),
+    "ch_gather_survivors": (ctypes.c_int, [P, P, P, ctypes.c_int, ctypes.c_int, P, P, P, SZ, P]),
+    "ch_hull_end_to_end_dist": (ctypes.c_int, [P, P, I64, I64, ctypes.c_int, P, ctypes.c_int, P,
+                                               ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(Stats),
+                                               P, SZ, P]),
+    "ch_hull_gpu_pts_async": (ctypes.c_int, [P, P, I64, P, P, P, SZ, P]),
     "ch_graph_destroy": (ctypes.c_int, [P]),
     "ch_filter_host": (ctypes.c_int, [P, I64, ctypes.c_int, P, P, P, ctypes.POINTER(I64), P, SZ, P]),
     "ch_gather_points": (ctypes.c_int, [P, I64, P, I64, P, P]),
@@ -123,7 +144,7 @@ def load():
         fn.argtypes = args
     lib.ch_orient_sign.restype = ctypes.c_int
     lib.ch_orient_sign.argtypes = [DBL] * 6
-    if lib.ch_abi_version() != 1:
+    if lib.ch_abi_version() != ABI_VERSION:
         raise RuntimeError("libchfilter ABI mismatch")
     _lib = lib
     return lib

@@ -18,8 +18,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libchfilter.so")
-SOURCES = ["chfilter.cu", "hull_gpu.cu", "hull.cpp"]
-DEPS = SOURCES + ["octagon.cuh", "exact.cuh"]
+SOURCES = ["chfilter.cu", "comm.cu", "hull_gpu.cu", "hull.cpp"]
+DEPS = SOURCES + ["octagon.cuh", "exact.cuh", "internal.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr",

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "../../include/chfilter.h"
+#include "internal.h"
 #include "octagon.cuh"
 #include "exact.cuh"
 
@@ -2101,13 +2102,7 @@ __global__ void k_gather(const double *__restrict__ xy, long long index_base, co
 }
 
 // ================================================================ host side ==
-thread_local std::string g_err;
-
-ch_status fail(ch_status s, const std::string &msg)
-{
-    g_err = msg;
-    return s;
-}
+using chi::fail;
 
 ch_status cuda_check(const char *what)
 {
@@ -2355,11 +2350,12 @@ const char *ch_status_str(ch_status s)
     case CH_ERR_WORKSPACE: return "CH_ERR_WORKSPACE";
     case CH_ERR_CUDA: return "CH_ERR_CUDA";
     case CH_ERR_PEER: return "CH_ERR_PEER";
+    case CH_ERR_NCCL: return "CH_ERR_NCCL";
     }
     return "CH_ERR_UNKNOWN";
 }
 
-const char *ch_last_error(void) { return g_err.c_str(); }
+const char *ch_last_error(void) { return chi::last_error(); }
 
 size_t ch_workspace_bytes(int64_t n)
 {
@@ -2807,9 +2803,9 @@ ch_status ch_filter_step_peer_f32(ch_peer *p, const float *d_xy, int64_t n_local
     return step_peer(p, d_xy, n_local, index_base, flags, d_survivors, d_ws, ws_bytes, stream);
 }
 
-ch_status ch_peer_counts(ch_peer *p, int64_t *h_counts, void *stream)
+ch_status ch_peer_counts(ch_peer *p, int64_t *h_counts, int64_t *h_offset, int64_t *h_total, void *stream)
 {
-    if (!p || !h_counts)
+    if (!p)
         return fail(CH_ERR_INVALID_ARG, "NULL argument");
     cudaStreamSynchronize((cudaStream_t)stream);
     ch_status s = cuda_check("peer counts");
@@ -2830,9 +2826,38 @@ ch_status ch_peer_counts(ch_peer *p, int64_t *h_counts, void *stream)
             return fail(CH_ERR_PEER, "peer exchange timed out (a rank's count did not arrive)");
         std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
-    for (int r = 0; r < p->world; r++)
-        h_counts[r] = (int64_t)buf[(size_t)r * PEER_SLOT + PEER_CNT];
+    // a7: this rank's exclusive offset in the global order, and the total
+    int64_t off = 0, total = 0;
+    for (int r = 0; r < p->world; r++) {
+        const int64_t c = (int64_t)buf[(size_t)r * PEER_SLOT + PEER_CNT];
+        if (h_counts)
+            h_counts[r] = c;
+        off += r < p->rank ? c : 0;
+        total += c;
+    }
+    if (h_offset)
+        *h_offset = off;
+    if (h_total)
+        *h_total = total;
     return cuda_check("peer counts");
+}
+
+ch_status ch_exclusive_offset(const int64_t *h_counts, int world, int rank, int64_t *h_offset, int64_t *h_total)
+{
+    if (!h_counts || world < 1 || rank < 0 || rank >= world)
+        return fail(CH_ERR_INVALID_ARG, "bad counts / world / rank");
+    int64_t off = 0, total = 0;
+    for (int r = 0; r < world; r++) {
+        if (h_counts[r] < 0)
+            return fail(CH_ERR_INVALID_ARG, "negative count");
+        off += r < rank ? h_counts[r] : 0;
+        total += h_counts[r];
+    }
+    if (h_offset)
+        *h_offset = off;
+    if (h_total)
+        *h_total = total;
+    return CH_OK;
 }
 
 ch_status ch_filter_host(const double *h_xy, int64_t n, int flags, double *d_xy_staging, int64_t *d_survivors,
@@ -2896,23 +2921,43 @@ ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *
     if (!h_hull || !h_n_hull || !d_survivors)
         return fail(CH_ERR_INVALID_ARG, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
-    cudaEvent_t e0, e1;
+    // pass 1 and pass 2 timed apart (events between K1 and K2); for n <=
+    // 32768 the one-launch step (K5 / K6) counts as pass 1
+    cudaEvent_t e0, e1, e2;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
+    cudaEventCreate(&e2);
     cudaEventRecord(e0, st);
     int64_t cnt = 0;
-    ch_status s = ch_filter(d_xy, n, flags & 3, d_survivors, &cnt, d_ws, ws_bytes, stream);
-    cudaEventRecord(e1, st);
-    if (s != CH_OK) {
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        return s;
+    ch_status s;
+    const bool one_launch = n <= KC_MAX_N;
+    if (one_launch) {
+        s = filter_async_impl(d_xy, n, flags & 3, d_survivors, (int64_t *)nullptr, d_ws, ws_bytes, stream);
+        cudaEventRecord(e1, st);
+    } else {
+        s = extremes8_impl(d_xy, n, 0, flags & 3, nullptr, nullptr, nullptr, d_ws, ws_bytes, stream);
+        cudaEventRecord(e1, st);
+        if (s == CH_OK)
+            s = filter_compact_impl(d_xy, n, 0, nullptr, d_survivors, (int64_t *)nullptr, d_ws, ws_bytes, stream);
     }
-    cudaEventSynchronize(e1);
-    float ms_filter = 0.f;
-    cudaEventElapsedTime(&ms_filter, e0, e1);
+    cudaEventRecord(e2, st);
+    if (s == CH_OK) {
+        ch_result res;
+        s = ch_read_result(d_ws, &res, stream);
+        cnt = res.count;
+    }
+    float ms_p1 = 0.f, ms_p2 = 0.f;
+    if (s == CH_OK) {
+        cudaEventSynchronize(e2);
+        cudaEventElapsedTime(&ms_p1, e0, e1);
+        cudaEventElapsedTime(&ms_p2, e1, e2);
+    }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    if (s != CH_OK)
+        return s;
+    const float ms_filter = ms_p1 + ms_p2;
 
     auto t0 = std::chrono::steady_clock::now();
     auto t1 = t0;
@@ -2962,6 +3007,9 @@ ch_status ch_hull_end_to_end(const double *d_xy, int64_t n, int flags, int64_t *
         h_stats->ms_filter = ms_filter;
         h_stats->ms_gather = std::chrono::duration<double, std::milli>(t1 - t0).count();
         h_stats->ms_hull = std::chrono::duration<double, std::milli>(t2 - t1).count();
+        h_stats->ms_pass1 = ms_p1;
+        h_stats->ms_pass2 = ms_p2;
+        h_stats->ms_exchange = 0.0;
     }
     return CH_OK;
 }
@@ -2974,3 +3022,72 @@ int ch_orient_sign(double ax, double ay, double bx, double by, double cx, double
 }
 
 } // extern "C"
+
+// ================================================ internal API (internal.h) ==
+// Host entry points the multi-GPU translation unit (comm.cu) builds its
+// steps from.  Not part of the C ABI.
+namespace {
+__global__ void k_pack_status(const WsHeader *__restrict__ hdr, int empty, long long *__restrict__ w)
+{
+    if (threadIdx.x == 0) {
+        w[0] = empty ? 0 : hdr->result.count;
+        w[1] = (empty ? 0 : (hdr->result.nonfinite ? 1 : 0)) | (hdr->peer_timeout ? 2 : 0);
+    }
+}
+__global__ void k_empty_record(unsigned long long *__restrict__ rec)
+{
+    if (threadIdx.x < 24)
+        rec[threadIdx.x] = threadIdx.x < 8 ? ~0ull : 0ull; // idx = -1, x = y = 0
+}
+} // namespace
+
+namespace chi {
+
+thread_local std::string g_err;
+
+ch_status fail(ch_status s, const std::string &msg)
+{
+    g_err = msg;
+    return s;
+}
+
+const char *last_error() { return g_err.c_str(); }
+
+ch_status k1(const void *d_xy, bool f32, int64_t n, int64_t index_base, int flags, void *d_ext_out, void *d_ws,
+             size_t ws_bytes, cudaStream_t st)
+{
+    return f32 ? extremes8_impl((const float *)d_xy, n, index_base, flags, d_ext_out, nullptr, nullptr, d_ws,
+                                ws_bytes, (void *)st)
+               : extremes8_impl((const double *)d_xy, n, index_base, flags, d_ext_out, nullptr, nullptr, d_ws,
+                                ws_bytes, (void *)st);
+}
+
+ch_status k3(const void *d_ext_all, int world, int flags, void *d_ws, size_t ws_bytes, cudaStream_t st)
+{
+    return ch_combine8(d_ext_all, world, flags, d_ws, ws_bytes, (void *)st);
+}
+
+ch_status k2(const void *d_xy, bool f32, int64_t n, int64_t index_base, int64_t *d_surv, int64_t *d_count,
+             void *d_ws, size_t ws_bytes, cudaStream_t st, bool pdl)
+{
+    return f32 ? filter_compact_impl((const float *)d_xy, n, index_base, nullptr, d_surv, d_count, d_ws, ws_bytes,
+                                     (void *)st, pdl)
+               : filter_compact_impl((const double *)d_xy, n, index_base, nullptr, d_surv, d_count, d_ws, ws_bytes,
+                                     (void *)st, pdl);
+}
+
+ch_status pack_status(const void *d_ws, bool empty, int64_t *d_words, cudaStream_t st)
+{
+    k_pack_status<<<1, 32, 0, st>>>((const WsHeader *)d_ws, empty ? 1 : 0, (long long *)d_words);
+    return cuda_check("pack status");
+}
+
+ch_status empty_record(void *d_ext, cudaStream_t st)
+{
+    k_empty_record<<<1, 32, 0, st>>>((unsigned long long *)d_ext);
+    return cuda_check("empty record");
+}
+
+const void *ws_extremes(const void *d_ws) { return &((const WsHeader *)d_ws)->ext; }
+
+} // namespace chi

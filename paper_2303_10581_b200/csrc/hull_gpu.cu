@@ -48,7 +48,7 @@ __global__ void k_ykeys(const double *__restrict__ xy, const long long *__restri
                         unsigned long long *__restrict__ key, V *__restrict__ val)
 {
     for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x) {
-        const long long id = surv[j];
+        const long long id = surv ? surv[j] : j; // NULL: every point of xy, in order
         key[j] = okey(xy[2 * id + 1]);
         val[j] = (V)id;
     }
@@ -211,13 +211,16 @@ __global__ void k_merge_copy(long long m_cap, long long nchunks, long long W, in
 template <typename I, typename V>
 __global__ void k_assemble(long long m, const I *__restrict__ low, const long long *__restrict__ d_nl,
                            const I *__restrict__ up, const long long *__restrict__ d_nu,
-                           const V *__restrict__ val, long long *__restrict__ out, long long *__restrict__ d_nh)
+                           const V *__restrict__ val, const long long *__restrict__ idmap, long long *__restrict__ out,
+                           long long *__restrict__ d_nh)
 {
+    // idmap (nullable): the output id of sort value v is idmap[v]
+    auto id = [&](V v) { return idmap ? idmap[(long long)v] : (long long)v; };
     const long long nl = *d_nl, nu = *d_nu;
     if (nl <= 1) {
         // a single distinct point: the lowest id among all survivors
         if (blockIdx.x == 0 && threadIdx.x == 0) {
-            out[0] = (long long)val[low[0]];
+            out[0] = id(val[low[0]]);
             *d_nh = 1;
         }
         return;
@@ -226,7 +229,7 @@ __global__ void k_assemble(long long m, const I *__restrict__ low, const long lo
     if (blockIdx.x == 0 && threadIdx.x == 0)
         *d_nh = total;
     for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x)
-        out[g] = (long long)(g < a ? val[low[g]] : val[m - 1 - (long long)up[g - a]]);
+        out[g] = g < a ? id(val[low[g]]) : id(val[m - 1 - (long long)up[g - a]]);
 }
 
 // One thread per item (the bridges: not grid-stride).
@@ -333,8 +336,11 @@ struct HullTmp {
 
 // The pipeline with sort values (survivor ids) of type V.
 template <typename V>
+// surv == NULL: the hull of d_xy[0..m) itself; idmap (nullable) maps the
+// resulting point positions / ids to output ids.
 static ch_status hull_async(const double *d_xy, const long long *surv, long long m, long long *d_hull,
-                            long long *d_n_hull, void *d_tmp, const HullTmp &L, cudaStream_t st)
+                            long long *d_n_hull, void *d_tmp, const HullTmp &L, cudaStream_t st,
+                            const long long *idmap = nullptr)
 {
     char *b = (char *)d_tmp;
     auto *k0 = (unsigned long long *)(b + L.o_k0), *k1 = (unsigned long long *)(b + L.o_k1);
@@ -368,7 +374,7 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
         const long long *d_hl, *d_hu;
         const I *low = chain_gpu<I>(P, m, 0, (I *)pa, (I *)pb, la, lb, bi, bj, bi2, bj2, bi3, bj3, lm, lm2, &d_hl, st);
         const I *up = chain_gpu<I>(P, m, 1, (I *)pc, (I *)pd, lc, ld, bi, bj, bi2, bj2, bi3, bj3, lm, lm2, &d_hu, st);
-        k_assemble<I, V><<<grid_for(m, 256), 256, 0, st>>>(m, low, d_hl, up, d_hu, val, d_hull, d_n_hull);
+        k_assemble<I, V><<<grid_for(m, 256), 256, 0, st>>>(m, low, d_hl, up, d_hu, val, idmap, d_hull, d_n_hull);
     };
     if (m < (1ll << 32))
         chains((unsigned)0);
@@ -405,6 +411,28 @@ ch_status ch_hull_gpu_async(const double *d_xy, int64_t n_points, const int64_t 
                                    : hull_async<unsigned long long>(d_xy, (const long long *)d_surv, m,
                                                                     (long long *)d_hull, (long long *)d_n_hull, d_tmp,
                                                                     L, st);
+}
+
+// The hull of m points given by their coordinates d_pts (e.g. survivors
+// gathered from every rank, in increasing id order) and ids d_ids.  Same
+// canonical form; duplicates resolve to the lowest position, which is the
+// lowest id when d_ids is increasing.  Asynchronous like ch_hull_gpu_async.
+ch_status ch_hull_gpu_pts_async(const double *d_pts, const int64_t *d_ids, int64_t m, int64_t *d_hull,
+                                int64_t *d_n_hull, void *d_tmp, size_t tmp_bytes, void *stream)
+{
+    cudaStream_t st = (cudaStream_t)stream;
+    if (m < 0 || !d_n_hull || (m > 0 && (!d_pts || !d_ids || !d_hull || !d_tmp)))
+        return CH_ERR_INVALID_ARG;
+    if (m == 0)
+        return cudaMemsetAsync(d_n_hull, 0, sizeof(int64_t), st) == cudaSuccess ? CH_OK : CH_ERR_CUDA;
+    const HullTmp L(m);
+    if (tmp_bytes < L.total)
+        return CH_ERR_WORKSPACE;
+    return m <= (1ll << 32) ? hull_async<unsigned>(d_pts, nullptr, m, (long long *)d_hull, (long long *)d_n_hull,
+                                                    d_tmp, L, st, (const long long *)d_ids)
+                            : hull_async<unsigned long long>(d_pts, nullptr, m, (long long *)d_hull,
+                                                             (long long *)d_n_hull, d_tmp, L, st,
+                                                             (const long long *)d_ids);
 }
 
 // The device hull with the ids copied to h_hull (host, capacity m).

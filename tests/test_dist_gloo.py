@@ -150,3 +150,67 @@ def test_peer_exchange_failure_is_collective():
     status = [m[1] for m in msgs if m[1] != "done"]
     assert len(status) == world and all(m.startswith("unavailable") for m in status), status
     assert sum(m[1] == "done" for m in msgs) == world
+
+
+def _comm_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # the ncclUniqueId hand-off: rank 0's bytes reach every rank
+        payload = bytes(range(129)) if rank == 0 else None
+        got = chdist.broadcast_bytes(payload, 129, 0)
+        assert got == bytes(range(129)), got[:8]
+        # a status seen on one rank is raised on every rank
+        worst = chdist.agree_status(3 if rank == world - 1 else 0)
+        assert worst == 3
+        # a7's scan runs in the library (ch_exclusive_offset)
+        counts = [5, 0, 7, 11][:world]
+        assert chdist.offsets_from_counts(counts, rank) == (sum(counts[:rank]), sum(counts))
+        # without a GPU ch_comm_init fails on every rank, none hangs
+        try:
+            chdist.NcclComm(device="cuda:0")
+            q.put((rank, "created"))
+        except Exception as e:
+            q.put((rank, "failed: " + type(e).__name__))
+        dist.barrier()
+        q.put((rank, "done"))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_nccl_comm_host_logic_world(world):
+    """The host side of the library-owned NCCL communicator over gloo on CPU:
+    unique-id broadcast, status agreement, the scan, and a collective failure
+    of ch_comm_init when there is no GPU."""
+    if torch.cuda.is_available():
+        pytest.skip("needs a machine without a GPU")
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    msgs = [q.get(timeout=120) for _ in range(2 * world)]
+    for p_ in procs:
+        p_.join(timeout=60)
+    status = [m[1] for m in msgs if m[1] != "done"]
+    assert len(status) == world and all(m.startswith("failed") for m in status), status
+
+
+def test_exclusive_offset_abi():
+    import ctypes
+    from paper_2303_10581_b200 import _lib
+    lib = _lib.load()
+    c = np.array([3, 0, 9, 2], dtype=np.int64)
+    o, t = ctypes.c_int64(0), ctypes.c_int64(0)
+    for r in range(4):
+        assert lib.ch_exclusive_offset(c.ctypes.data_as(ctypes.c_void_p), 4, r, ctypes.byref(o), ctypes.byref(t)) == 0
+        assert (o.value, t.value) == (int(c[:r].sum()), 14)
+    assert lib.ch_exclusive_offset(c.ctypes.data_as(ctypes.c_void_p), 4, 4, None, None) == 1
+    bad = np.array([1, -1], dtype=np.int64)
+    assert lib.ch_exclusive_offset(bad.ctypes.data_as(ctypes.c_void_p), 2, 0, None, None) == 1

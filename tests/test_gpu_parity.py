@@ -446,7 +446,7 @@ def _dist_worker(rank, world, port, n, dist_name, storage, q):
         xy = synth.points(dist_name, n, seed=4, device="cuda", lo=lo, hi=hi)
         if storage == "f32":
             xy = xy.float()
-        df = chdist.DistFilter(n, xy)
+        df = chdist.DistFilter(n, xy, exchange="torch")
         df.step()
         loc, off, total = df.result()
         q.put((rank, lo, hi, off, total, loc.cpu().numpy()))
