@@ -251,6 +251,11 @@ def run_ours(a):
     # the sharded path: N > 1, or an explicit --exchange (also at N = 1, to
     # run the distributed step's code on one GPU)
     multi = world > 1 or a.exchange != "auto"
+    # stdout carries exactly one JSON line: NCCL's own messages (e.g. its
+    # version banner when the environment sets NCCL_DEBUG=VERSION) go to stderr
+    if "CH_KEEP_NCCL_DEBUG" not in os.environ:
+        os.environ["NCCL_DEBUG"] = "WARN"
+        os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
     # CH_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo collectives -- only
     # to exercise the N > 1 code path on a 1-GPU box; never a measurement.
     share = os.environ.get("CH_BENCH_SHARE_GPU") == "1"

@@ -46,7 +46,7 @@ def test_workspace_octagon_reused_on_other_points():
     edge = near_edge_points(rng, V, 50_000, ulps=3)
     b = np.concatenate([inner, far, edge, an[100_000:150_000] * 3.0])
     bd = torch.tensor(b, device=DEV)
-    ws = chf.Workspace(len(b))
+    ws = chf.Workspace(max(len(b), a.shape[0]))
     for storage in ("f64", "f32"):
         aa = a if storage == "f64" else a.float()
         bb = bd if storage == "f64" else bd.float()
