@@ -46,7 +46,8 @@
 extern "C" {
 #endif
 
-#define CH_ABI_VERSION 2 /* 2: ch_comm_* (NCCL), ch_gather_survivors, ch_peer_counts with offsets, ch_stats pass times */
+#define CH_ABI_VERSION 3 /* 2: ch_comm_* (NCCL), ch_gather_survivors, ch_peer_counts with offsets, ch_stats pass times;
+                            3: ch_octagon's fp32 certificate as scaled edges with one keep bound */
 
 typedef enum {
     CH_OK = 0,
@@ -91,10 +92,12 @@ typedef struct {
  * the corners bound it); points inside it are discarded without edge tests.
  * It never changes a result.  guess_edge/cx/cy: the octant of (x-cx, y-cy)
  * picks the edge tested first (a pure speed hint).
- * f32_*: an fp32 pre-filter per edge with a static error bound (DESIGN.md
- * "fp32 certification"): g = fma(a, fl32(x), fma(b, fl32(y), cin)) >= 0
- * proves D_k > thr[k]; h = fma(a, fl32(x), fma(b, fl32(y), cout)) <= -0
- * proves D_k < thr[k]; otherwise D_k is evaluated in fp64.  Valid only for
+ * f32_*: an fp32 pre-filter with static error bounds (DESIGN.md "fp32
+ * certification"), edge k scaled by an exact power of two 2^s_k so that
+ * max(|a|, |b|) is in [1, 2): v_k = fma(a, fl32(x), fma(b, fl32(y), c)) >= 0
+ * proves D_k > thr[k], v_k < -f32_dk[k] proves D_k < thr[k] (CH_EXACT:
+ * < -thr[k]); with G = min_k v_k, G >= 0 proves the point is discarded and
+ * G + f32_delta < 0 that it is kept; otherwise D_k is evaluated in fp64.  Valid only for
  * points inside bbox, so the kernels use it only with octagons they built
  * themselves from the same points (has_f32 is cleared on a caller-supplied
  * octagon; a workspace octagon is tagged with the (pointer, n, index_base) it
@@ -116,7 +119,9 @@ typedef struct {
     int32_t plain;     /* 1 if built with CH_PLAIN                       */
     int32_t guess_edge[8];
     double cx, cy;
-    float f32_a[8], f32_b[8], f32_cin[8], f32_cout[8];
+    float f32_a[8], f32_b[8], f32_c[8]; /* fp32 certificate of edge k scaled by 2^s_k */
+    float f32_dk[8];   /* edge k's keep bound (scaled)                   */
+    float f32_delta;   /* max over the edges of f32_dk                   */
     int32_t has_f32;
     int32_t exact;     /* 1 if built with CH_EXACT                       */
 } ch_octagon;

@@ -18,7 +18,7 @@ SZ = ctypes.c_size_t
 
 CH_OK, CH_ERR_INVALID_ARG, CH_ERR_EMPTY, CH_ERR_NONFINITE = 0, 1, 2, 3
 CH_ERR_MISALIGNED, CH_ERR_WORKSPACE, CH_ERR_CUDA, CH_ERR_PEER, CH_ERR_NCCL = 4, 5, 6, 7, 8
-ABI_VERSION = 2
+ABI_VERSION = 3
 CH_NCCL_ID_BYTES = 128
 CH_MAX_PEERS = 16
 CH_CERTIFIED, CH_PLAIN, CH_EXACT = 0, 1, 2
@@ -35,8 +35,8 @@ class Octagon(ctypes.Structure):
         ("vx", DBL * 8), ("vy", DBL * 8), ("ex", DBL * 8), ("ey", DBL * 8), ("thr", DBL * 8),
         ("bbox", DBL * 4), ("box", DBL * 4), ("has_box", I32), ("plain", I32),
         ("guess_edge", I32 * 8), ("cx", DBL), ("cy", DBL),
-        ("f32_a", ctypes.c_float * 8), ("f32_b", ctypes.c_float * 8), ("f32_cin", ctypes.c_float * 8),
-        ("f32_cout", ctypes.c_float * 8), ("has_f32", I32), ("exact", I32),
+        ("f32_a", ctypes.c_float * 8), ("f32_b", ctypes.c_float * 8), ("f32_c", ctypes.c_float * 8),
+        ("f32_dk", ctypes.c_float * 8), ("f32_delta", ctypes.c_float), ("has_f32", I32), ("exact", I32),
     ]
 
 

@@ -535,7 +535,7 @@ __device__ __forceinline__ void octagon_vertices_warp(const ch_extremes &e, int 
             o.vx[k] = o.vy[k] = 0.0;
         }
         o.ex[k] = o.ey[k] = o.thr[k] = 0.0;
-        o.f32_a[k] = o.f32_b[k] = o.f32_cin[k] = o.f32_cout[k] = 0.0f;
+        o.f32_a[k] = o.f32_b[k] = o.f32_c[k] = o.f32_dk[k] = 0.0f;
         const int sv = __popc(mask & ((2u << k) - 1u)) - 1; // slot k's kept vertex
         o.guess_edge[k] = (!degenerate && sv < nv) ? sv : 0;
     }
@@ -546,6 +546,7 @@ __device__ __forceinline__ void octagon_vertices_warp(const ch_extremes &e, int 
         o.plain = (flags & CH_PLAIN) ? 1 : 0;
         o.exact = (!o.plain && (flags & CH_EXACT)) ? 1 : 0;
         o.has_f32 = 0;
+        o.f32_delta = 0.0f;
         o.bbox[0] = e.x[4]; // xmin (L)
         o.bbox[1] = e.x[0]; // xmax (R)
         o.bbox[2] = e.y[6]; // ymin (B)
@@ -613,6 +614,7 @@ __device__ void build_octagon_cta(const ch_extremes &e, int flags, ch_octagon &o
             o.has_box = 1;
         }
     } else if (tid == 32) { // (another warp: runs alongside the pick)
+        chf::octagon_f32_delta(o);
         o.has_f32 = chf::f32_domain_ok(o) ? 1 : 0;
     }
     __syncthreads();
@@ -925,8 +927,9 @@ struct __align__(16) SEdge { // 48 B: lanes indexing different edges hit distinc
 };
 struct SOct {
     SEdge e[8];
-    float4 fab[8]; // {a, a, b, b}: edge k's fp32 coefficients as FFMA2 operand pairs
-    float4 fc[8];  // {cin, cin, cout, cout}
+    float4 fab[8]; // {a, a, b, b}: edge k's (scaled) fp32 coefficients as FFMA2 operand pairs
+    float2 fc[8];  // {c, c}; edges k >= nv: a = b = 0, c = 2^100 (never the minimum)
+    unsigned long long fdelta; // {f32_delta, f32_delta}
     unsigned long long nbx0, bx1, nby0, by1; // float storage, as f32x2 pairs: (-boxf[0], -boxf[0]), (boxf[1], boxf[1]), ...
     double box[4];
     float boxf[4]; // float bounds with x >= boxf[0] <=> (double)x >= box[0], etc.
@@ -948,8 +951,11 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.e[t].thr = o->thr[t];
         s.e[t].pad = 0.0;
         s.guess[t] = o->guess_edge[t];
-        s.fab[t] = make_float4(o->f32_a[t], o->f32_a[t], o->f32_b[t], o->f32_b[t]);
-        s.fc[t] = make_float4(o->f32_cin[t], o->f32_cin[t], o->f32_cout[t], o->f32_cout[t]);
+        const bool used = t < o->nv;
+        const float a = used ? o->f32_a[t] : 0.0f, b = used ? o->f32_b[t] : 0.0f;
+        const float c = used ? o->f32_c[t] : 0x1p100f;
+        s.fab[t] = make_float4(a, a, b, b);
+        s.fc[t] = make_float2(c, c);
     } else if (t < 12) { // one float bound of the accept box each (threads 8..11)
         const int j = t - 8;
         const double bj = o->box[j];
@@ -973,6 +979,7 @@ __device__ __forceinline__ void load_soct(SOct &s, const ch_octagon *__restrict_
         s.degenerate = o->degenerate;
         s.has_f32 = f32_ok ? o->has_f32 : 0;
         s.exact = o->exact;
+        s.fdelta = ((unsigned long long)__float_as_uint(o->f32_delta) << 32) | __float_as_uint(o->f32_delta);
     }
 }
 
@@ -1141,34 +1148,45 @@ __device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b)
     return d;
 }
 
-// OR of the sign bits of the fp32 certificate values over the octagon's
-// edges, two points per FFMA2 (sg[q] bit 31: point 2q, bit 63: point 2q+1):
-// IN = g_k = fma(a, x, fma(b, y, cin)) (inside certificate), else h_k with
-// cout (keep certificate) -- the same correctly rounded fma chain as the
-// scalar proof at chf::octagon_edge.  Edge-outer, so each edge's constants
-// load once per pass; nv == 8 (the usual case) is fully unrolled.
-template <bool IN, int NQ>
-__device__ __forceinline__ void sign_or(const SOct &s, int nv, const f32x2 (&X)[NQ], const f32x2 (&Y)[NQ],
-                                        f32x2 (&sg)[NQ])
+__device__ __forceinline__ void unpk2(f32x2 v, float &lo, float &hi)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ float fmin3(float a, float b, float c) // FMNMX3 (sm_100)
+{
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ bool sign_lo(f32x2 v) { return (int)(unsigned)v < 0; }
+__device__ __forceinline__ bool sign_hi(f32x2 v) { return (int)(unsigned)(v >> 32) < 0; }
+
+// G = min over the 8 edge slots of the certificate values v_k =
+// fma(a_k, x, fma(b_k, y, c_k)) (scaled edges, chf::octagon_edge), two
+// points per FFMA2 and two edges per FMNMX3; the unused slots (k >= nv) give
+// 2^100.  glo / ghi: G of points 2q and 2q + 1.
+template <int NQ>
+__device__ __forceinline__ void cert_min(const SOct &s, const f32x2 (&X)[NQ], const f32x2 (&Y)[NQ],
+                                         float (&glo)[NQ], float (&ghi)[NQ])
 {
 #pragma unroll
-    for (int q = 0; q < NQ; q++)
-        sg[q] = 0ull;
-    auto edge = [&](int k) {
-        const f32x2 *e = (const f32x2 *)&s.fab[k];
-        const f32x2 a = e[0], b = e[1];
-        const f32x2 c = ((const f32x2 *)&s.fc[k])[IN ? 0 : 1];
+    for (int k = 0; k < 8; k += 2) {
+        const f32x2 *e0 = (const f32x2 *)&s.fab[k], *e1 = (const f32x2 *)&s.fab[k + 1];
+        const f32x2 a0 = e0[0], b0 = e0[1], a1 = e1[0], b1 = e1[1];
+        const f32x2 c0 = *(const f32x2 *)&s.fc[k], c1 = *(const f32x2 *)&s.fc[k + 1];
 #pragma unroll
-        for (int q = 0; q < NQ; q++)
-            sg[q] |= ffma2(a, X[q], ffma2(b, Y[q], c));
-    };
-    if (nv == 8) {
-#pragma unroll
-        for (int k = 0; k < 8; k++)
-            edge(k);
-    } else {
-        for (int k = 0; k < nv; k++)
-            edge(k);
+        for (int q = 0; q < NQ; q++) {
+            float l0, h0, l1, h1;
+            unpk2(ffma2(a0, X[q], ffma2(b0, Y[q], c0)), l0, h0);
+            unpk2(ffma2(a1, X[q], ffma2(b1, Y[q], c1)), l1, h1);
+            if (k == 0) {
+                glo[q] = fminf(l0, l1);
+                ghi[q] = fminf(h0, h1);
+            } else {
+                glo[q] = fmin3(glo[q], l0, l1);
+                ghi[q] = fmin3(ghi[q], h0, h1);
+            }
+        }
     }
 }
 
@@ -1178,13 +1196,13 @@ __device__ __forceinline__ void sign_or(const SOct &s, int nv, const f32x2 (&X)[
 // mw[u * K2_CWARPS] (lane 0), bit-identical to "not (forall k: D_k > T_k)"
 // (R4).  Every stage is a certificate proven on its own (box:
 // chf::box_corner_ok; fp32: chf::octagon_edge), so the order cannot change a
-// result.  Per-point state is a sign bit, combined by LOP3; the warp-uniform
-// skips are one vote per pass:
+// result.  Per-point state is a sign bit; the warp-uniform skips are one
+// vote per pass:
 //  1. the accept box: inside => discarded.  A pass whose points are all
 //     inside is done (normal data);
-//  2. keep certificate on any edge: some h_k <= -0 (circle-like data);
-//  3. if some point is still open: inside certificate, all g_k >= +0;
-//  4. fp64 D_k on every edge for points in neither (the ~1e-7 band), the
+//  2. G = min_k v_k over the scaled edges: G >= +0 => discarded (inside
+//     every edge), G + f32_delta < 0 => kept (outside some edge);
+//  3. fp64 D_k on every edge for the points in neither (the ~1e-7 band), the
 //     coordinates re-read from the stage.
 template <typename T, int NP>
 __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTraits<T>::V2 *sp, unsigned *mw)
@@ -1194,7 +1212,6 @@ __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTra
     constexpr f32x2 SIGN2 = 0x8000000080000000ull;
     const int tid = threadIdx.x;
     const bool lane0 = (tid & 31) == 0;
-    const int nv = s.nv;
 #pragma unroll
     for (int h0 = 0; h0 < NP; h0 += H) {
         f32x2 X[HQ], Y[HQ]; // x (resp. y) of points (2q, 2q + 1) of the pass
@@ -1247,50 +1264,44 @@ __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTra
                     mw[(h0 + i) * K2_CWARPS] = 0u;
             continue;
         }
-        f32x2 keep[HQ], sg[HQ];
-        sign_or<false, HQ>(s, nv, X, Y, sg); // 2. keep certificate
-        f32x2 open = 0;
+        float glo[HQ], ghi[HQ];
+        cert_min<HQ>(s, X, Y, glo, ghi);
+        f32x2 keep[HQ], band = 0;
 #pragma unroll
         for (int q = 0; q < HQ; q++) {
-            keep[q] = ob[q] & sg[q];
-            open |= ob[q] & ~sg[q];
+            const f32x2 G = pk2(glo[q], ghi[q]);
+            const f32x2 t = fadd2(G, s.fdelta); // sign: G + delta < 0, certified kept
+            keep[q] = ob[q] & t & SIGN2;
+            ob[q] &= ~t & G & SIGN2; // the band: outside the box, neither certificate
+            band |= ob[q];
         }
-        if (__any_sync(FULL, open != 0ull)) {
-            sign_or<true, HQ>(s, nv, X, Y, sg); // 3. inside certificate
-            f32x2 band = 0;
+        if (__any_sync(FULL, band != 0ull)) {
+            // 3. fp64 on every edge for the band points (rare)
 #pragma unroll
-            for (int q = 0; q < HQ; q++) {
-                sg[q] = ob[q] & ~keep[q] & sg[q]; // open and not certified inside
-                band |= sg[q];
-            }
-            if (__any_sync(FULL, band != 0ull)) {
-                // 4. fp64 on every edge for the band points (rare)
-#pragma unroll
-                for (int i = 0; i < H; i++) {
-                    if ((sg[i / 2] >> (32 * (i & 1) + 31)) & 1ull) {
-                        double x, y;
-                        if constexpr (sizeof(T) == 8) {
-                            // re-read (volatile: the doubles must not stay live across the pass)
-                            const volatile double *vp = (const volatile double *)(sp + (h0 + i) * K2_CTHREADS + tid);
-                            x = vp[0];
-                            y = vp[1];
-                        } else {
-                            const auto v = sp[(h0 + i) * K2_CTHREADS + tid];
-                            x = v.x;
-                            y = v.y;
-                        }
-                        bool kf = false;
-                        for (int k = 0; k < nv && !kf; k++)
-                            kf = !edge_inside(s, k, s.exact, x, y);
-                        if (kf)
-                            keep[i / 2] |= 1ull << (32 * (i & 1) + 31);
+            for (int i = 0; i < H; i++) {
+                if ((i & 1) ? sign_hi(ob[i / 2]) : sign_lo(ob[i / 2])) {
+                    double x, y;
+                    if constexpr (sizeof(T) == 8) {
+                        // re-read (volatile: the doubles must not stay live across the pass)
+                        const volatile double *vp = (const volatile double *)(sp + (h0 + i) * K2_CTHREADS + tid);
+                        x = vp[0];
+                        y = vp[1];
+                    } else {
+                        const auto v = sp[(h0 + i) * K2_CTHREADS + tid];
+                        x = v.x;
+                        y = v.y;
                     }
+                    bool kf = false;
+                    for (int k = 0; k < s.nv && !kf; k++)
+                        kf = !edge_inside(s, k, s.exact, x, y);
+                    if (kf)
+                        keep[i / 2] |= (i & 1) ? 0x8000000000000000ull : 0x80000000ull;
                 }
             }
         }
 #pragma unroll
         for (int i = 0; i < H; i++) {
-            const unsigned m = __ballot_sync(FULL, (keep[i / 2] >> (32 * (i & 1) + 31)) & 1ull);
+            const unsigned m = __ballot_sync(FULL, (i & 1) ? sign_hi(keep[i / 2]) : sign_lo(keep[i / 2]));
             if (lane0)
                 mw[(h0 + i) * K2_CWARPS] = m;
         }

@@ -24,6 +24,8 @@
 #define CH_INF (__longlong_as_double(0x7ff0000000000000LL))
 #define CH_F32(v) __double2float_rn(v)
 #define CH_NEXTF(a, b) nextafterf((a), (b))
+#define CH_D2LL(v) __double_as_longlong(v)
+#define CH_LL2D(v) __longlong_as_double(v)
 #else
 #define CH_HD inline
 #define CH_ADD(a, b) ((a) + (b))
@@ -32,6 +34,11 @@
 #define CH_INF (__builtin_inf())
 #define CH_F32(v) ((float)(v))
 #define CH_NEXTF(a, b) __builtin_nextafterf((a), (b))
+#define CH_D2LL(v) chf_d2ll(v)
+#define CH_LL2D(v) chf_ll2d(v)
+#include <string.h>
+static inline long long chf_d2ll(double v) { long long r; memcpy(&r, &v, 8); return r; }
+static inline double chf_ll2d(long long v) { double r; memcpy(&r, &v, 8); return r; }
 #endif
 
 namespace chf {
@@ -72,21 +79,35 @@ CH_HD float f32_down(double v)
 
 // fp32 certification of the edge predicate,
 // computed per edge in octagon_edge().
-// For a point inside the bounding box let E = a x + b y + c exactly, with
-// a = -ey, b = ex, c = ey ax - ex ay (ex, ey, ax, ay the stored doubles), so
-// E = ex (y - ay) - ey (x - ax).  Then (eps = 2^-53, u = 2^-24):
-//   |D_k - E| <= 3.001 eps S_k                           (five fp64 roundings)
-//   g = fma32(fl32(a), fl32(x), fma32(fl32(b), fl32(y), cin))
-//   |g - (a x + b y + cin)| <= 4.001 u (|a| Xm + |b| Ym + |cin|)
+// Edge k is first scaled by sigma = 2^s (s = -ilogb(max(|ex|, |ey|)), clamped
+// to [-100, 100]), exactly: ex' = sigma ex, ey' = sigma ey, T' = sigma T,
+// S' = sigma S.  For a point inside the bounding box let
+// E' = a x + b y + c exactly, with a = -ey', b = ex', c = ey' ax - ex' ay, so
+// E' = sigma (ex (y - ay) - ey (x - ax)).  Then (eps = 2^-53, u = 2^-24):
+//   |sigma D_k - E'| <= 3.001 eps S'                     (five fp64 roundings)
+//   v = fma32(fl32(a), fl32(x), fma32(fl32(b), fl32(y), cin))
+//   |v - (a x + b y + cin)| <= 4.001 u (|a| Xm + |b| Ym + |cin|)
 // (Xm, Ym: largest |x|, |y| in the box).  cin is rounded DOWN from
-// fl(c) - T_k - M_k with M_k = 8 u (B0 + C + |T_k|) + 4 eps S_k + 2^-100,
-// B0 = |a| Xm + |b| Ym, C = |ey ax| + |ex ay| (>= |c| and bounding fl(c)'s
-// error by 3 eps C).  So c - T_k - cin >= M_k - 3 eps C, which exceeds
-// 4.001 u (B0 + |cin|) + 3.001 eps S_k, and g >= 0 implies E - T_k >
-// 3.001 eps S_k, i.e. D_k > T_k.  Symmetrically cout is rounded UP from
-// fl(c) - T_k + M_k and h <= 0 implies D_k < T_k.  The 2^-100 slack covers
-// fp32 subnormal roundings.  Enabled only when the box lies within
-// [-2^40, 2^40]^2 (no fp32 overflow).
+// fl(c) - T' - M with M = 8 u (B0 + C + |T'|) + 4 eps S' + 2^-100,
+// B0 = |a| Xm + |b| Ym, C = |ey' ax| + |ex' ay| (>= |c| and bounding fl(c)'s
+// error by 3 eps C).  So c - T' - cin >= M - 3 eps C, which exceeds
+// 4.001 u (B0 + |cin|) + 3.001 eps S', and v >= 0 implies E' - T' >
+// 3.001 eps S', i.e. D_k > T_k (inside certificate).  The 2^-100 slack
+// covers fp32 subnormal roundings (|a|, |b| < 2 after scaling) and sigma
+// times the fp64 ones (|s| <= 100).
+// Keep certificate from the SAME value v: sigma D_k <= v + (fl(c) - cin)
+// + 3 eps C + 4.001 u (B0 + |cin|) + 3.001 eps S', so v < -dk with
+// dk >= (fl(c) - cin - T'') + 3 eps C + 4.001 u (B0 + |cin|) + 3.001 eps S'
+// implies D_k < T'' / sigma, where T'' = T' (certified, plain: the point is
+// kept) or -T' (exact mode: the exact orientation is negative, R4's bound).
+// dk is evaluated in fp64 with 5 u, 4 eps S', an extra 16 eps (C + |T'| +
+// |cin|) for the fp64 roundings of the sum, 2^-100, a factor 1 + 2^-20, and
+// rounded UP to fp32.  The scaling makes |a|, |b| of every edge comparable,
+// so one bound f32_delta = max_k dk serves all edges: with
+// G = min_k v_k, "G >= 0" proves the point is discarded and
+// "G + f32_delta < 0" proves it is kept (v_k = G < -f32_delta <= -dk_k for
+// the minimising k).  Enabled only when the box lies within [-2^40, 2^40]^2
+// (no fp32 overflow).
 CH_HD bool f32_domain_ok(const ch_octagon &o)
 {
     const double Xm = dmax(dabs(o.bbox[0]), dabs(o.bbox[1]));
@@ -94,9 +115,8 @@ CH_HD bool f32_domain_ok(const ch_octagon &o)
     return !o.degenerate && Xm <= 0x1p40 && Ym <= 0x1p40;
 }
 
-// Edge k of an octagon whose vertices and bbox are set: ex, ey, T_k (R4)
-// and the fp32 pre-filter constants.
-// ex, ey, S_k and T_k of edge k (R4), from the vertices and the bbox only.
+// Edge k of an octagon whose vertices and bbox are set: ex, ey, S_k, T_k (R4)
+// from the vertices and the bbox only.
 CH_HD void edge_core(const ch_octagon &o, int k, double &ex, double &ey, double &S, double &T)
 {
     const int k1 = (k + 1 == o.nv) ? 0 : k + 1;
@@ -109,6 +129,18 @@ CH_HD void edge_core(const ch_octagon &o, int k, double &ex, double &ey, double 
     T = o.plain ? 0.0 : CH_MUL(S, 0x1p-50); // exact power-of-two scaling
 }
 
+// 2^s with s = -(binary exponent of m), clamped to [-100, 100]; 1 for
+// m == 0.  From the exponent field (a subnormal m reads as 2^-1023, then
+// clamps), so host and device agree exactly.
+CH_HD double edge_scale(double m)
+{
+    if (!(m > 0.0))
+        return 1.0;
+    int e = (int)((CH_D2LL(m) >> 52) & 0x7ff) - 1023;
+    e = e < -100 ? -100 : (e > 100 ? 100 : e);
+    return CH_LL2D((long long)(1023 - e) << 52);
+}
+
 CH_HD void octagon_edge(ch_octagon &o, int k)
 {
     const double ax = o.vx[k], ay = o.vy[k];
@@ -117,23 +149,39 @@ CH_HD void octagon_edge(ch_octagon &o, int k)
     o.ex[k] = ex;
     o.ey[k] = ey;
     o.thr[k] = T;
-    // fp32 pre-filter constants (used only if f32_domain_ok)
+    // fp32 certificate constants (used only if f32_domain_ok), on the edge
+    // scaled by sigma (exact power-of-two products)
+    const double sg = edge_scale(dmax(dabs(ex), dabs(ey)));
+    const double sex = CH_MUL(ex, sg), sey = CH_MUL(ey, sg), sT = CH_MUL(T, sg), sS = CH_MUL(S, sg);
     const double Xm = dmax(dabs(o.bbox[0]), dabs(o.bbox[1]));
     const double Ym = dmax(dabs(o.bbox[2]), dabs(o.bbox[3]));
-    const double c = CH_SUB(CH_MUL(ey, ax), CH_MUL(ex, ay));
-    const double C = CH_ADD(dabs(CH_MUL(ey, ax)), dabs(CH_MUL(ex, ay)));
-    const double B0 = CH_ADD(CH_MUL(dabs(ey), Xm), CH_MUL(dabs(ex), Ym));
-    // 1 + 2^-20 absorbs the roundings of this fp64 bound computation
-    const double M = CH_MUL(CH_ADD(CH_ADD(CH_MUL(CH_ADD(CH_ADD(B0, C), dabs(T)), 8.0 * 0x1p-24),
-                                          CH_MUL(S, 4.0 * 0x1p-53)),
+    const double c = CH_SUB(CH_MUL(sey, ax), CH_MUL(sex, ay));
+    const double C = CH_ADD(dabs(CH_MUL(sey, ax)), dabs(CH_MUL(sex, ay)));
+    const double B0 = CH_ADD(CH_MUL(dabs(sey), Xm), CH_MUL(dabs(sex), Ym));
+    // 1 + 2^-20 absorbs the roundings of these fp64 bound computations
+    const double M = CH_MUL(CH_ADD(CH_ADD(CH_MUL(CH_ADD(CH_ADD(B0, C), dabs(sT)), 8.0 * 0x1p-24),
+                                          CH_MUL(sS, 4.0 * 0x1p-53)),
                                    0x1p-100),
                             1.0 + 0x1p-20);
-    o.f32_a[k] = CH_F32(-ey);
-    o.f32_b[k] = CH_F32(ex);
-    o.f32_cin[k] = f32_down(CH_SUB(CH_SUB(c, T), M));
-    // keep-certificate: h <= 0 proves D_k < T_k; in exact mode it must prove
-    // D_k < -T_k (then the exact orientation is negative, R4's bound)
-    o.f32_cout[k] = f32_up(CH_ADD(CH_SUB(c, o.exact ? -T : T), M));
+    const float cin = f32_down(CH_SUB(CH_SUB(c, sT), M));
+    o.f32_a[k] = CH_F32(-sey);
+    o.f32_b[k] = CH_F32(sex);
+    o.f32_c[k] = cin;
+    const double acin = dabs((double)cin);
+    const double d1 = CH_SUB(CH_SUB(c, (double)cin), o.exact ? -sT : sT);
+    const double err = CH_ADD(CH_ADD(CH_ADD(CH_MUL(C, 3.0 * 0x1p-53), CH_MUL(CH_ADD(B0, acin), 5.0 * 0x1p-24)),
+                                     CH_MUL(sS, 4.0 * 0x1p-53)),
+                              CH_MUL(CH_ADD(CH_ADD(C, dabs(sT)), acin), 16.0 * 0x1p-53));
+    o.f32_dk[k] = f32_up(CH_MUL(CH_ADD(CH_ADD(dmax(d1, 0.0), err), 0x1p-100), 1.0 + 0x1p-20));
+}
+
+// The common keep bound (after every edge is set).
+CH_HD void octagon_f32_delta(ch_octagon &o)
+{
+    float d = 0.0f;
+    for (int k = 0; k < o.nv; k++)
+        d = o.f32_dk[k] > d ? o.f32_dk[k] : d;
+    o.f32_delta = d;
 }
 
 // Octagon assembly (DESIGN R5), vertex part: cycle [R,TR,T,TL,L,BL,B,BR];
@@ -152,9 +200,10 @@ CH_HD void octagon_vertices(const ch_extremes &e, int flags, ch_octagon &o)
         o.vidx[k] = -1;
         o.vx[k] = o.vy[k] = o.ex[k] = o.ey[k] = o.thr[k] = 0.0;
         o.guess_edge[k] = 0;
-        o.f32_a[k] = o.f32_b[k] = o.f32_cin[k] = o.f32_cout[k] = 0.0f;
+        o.f32_a[k] = o.f32_b[k] = o.f32_c[k] = o.f32_dk[k] = 0.0f;
     }
     o.has_f32 = 0;
+    o.f32_delta = 0.0f;
     for (int k = 0; k < 8; k++) {
         double x = e.x[k], y = e.y[k];
         if (!(o.nv > 0 && x == o.vx[o.nv - 1] && y == o.vy[o.nv - 1])) {
@@ -241,6 +290,7 @@ CH_HD void build_octagon(const ch_extremes &e, int flags, ch_octagon &o)
         return;
     for (int k = 0; k < o.nv; k++)
         octagon_edge(o, k);
+    octagon_f32_delta(o);
     o.has_f32 = f32_domain_ok(o) ? 1 : 0;
     for (int t = 0; t < BOX_CANDIDATES; t++) {
         double b[4];

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for name in names:
         assert hasattr(lib, name), name
         assert name in chf._lib.SIGNATURES, name
-    assert lib.ch_abi_version() == chf._lib.ABI_VERSION == 2
+    assert lib.ch_abi_version() == chf._lib.ABI_VERSION == 3
 
 
 def test_library_is_sm100a():
