@@ -53,6 +53,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef CH_K2_MINB
 #define CH_K2_MINB 2 // K2 resident CTAs per SM the registers are sized for
 #endif
+#ifndef CH_K2_BOX
+#define CH_K2_BOX 1 // K2 accept-box stage: 0 never (certificates only), 1 adaptive
+#endif
 #ifndef CH_CERT_H
 #define CH_CERT_H 8 // points per consume_cert pass
 #endif
@@ -1204,8 +1207,9 @@ __device__ __forceinline__ void cert_min(const SOct &s, const f32x2 (&X)[NQ], co
 //     every edge), G + f32_delta < 0 => kept (outside some edge);
 //  3. fp64 D_k on every edge for the points in neither (the ~1e-7 band), the
 //     coordinates re-read from the stage.
-template <typename T, int NP>
-__device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTraits<T>::V2 *sp, unsigned *mw)
+template <typename T, int NP, bool USE_BOX>
+__device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTraits<T>::V2 *sp, unsigned *mw,
+                                             int &box_mode)
 {
     constexpr int H = CH_CERT_H < NP ? CH_CERT_H : NP; // points per pass (register budget)
     constexpr int HQ = H / 2;
@@ -1217,6 +1221,7 @@ __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTra
         f32x2 X[HQ], Y[HQ]; // x (resp. y) of points (2q, 2q + 1) of the pass
         f32x2 ob[HQ];       // sign bits: outside the accept box
         f32x2 anyout = 0;
+        constexpr bool use_box = USE_BOX;
         // Outside the accept box <=> a sign bit among x - x0, x1 - x, y - y0,
         // y1 - y: an RNE difference has the sign of the exact one and is +0
         // when equal (the same decision as x >= x0 && ... on finite input).
@@ -1228,10 +1233,14 @@ __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTra
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
                     const double2 v = sp[(h0 + 2 * q + h) * K2_CTHREADS + tid];
-                    const double t0 = __dsub_rn(v.x, s.box[0]), t1 = __dsub_rn(s.box[1], v.x);
-                    const double t2 = __dsub_rn(v.y, s.box[2]), t3 = __dsub_rn(s.box[3], v.y);
-                    o[h] = (__double2hiint(t0) | __double2hiint(t1) | __double2hiint(t2) | __double2hiint(t3)) &
-                           0x80000000u;
+                    if (use_box) {
+                        const double t0 = __dsub_rn(v.x, s.box[0]), t1 = __dsub_rn(s.box[1], v.x);
+                        const double t2 = __dsub_rn(v.y, s.box[2]), t3 = __dsub_rn(s.box[3], v.y);
+                        o[h] = (__double2hiint(t0) | __double2hiint(t1) | __double2hiint(t2) |
+                                __double2hiint(t3)) & 0x80000000u;
+                    } else {
+                        o[h] = 0x80000000u;
+                    }
                     fx[h] = (float)v.x;
                     fy[h] = (float)v.y;
                 }
@@ -1252,20 +1261,41 @@ __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTra
                 // register allocator then keeps whole)
                 X[q] = fmul2(pk2(lds_f32(a0), lds_f32(a1)), ONE2);
                 Y[q] = fmul2(pk2(lds_f32(a0 + 4), lds_f32(a1 + 4)), ONE2);
-                ob[q] = (fadd2(X[q], s.nbx0) | ffma2(m1, X[q], s.bx1) | fadd2(Y[q], s.nby0) |
-                         ffma2(m1, Y[q], s.by1)) & SIGN2;
+                if (use_box)
+                    ob[q] = (fadd2(X[q], s.nbx0) | ffma2(m1, X[q], s.bx1) | fadd2(Y[q], s.nby0) |
+                             ffma2(m1, Y[q], s.by1)) & SIGN2;
+                else
+                    ob[q] = SIGN2;
                 anyout |= ob[q];
             }
         }
-        if (!__any_sync(FULL, anyout != 0ull)) {
+        if (use_box) {
+            const int nout = __popc(__ballot_sync(FULL, anyout != 0ull));
+            if (nout >= 8)
+                box_mode = 64;
+            if (nout == 0) {
 #pragma unroll
-            for (int i = 0; i < H; i++)
-                if (lane0)
-                    mw[(h0 + i) * K2_CWARPS] = 0u;
-            continue;
+                for (int i = 0; i < H; i++)
+                    if (lane0)
+                        mw[(h0 + i) * K2_CWARPS] = 0u;
+                continue;
+            }
         }
         float glo[HQ], ghi[HQ];
         cert_min<HQ>(s, X, Y, glo, ghi);
+        if constexpr (!USE_BOX) { // every point certified inside (G >= +0): all discarded
+            unsigned neg = 0;
+#pragma unroll
+            for (int q = 0; q < HQ; q++)
+                neg |= __float_as_uint(glo[q]) | __float_as_uint(ghi[q]);
+            if (!__any_sync(FULL, (int)neg < 0)) {
+#pragma unroll
+                for (int i = 0; i < H; i++)
+                    if (lane0)
+                        mw[(h0 + i) * K2_CWARPS] = 0u;
+                continue;
+            }
+        }
         f32x2 keep[HQ], band = 0;
 #pragma unroll
         for (int q = 0; q < HQ; q++) {
@@ -1515,6 +1545,7 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
         };
         int b = 0, uses0 = 0, uses1 = 0;
         int guess_mode = 0; // adaptive: see classify()
+        int box_mode = 0;   // adaptive: see consume_cert()
         for (unsigned seq = 0;; seq++) {
             const int st = (int)(seq % K2_STAGES);
             mbar_wait(&s_full[st], (seq / K2_STAGES) & 1u);
@@ -1531,7 +1562,15 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
             const int copied = s_desc_copied[st];
             unsigned *bw = bits + b * K2_ENTRIES + j * K2_GROUPS + warp;
             if (so.has_f32 && copied == (int)K2_SUB) {
-                consume_cert<T, K2_NP>(so, sp, bw);
+                // adaptive (warp-uniform): a pass where the accept box left
+                // >= 8 lanes with points outside it (ring-like data) makes
+                // the next 64 sub-tiles skip the box test
+                if (CH_K2_BOX && box_mode == 0) {
+                    consume_cert<T, K2_NP, true>(so, sp, bw, box_mode);
+                } else {
+                    box_mode -= box_mode > 0;
+                    consume_cert<T, K2_NP, false>(so, sp, bw, box_mode);
+                }
                 __syncwarp();
                 if (lane == 0)
                     mbar_arrive(&s_empty[st]); // this warp is done with stage st
