@@ -1448,11 +1448,13 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
     if (warp == K2_PROD_WARP) {
         // ------------------------------------------------ TMA producer --
         // Streams this CTA's claimed super-tiles, sub-tile by sub-tile, into
-        // the ring.  Claims are made one super-tile ahead, in increasing order.
+        // the ring.  Claims are made in increasing order, each two sub-tiles
+        // before the current super-tile ends.
         if (lane == 0) {
             __threadfence();
             unsigned p_super = atomicAdd(&hdr->k2_claim, 1u);
-            unsigned p_next = p_super < nsuper ? atomicAdd(&hdr->k2_claim, 1u) : TILE_DONE;
+            unsigned p_next = TILE_DONE;
+            bool next_claimed = false;
             int p_j = 0;
             int p_nsub = 0;
             if (p_super < nsuper)
@@ -1477,6 +1479,15 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
                 // bulk copies move multiples of 16 bytes: an odd float tail
                 // point is read from global memory by its consumer thread
                 const unsigned copied = (cnt * (unsigned)sizeof(V2)) % 16u ? cnt - 1 : cnt;
+                // Claim the next super-tile two sub-tiles before this one's
+                // end (the atomic's latency hides behind them), not earlier:
+                // super-tiles are then processed nearly in claim order, so a
+                // look-back rarely waits on a predecessor that another CTA
+                // claimed but has not started.
+                if (!next_claimed && p_j >= p_nsub - 2) {
+                    p_next = atomicAdd(&hdr->k2_claim, 1u);
+                    next_claimed = true;
+                }
                 s_desc_super[st] = p_super;
                 s_desc_j[st] = p_j;
                 s_desc_nsub[st] = p_nsub;
@@ -1485,8 +1496,8 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
                 if (copied > 0)
                     tma_load_1d(stage + (size_t)st * K2_SUB, xy + 2 * base, copied * (unsigned)sizeof(V2), &s_full[st]);
                 if (++p_j == p_nsub) {
-                    p_super = p_next;
-                    p_next = p_super < nsuper ? atomicAdd(&hdr->k2_claim, 1u) : TILE_DONE;
+                    p_super = p_next >= nsuper ? TILE_DONE : p_next;
+                    next_claimed = false;
                     p_j = 0;
                     p_nsub = 0;
                     if (p_super < nsuper)
