@@ -50,6 +50,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef CH_K2_STAGES
 #define CH_K2_STAGES 3 // K2 TMA ring depth
 #endif
+#ifndef CH_K2_STAGES_F
+#define CH_K2_STAGES_F 3 // the same, float32 storage
+#endif
 #ifndef CH_K2_MINB
 #define CH_K2_MINB 2 // K2 resident CTAs per SM the registers are sized for
 #endif
@@ -78,7 +81,7 @@ template <> struct PtTraits<float> {
     static constexpr int K1_UNROLL = CH_K1_UNROLL_F;
     static constexpr int K1_MINB = CH_K1_MINB_F;
     static constexpr int K2_NP = CH_K2_NP_F;
-    static constexpr int K2_STAGES = CH_K2_STAGES;
+    static constexpr int K2_STAGES = CH_K2_STAGES_F;
 };
 template <typename T> constexpr long long k1_chunk() { return (long long)K1_THREADS * PtTraits<T>::K1_UNROLL * 2; }
 constexpr int K1_MAX_CTAS = 2048;
@@ -366,6 +369,39 @@ __device__ __forceinline__ void k1_update(Best &b, double x, double y, long long
         k1_slow_update(b, x, y, s, d, gi);
     acc = __fma_rn(x, 0.0, acc);
     acc = __fma_rn(y, 0.0, acc);
+}
+
+// Float storage: the same filter on fp32 keys (no fp64 op on the fast path).
+// x and y are floats, so x >= th[0] etc. are exact; s and d are compared as
+// RN32 sums against the running fp64 best rounded outward (RD32 for a max
+// slot, RU32 for a min slot): fl64(x + y) >= best implies fl32(x + y) >=
+// RD32(best) (RN32 and RN64 are monotone and RD32(best) is a float <= best
+// with no float in between), so every point the fp64 rule would consider
+// still reaches k1_slow_update, which decides exactly as the fp64 path does.
+__device__ __forceinline__ void k1_thresholds(const Best &b, float (&th)[8])
+{
+    th[0] = (float)b.v[0]; // x, y slots: floats (or +-inf) already
+    th[1] = __double2float_rd(b.v[1]);
+    th[2] = (float)b.v[2];
+    th[3] = __double2float_ru(b.v[3]);
+    th[4] = (float)b.v[4];
+    th[5] = __double2float_ru(b.v[5]);
+    th[6] = (float)b.v[6];
+    th[7] = __double2float_rd(b.v[7]);
+}
+__device__ __forceinline__ void k1_update_f32(Best &b, float (&th)[8], float x, float y, long long gi, float &acc)
+{
+    const float s = __fadd_rn(x, y);
+    const float d = __fsub_rn(x, y);
+    const bool t = (x >= th[0]) | (s >= th[1]) | (y >= th[2]) | (d <= th[3]) | (x <= th[4]) | (s <= th[5]) |
+                   (y <= th[6]) | (d >= th[7]);
+    if (t) {
+        const double xd = x, yd = y;
+        k1_slow_update(b, xd, yd, __dadd_rn(xd, yd), __dsub_rn(xd, yd), gi);
+        k1_thresholds(b, th);
+    }
+    acc = __fmaf_rn(x, 0.0f, acc);
+    acc = __fmaf_rn(y, 0.0f, acc);
 }
 
 __device__ __forceinline__ void k1_warp_share(Best &b)
@@ -720,11 +756,43 @@ k1_extremes8(const T *__restrict__ xy, long long n, long long index_base, int fl
         b.i[k] = LLONG_MAX;
     }
     double acc = 0.0;
+    float accf = 0.0f;
+    float th[8];
+    k1_thresholds(b, th);
     const long long nchunks = (n + K1_CHUNK - 1) / K1_CHUNK;
     int it = 0;
     for (long long c = nchunks - 1 - blockIdx.x; c >= 0; c -= gridDim.x, it++) {
         const long long base = c * K1_CHUNK;
         const long long gbase = index_base + base + 2 * tid;
+        if constexpr (sizeof(T) == 4) {
+            if (base + K1_CHUNK <= n) {
+                T v[K1_UNROLL][4];
+#pragma unroll
+                for (int u = 0; u < K1_UNROLL; u++)
+                    ld2raw<T, VEC>(xy + 2 * (base + 2 * ((long long)u * K1_THREADS + tid)), v[u]);
+#pragma unroll
+                for (int u = K1_UNROLL - 1; u >= 0; u--) {
+                    k1_update_f32(b, th, v[u][2], v[u][3], gbase + 2 * u * K1_THREADS + 1, accf);
+                    k1_update_f32(b, th, v[u][0], v[u][1], gbase + 2 * u * K1_THREADS, accf);
+                }
+            } else {
+                for (int u = K1_UNROLL - 1; u >= 0; u--) {
+                    long long p = base + 2 * ((long long)u * K1_THREADS + tid);
+                    for (int h = 1; h >= 0; h--) {
+                        if (p + h < n) {
+                            float x, y;
+                            ld1raw(xy, p + h, x, y);
+                            k1_update_f32(b, th, x, y, index_base + p + h, accf);
+                        }
+                    }
+                }
+            }
+            if ((it & (K1_SHARE - 1)) == 0) {
+                k1_warp_share(b);
+                k1_thresholds(b, th);
+            }
+            continue;
+        }
         if (base + K1_CHUNK <= n) {
             T v[K1_UNROLL][4];
 #pragma unroll
@@ -779,7 +847,7 @@ k1_extremes8(const T *__restrict__ xy, long long n, long long index_base, int fl
             s_i[warp][k] = id[k];
         }
     }
-    int nf = __syncthreads_or(acc != acc);
+    int nf = __syncthreads_or(acc != acc || accf != accf);
     if (tid < 8) {
         const int k = tid;
         double bv = s_v[0][k];
