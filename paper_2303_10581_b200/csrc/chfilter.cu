@@ -38,6 +38,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef CH_K1_UNROLL_F
 #define CH_K1_UNROLL_F 6 // K1 wide loads (2 points each) per thread per chunk, float32 storage (8 spills at 80 registers)
 #endif
+#ifndef CH_K1_PPL_F
+#define CH_K1_PPL_F 2 // float32 points per K1 wide load: 2 (128 bits) or 4 (256 bits)
+#endif
 #ifndef CH_K1_MINB_F
 #define CH_K1_MINB_F 3 // K1 CTAs per SM for float32 storage
 #endif
@@ -72,6 +75,7 @@ template <typename T> struct PtTraits;
 template <> struct PtTraits<double> {
     using V2 = double2;
     static constexpr int K1_UNROLL = 4; // wide loads (2 points each) per thread per chunk
+    static constexpr int K1_PPL = 2;    // points per wide load (256 bits)
     static constexpr int K1_MINB = 3;   // K1 CTAs per SM the registers are sized for
     static constexpr int K2_NP = CH_K2_NP_D;     // points per consumer thread per sub-tile
     static constexpr int K2_STAGES = CH_K2_STAGES; // TMA ring depth (sub-tiles)
@@ -79,11 +83,15 @@ template <> struct PtTraits<double> {
 template <> struct PtTraits<float> {
     using V2 = float2;
     static constexpr int K1_UNROLL = CH_K1_UNROLL_F;
+    static constexpr int K1_PPL = CH_K1_PPL_F;
     static constexpr int K1_MINB = CH_K1_MINB_F;
     static constexpr int K2_NP = CH_K2_NP_F;
     static constexpr int K2_STAGES = CH_K2_STAGES_F;
 };
-template <typename T> constexpr long long k1_chunk() { return (long long)K1_THREADS * PtTraits<T>::K1_UNROLL * 2; }
+template <typename T> constexpr long long k1_chunk()
+{
+    return (long long)K1_THREADS * PtTraits<T>::K1_UNROLL * PtTraits<T>::K1_PPL;
+}
 constexpr int K1_MAX_CTAS = 2048;
 
 constexpr int K2_CWARPS = 8;                                   // consumer (compute) warps per CTA
@@ -150,6 +158,12 @@ __device__ __forceinline__ void ld128f(const float *p, float &a, float &b, float
 {
     asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
                  : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld256f(const float *p, float (&r)[8])
+{
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
                  : "l"(p));
 }
 __device__ __forceinline__ void ld64f(const float *p, float &a, float &b)
@@ -765,20 +779,30 @@ k1_extremes8(const T *__restrict__ xy, long long n, long long index_base, int fl
         const long long base = c * K1_CHUNK;
         const long long gbase = index_base + base + 2 * tid;
         if constexpr (sizeof(T) == 4) {
+            constexpr int PPL = PtTraits<T>::K1_PPL;
+            const long long gb = index_base + base + PPL * tid;
             if (base + K1_CHUNK <= n) {
-                T v[K1_UNROLL][4];
+                float v[K1_UNROLL][2 * PPL];
 #pragma unroll
-                for (int u = 0; u < K1_UNROLL; u++)
-                    ld2raw<T, VEC>(xy + 2 * (base + 2 * ((long long)u * K1_THREADS + tid)), v[u]);
+                for (int u = 0; u < K1_UNROLL; u++) {
+                    const float *q = (const float *)xy + 2 * (base + PPL * ((long long)u * K1_THREADS + tid));
+                    if constexpr (PPL == 4 && VEC) {
+                        ld256f(q, *(float(*)[8]) & v[u][0]);
+                    } else {
 #pragma unroll
-                for (int u = K1_UNROLL - 1; u >= 0; u--) {
-                    k1_update_f32(b, th, v[u][2], v[u][3], gbase + 2 * u * K1_THREADS + 1, accf);
-                    k1_update_f32(b, th, v[u][0], v[u][1], gbase + 2 * u * K1_THREADS, accf);
+                        for (int h2 = 0; h2 < PPL / 2; h2++)
+                            ld2raw<T, VEC>((const T *)q + 4 * h2, *(T(*)[4]) & v[u][4 * h2]);
+                    }
                 }
+#pragma unroll
+                for (int u = K1_UNROLL - 1; u >= 0; u--)
+#pragma unroll
+                    for (int h = PPL - 1; h >= 0; h--)
+                        k1_update_f32(b, th, v[u][2 * h], v[u][2 * h + 1], gb + PPL * u * K1_THREADS + h, accf);
             } else {
                 for (int u = K1_UNROLL - 1; u >= 0; u--) {
-                    long long p = base + 2 * ((long long)u * K1_THREADS + tid);
-                    for (int h = 1; h >= 0; h--) {
+                    long long p = base + PPL * ((long long)u * K1_THREADS + tid);
+                    for (int h = PPL - 1; h >= 0; h--) {
                         if (p + h < n) {
                             float x, y;
                             ld1raw(xy, p + h, x, y);
@@ -2321,8 +2345,8 @@ ch_status launch_k1(const T *d_xy, long long n, long long index_base, int flags,
     g = std::min<long long>(g, K1_MAX_CTAS);
     if (g < 1)
         g = 1;
-    // wide loads need the pair of points aligned to its size (32 B / 16 B)
-    if (((uintptr_t)d_xy & (4 * sizeof(T) - 1)) == 0)
+    // wide loads need their points aligned to the load size (32 B / 16 B)
+    if (((uintptr_t)d_xy & (2 * PtTraits<T>::K1_PPL * sizeof(T) - 1)) == 0)
         k1_extremes8<T, true><<<(unsigned)g, K1_THREADS, 0, st>>>(d_xy, n, index_base, flags, hdr_of(d_ws),
                                                                    parts_of(d_ws), d_ext_out, pp);
     else
