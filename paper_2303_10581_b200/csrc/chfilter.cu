@@ -1285,6 +1285,73 @@ __device__ __forceinline__ void cert_min(const SOct &s, const f32x2 (&X)[NQ], co
     }
 }
 
+// The min-certificate (chf::octagon_edge) on points held
+// in registers (K5, K6): slots [0, np) of this thread (np warp-uniform),
+// `valid` the slots holding a point.  Survivor mask, bit-identical to
+// "not (forall k: D_k > T_k)" (R4): G >= +0 discards, G + f32_delta < 0
+// keeps, the rest (the ~1e-7 band) is decided in fp64 on every edge.
+template <int NP>
+__device__ __forceinline__ unsigned cert_classify(const SOct &s, const double (&px)[NP], const double (&py)[NP],
+                                                  unsigned valid, int np)
+{
+    static_assert(NP % 2 == 0, "point pairs");
+    constexpr int HQ = NP / 2;
+    f32x2 X[HQ], Y[HQ];
+    float glo[HQ], ghi[HQ];
+#pragma unroll
+    for (int q = 0; q < HQ; q++) {
+        X[q] = pk2((float)px[2 * q], (float)px[2 * q + 1]);
+        Y[q] = pk2((float)py[2 * q], (float)py[2 * q + 1]);
+        glo[q] = ghi[q] = 0.0f;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+        const f32x2 *e0 = (const f32x2 *)&s.fab[k], *e1 = (const f32x2 *)&s.fab[k + 1];
+        const f32x2 a0 = e0[0], b0 = e0[1], a1 = e1[0], b1 = e1[1];
+        const f32x2 c0 = *(const f32x2 *)&s.fc[k], c1 = *(const f32x2 *)&s.fc[k + 1];
+#pragma unroll
+        for (int q = 0; q < HQ; q++) {
+            if (2 * q >= np)
+                break;
+            float l0, h0, l1, h1;
+            unpk2(ffma2(a0, X[q], ffma2(b0, Y[q], c0)), l0, h0);
+            unpk2(ffma2(a1, X[q], ffma2(b1, Y[q], c1)), l1, h1);
+            if (k == 0) {
+                glo[q] = fminf(l0, l1);
+                ghi[q] = fminf(h0, h1);
+            } else {
+                glo[q] = fmin3(glo[q], l0, l1);
+                ghi[q] = fmin3(ghi[q], h0, h1);
+            }
+        }
+    }
+    float dl, dh;
+    unpk2(s.fdelta, dl, dh);
+    unsigned keep = 0, band = 0;
+#pragma unroll
+    for (int i = 0; i < NP; i++) {
+        const float G = (i & 1) ? ghi[i / 2] : glo[i / 2];
+        const bool neg = (int)__float_as_uint(G) < 0;                    // not certified inside
+        const bool kc = (int)__float_as_uint(__fadd_rn(G, dl)) < 0;     // certified kept
+        keep |= (kc ? 1u : 0u) << i;
+        band |= (neg && !kc ? 1u : 0u) << i;
+    }
+    keep &= valid;
+    band &= valid;
+    if (__any_sync(FULL, band)) {
+#pragma unroll
+        for (int i = 0; i < NP; i++) {
+            if ((band >> i) & 1u) {
+                bool kf = false;
+                for (int k = 0; k < s.nv && !kf; k++)
+                    kf = !edge_inside(s, k, s.exact, px[i], py[i]);
+                keep |= (kf ? 1u : 0u) << i;
+            }
+        }
+    }
+    return keep;
+}
+
 // One full sub-tile of a consumer warp for has_f32 octagons, read straight
 // from the TMA stage (held until the caller releases it).  Writes, for each
 // point slot u, the warp ballot of "point u of this lane survives" to
@@ -1948,7 +2015,9 @@ k5_small_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hdr,
     // ---- octagon test + stable compaction: groups (j, warp) of 32
     //      consecutive points, block scan of their popcounts ----
     int guess_mode = 0; // adaptive: see classify()
-    const unsigned keep = so.degenerate ? valid : classify<double, B>(so, px, py, valid, guess_mode, P);
+    const unsigned keep = so.degenerate ? valid
+                          : so.has_f32  ? cert_classify<B>(so, px, py, valid, P)
+                                        : classify<double, B>(so, px, py, valid, guess_mode, P);
     CH_TR(6);
     unsigned m[B];
 #pragma unroll
@@ -2021,11 +2090,12 @@ k5_small_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hdr,
 // step in ONE launch of one 8-CTA thread-block cluster, each point read once
 // into registers.  CTA r holds points [r P T, (r + 1) P T) (T threads, P =
 // ceil(n / 8T) slots per thread, so every CTA has work).  Extremes per CTA
-// (selects, butterflies), pushed into CTA 0's shared memory; CTA 0 builds the
-// octagon (build_octagon_cta) and pushes it into every CTA's shared memory;
-// the octagon test, and a stable compaction whose per-CTA totals are pushed
-// to every CTA.  Only remote STORES cross the cluster, each followed by one
-// cluster barrier (release / acquire).  Same decisions as K1 + K2.
+// (selects, butterflies), pushed into EVERY CTA's shared memory; every CTA
+// combines them and builds the octagon itself (build_octagon_cta; the same
+// values everywhere); the octagon test, and a stable compaction whose
+// per-CTA totals are pushed to every CTA.  Only remote STORES cross the
+// cluster, each followed by one cluster barrier (release / acquire): two in
+// all.  Same decisions as K1 + K2.
 constexpr int KC_CTAS = 8, KC_THREADS = 512, KC_P = 8;
 constexpr long long KC_MAX_N = (long long)KC_CTAS * KC_THREADS * KC_P;
 
@@ -2039,13 +2109,13 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
     constexpr int NW = KC_THREADS / 32;
     __shared__ double s_v[NW][8];
     __shared__ long long s_i[NW][8];
-    __shared__ double s_cv[KC_CTAS][8];     // CTA 0: every CTA's extremes (pushed)
+    __shared__ double s_cv[KC_CTAS][8];     // every CTA's extremes (pushed to every CTA)
     __shared__ long long s_ci[KC_CTAS][8];
-    __shared__ int s_cnf[KC_CTAS];          // CTA 0: every CTA's non-finite flag (pushed)
-    __shared__ int s_nfall;                 // CTA 0: the cluster's
-    __shared__ ch_extremes s_e;             // CTA 0
-    __shared__ ch_octagon s_o;              // CTA 0
-    __shared__ SOct so;                     // every CTA (pushed by CTA 0)
+    __shared__ int s_cnf[KC_CTAS];          // every CTA's non-finite flag (pushed)
+    __shared__ int s_nfall;                 // the cluster's
+    __shared__ ch_extremes s_e;             // built by every CTA (the same values)
+    __shared__ ch_octagon s_o;
+    __shared__ SOct so;
     __shared__ int s_cnt[KC_P * NW], s_pre[KC_P * NW];
     __shared__ int s_tots[KC_CTAS];         // every CTA's survivor total (pushed)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -2094,54 +2164,52 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
     const int nf = __syncthreads_or(acc != acc);
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); // every CTA of the cluster runs
     CH_TR(12);
-    if (warp == 0) { // this CTA's extremes (lane k < 8: key k) -> CTA 0's shared memory
+    if (warp == 0) { // this CTA's extremes (lane k < 8: key k) -> every CTA's shared memory
         double cv;
         long long ci;
         rows_combine<NW>(s_v, s_i, cv, ci);
-        if (lane < 8) {
-            *cluster.map_shared_rank(&s_cv[r][lane], 0) = cv;
-            *cluster.map_shared_rank(&s_ci[r][lane], 0) = ci;
-            if (lane == 0)
-                *cluster.map_shared_rank(&s_cnf[r], 0) = nf;
+        // lane L pushes key L & 7 to CTAs (L >> 3) and (L >> 3) + 4
+        const int k = lane & 7, d0 = lane >> 3;
+        cv = __shfl_sync(FULL, cv, k);
+        ci = __shfl_sync(FULL, ci, k);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int d = d0 + 4 * h;
+            *cluster.map_shared_rank(&s_cv[r][k], d) = cv;
+            *cluster.map_shared_rank(&s_ci[r][k], d) = ci;
+            if (k == 0)
+                *cluster.map_shared_rank(&s_cnf[r], d) = nf;
         }
     }
-    cluster.sync(); // CTA 0 holds every CTA's partial
+    cluster.sync(); // every CTA holds every CTA's partial
     CH_TR(13);
-    if (r == 0) {
-        if (warp == 0) {
-            double cv;
-            long long ci;
-            rows_combine<KC_CTAS>(s_cv, s_ci, cv, ci);
-            const int anynf = __any_sync(FULL, lane < KC_CTAS && s_cnf[lane]);
-            if (lane < 8) {
-                s_e.idx[lane] = ci;
-                s_e.x[lane] = (double)xy[2 * ci];
-                s_e.y[lane] = (double)xy[2 * ci + 1];
-            }
-            if (lane == 0)
-                s_nfall = anynf;
+    // Every CTA combines the partials and builds the octagon itself (the
+    // same operations on the same values, so the same octagon): no second
+    // push and no cluster barrier for it.
+    if (warp == 0) {
+        double cv;
+        long long ci;
+        rows_combine<KC_CTAS>(s_cv, s_ci, cv, ci);
+        const int anynf = __any_sync(FULL, lane < KC_CTAS && s_cnf[lane]);
+        if (lane < 8) {
+            s_e.idx[lane] = ci;
+            s_e.x[lane] = (double)xy[2 * ci];
+            s_e.y[lane] = (double)xy[2 * ci + 1];
         }
-        __syncthreads();
-        CH_TR(14);
-        build_octagon_cta(s_e, flags, s_o);
-        load_soct(so, &s_o);
-        __syncthreads();
-        CH_TR(15);
-        // push the SOct into the other CTAs' shared memory
-        static_assert(sizeof(SOct) % 16 == 0 && alignof(SOct) >= 16, "SOct is pushed as 16-byte words");
-        constexpr int WORDS = (int)(sizeof(SOct) / 16);
-        const uint4 *src = (const uint4 *)&so;
-        for (int q = tid; q < (KC_CTAS - 1) * WORDS; q += KC_THREADS) {
-            const int dstc = 1 + q / WORDS, w = q % WORDS;
-            uint4 *dst = (uint4 *)cluster.map_shared_rank(&so, dstc);
-            dst[w] = src[w];
-        }
+        if (lane == 0)
+            s_nfall = anynf;
     }
-    cluster.sync(); // every CTA has the octagon
+    __syncthreads();
+    CH_TR(14);
+    build_octagon_cta(s_e, flags, s_o);
+    load_soct(so, &s_o);
+    __syncthreads();
     CH_TR(16);
     // ---- octagon test + stable compaction (groups (j, warp) of 32 points) ----
     int guess_mode = 0;
-    const unsigned keep = so.degenerate ? valid : classify<double, KC_P>(so, px, py, valid, guess_mode, P);
+    const unsigned keep = so.degenerate ? valid
+                          : so.has_f32  ? cert_classify<KC_P>(so, px, py, valid, P)
+                                        : classify<double, KC_P>(so, px, py, valid, guess_mode, P);
     CH_TR(17);
     unsigned m[KC_P];
 #pragma unroll
