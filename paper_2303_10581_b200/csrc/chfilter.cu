@@ -2214,7 +2214,7 @@ k6_cluster_filter(const T *__restrict__ xy, long long n, int flags, WsHeader *hd
     unsigned m[KC_P];
 #pragma unroll
     for (int j = 0; j < KC_P; j++) {
-        m[j] = __ballot_sync(FULL, (keep >> j) & 1u);
+        m[j] = j < P ? __ballot_sync(FULL, (keep >> j) & 1u) : 0u; // (P is CTA-uniform)
         if (lane == 0)
             s_cnt[j * NW + warp] = __popc(m[j]);
     }

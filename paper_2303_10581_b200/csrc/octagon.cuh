@@ -65,16 +65,26 @@ CH_HD double dmin(double a, double b) { return a < b ? a : b; }
 // every point of the box does, i.e. the box only ever discards points the
 // oracle discards.
 
-// fp32 value >= v (round to nearest, then one step up if it fell below).
+// The smallest fp32 value >= v, i.e. v rounded toward +inf (host: round to
+// nearest, then one step up if it fell below; device: the directed-rounding
+// conversion, one instruction, the same function), and likewise down.
 CH_HD float f32_up(double v)
 {
+#ifdef __CUDA_ARCH__
+    return __double2float_ru(v);
+#else
     float f = CH_F32(v);
     return ((double)f < v) ? CH_NEXTF(f, __builtin_huge_valf()) : f;
+#endif
 }
 CH_HD float f32_down(double v)
 {
+#ifdef __CUDA_ARCH__
+    return __double2float_rd(v);
+#else
     float f = CH_F32(v);
     return ((double)f > v) ? CH_NEXTF(f, -__builtin_huge_valf()) : f;
+#endif
 }
 
 // fp32 certification of the edge predicate,

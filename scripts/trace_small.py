@@ -30,6 +30,7 @@ for dist in ("normal", "circle"):
         r = rows[-1]
         b = 0 if n <= 4096 else 10
         last = 8 if b == 0 else 20
-        ph = [r[k] - r[b] for k in range(b, last + 1)]
+        ks = [k for k in range(b, last + 1) if k != 15]  # (K6 has no phase 15 since the octagon push went)
+        ph = [r[k] - r[b] for k in ks]
         bo = [r[k] - r[14 if b else 3] for k in (21, 22, 23, 24)]
         print(f"{dist:7s} {n:6d} " + " ".join(f"{v:6d}" for v in ph) + "  | octagon " + " ".join(f"{v:6d}" for v in bo))
