@@ -59,6 +59,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef CH_K2_MINB
 #define CH_K2_MINB 2 // K2 resident CTAs per SM the registers are sized for
 #endif
+#ifndef CH_K2_SUPERS
+#define CH_K2_SUPERS 8 // K2 super-tiles per resident CTA the super-tile size aims for
+#endif
 #ifndef CH_K2_BOX
 #define CH_K2_BOX 1 // K2 accept-box stage: 0 never (certificates only), 1 adaptive
 #endif
@@ -99,6 +102,7 @@ constexpr int K2_CTHREADS = K2_CWARPS * 32;
 constexpr int K2_PROD_WARP = K2_CWARPS + 1;                    // TMA producer warp
 constexpr int K2_THREADS = K2_CTHREADS + 64;
 constexpr int K2_ENTRIES = 4 * K2_CTHREADS;                    // ballot words per super-tile (block scan: 4/thread)
+constexpr int K2_SLOTS = K2_ENTRIES / K2_CWARPS;               // ballot words per consumer warp per super-tile
 template <typename T> constexpr long long k2_sub() { return (long long)K2_CTHREADS * PtTraits<T>::K2_NP; }
 template <typename T> constexpr int k2_groups() { return PtTraits<T>::K2_NP * K2_CWARPS; } // 32-point groups / sub-tile
 template <typename T> constexpr int k2_maxsub() { return K2_ENTRIES / k2_groups<T>(); }   // sub-tiles / super-tile
@@ -1355,7 +1359,7 @@ __device__ __forceinline__ unsigned cert_classify(const SOct &s, const double (&
 // One full sub-tile of a consumer warp for has_f32 octagons, read straight
 // from the TMA stage (held until the caller releases it).  Writes, for each
 // point slot u, the warp ballot of "point u of this lane survives" to
-// mw[u * K2_CWARPS] (lane 0), bit-identical to "not (forall k: D_k > T_k)"
+// mw[u] (lane 0; the warp's slots are contiguous, 16-byte aligned), bit-identical to "not (forall k: D_k > T_k)"
 // (R4).  Every stage is a certificate proven on its own (box:
 // chf::box_corner_ok; fp32: chf::octagon_edge), so the order cannot change a
 // result.  Per-point state is a sign bit; the warp-uniform skips are one
@@ -1372,6 +1376,7 @@ __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTra
 {
     constexpr int H = CH_CERT_H < NP ? CH_CERT_H : NP; // points per pass (register budget)
     constexpr int HQ = H / 2;
+    static_assert(H % 4 == 0 && NP % H == 0, "passes of whole 16-byte ballot stores");
     constexpr f32x2 SIGN2 = 0x8000000080000000ull;
     const int tid = threadIdx.x;
     const bool lane0 = (tid & 31) == 0;
@@ -1434,9 +1439,9 @@ __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTra
                 box_mode = 64;
             if (nout == 0) {
 #pragma unroll
-                for (int i = 0; i < H; i++)
+                for (int i = 0; i < H; i += 4)
                     if (lane0)
-                        mw[(h0 + i) * K2_CWARPS] = 0u;
+                        *(uint4 *)&mw[h0 + i] = make_uint4(0u, 0u, 0u, 0u);
                 continue;
             }
         }
@@ -1449,9 +1454,9 @@ __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTra
                 neg |= __float_as_uint(glo[q]) | __float_as_uint(ghi[q]);
             if (!__any_sync(FULL, (int)neg < 0)) {
 #pragma unroll
-                for (int i = 0; i < H; i++)
+                for (int i = 0; i < H; i += 4)
                     if (lane0)
-                        mw[(h0 + i) * K2_CWARPS] = 0u;
+                        *(uint4 *)&mw[h0 + i] = make_uint4(0u, 0u, 0u, 0u);
                 continue;
             }
         }
@@ -1489,10 +1494,13 @@ __device__ __forceinline__ void consume_cert(const SOct &s, const typename PtTra
             }
         }
 #pragma unroll
-        for (int i = 0; i < H; i++) {
-            const unsigned m = __ballot_sync(FULL, (i & 1) ? sign_hi(keep[i / 2]) : sign_lo(keep[i / 2]));
+        for (int i = 0; i < H; i += 4) { // four ballots, one 16-byte store (this warp's slots are contiguous)
+            const unsigned m0 = __ballot_sync(FULL, sign_lo(keep[i / 2]));
+            const unsigned m1 = __ballot_sync(FULL, sign_hi(keep[i / 2]));
+            const unsigned m2 = __ballot_sync(FULL, sign_lo(keep[i / 2 + 1]));
+            const unsigned m3 = __ballot_sync(FULL, sign_hi(keep[i / 2 + 1]));
             if (lane0)
-                mw[(h0 + i) * K2_CWARPS] = m;
+                *(uint4 *)&mw[h0 + i] = make_uint4(m0, m1, m2, m3);
         }
     }
 }
@@ -1672,46 +1680,52 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
         // consumer warp for its own 32-point groups, once the publisher has
         // resolved the super-tile's global offset.
         // Group e of a super-tile holds its points [32 e, 32 e + 32) (e =
-        // (j * K2_NP + u) * K2_CWARPS + warp), so warp w writes the contiguous
-        // groups [w E / 8, (w + 1) E / 8), four per step, branch-free.
+        // (j * K2_NP + u) * K2_CWARPS + warp); its ballot word and offset sit
+        // at [warp][j * K2_NP + u], so warp w writes the groups it tested,
+        // four per step (one 16-byte load of ballots, one of offsets).
         auto write_survivors = [&](int bb) {
             bar_sync(K2_BAR_BASE + 2 + bb, K2_CTHREADS + 32); // offset of buffer bb is known
             if (s_total[bb] > 0) {
-                const int E = s_nsub[bb] * K2_GROUPS, per = E / K2_CWARPS, e0 = warp * per;
+                // this warp's own slots (the groups it tested): slot t is
+                // group e = 8 t + warp, points [32 e, 32 e + 32) of the
+                // super-tile; its ballot and offset words are contiguous
+                const int per = s_nsub[bb] * K2_NP;
                 long long *ob = out + s_excl[bb];
                 asm("" : "+l"(ob)); // one base register: offsets below are 32-bit
-                long long v = (long long)s_tile[bb] * super_pts + index_base + 32LL * e0 + lane;
-                const uint4 *bw = (const uint4 *)(bits + bb * K2_ENTRIES + e0);
-                const int4 *sc = (const int4 *)(gscan + bb * K2_ENTRIES + e0);
+                long long v = (long long)s_tile[bb] * super_pts + index_base + 32LL * warp + lane;
+                const uint4 *bw = (const uint4 *)(bits + bb * K2_ENTRIES + warp * K2_SLOTS);
+                const int4 *sc = (const int4 *)(gscan + bb * K2_ENTRIES + warp * K2_SLOTS);
                 const unsigned lb = 1u << lane;
-                const long long vend = v + 32LL * per; // this warp's index range: [v - lane, vend)
+                const long long vend = v - lane + 256LL * (per - 1) + 32; // this warp's index range: [v - lane, vend)
                 if ((v >> 32) == ((vend - 1) >> 32)) {
                     // no 2^32 crossing: the high word is constant, the low word a 32-bit add
                     const unsigned hi = (unsigned)(v >> 32);
                     unsigned lo = (unsigned)v;
-                    for (int q = 0; q < per / 4; q++, lo += 128) {
+                    for (int q = 0; q < per / 4; q++, lo += 1024) {
                         const uint4 m = bw[q];
                         if ((m.x | m.y | m.z | m.w) == 0u)
                             continue;
                         const int4 c = sc[q];
                         store_group32(ob, m.x, c.x, lo, hi, lb, lt);
-                        store_group32(ob, m.y, c.y, lo + 32, hi, lb, lt);
-                        store_group32(ob, m.z, c.z, lo + 64, hi, lb, lt);
-                        store_group32(ob, m.w, c.w, lo + 96, hi, lb, lt);
+                        store_group32(ob, m.y, c.y, lo + 256, hi, lb, lt);
+                        store_group32(ob, m.z, c.z, lo + 512, hi, lb, lt);
+                        store_group32(ob, m.w, c.w, lo + 768, hi, lb, lt);
                     }
+                    __syncwarp();
                     return;
                 }
-                for (int q = 0; q < per / 4; q++, v += 128) {
+                for (int q = 0; q < per / 4; q++, v += 1024) {
                     const uint4 m = bw[q];
                     if ((m.x | m.y | m.z | m.w) == 0u)
                         continue;
                     const int4 c = sc[q];
                     store_group(ob, m.x, c.x, v, lb, lt);
-                    store_group(ob, m.y, c.y, v + 32, lb, lt);
-                    store_group(ob, m.z, c.z, v + 64, lb, lt);
-                    store_group(ob, m.w, c.w, v + 96, lb, lt);
+                    store_group(ob, m.y, c.y, v + 256, lb, lt);
+                    store_group(ob, m.z, c.z, v + 512, lb, lt);
+                    store_group(ob, m.w, c.w, v + 768, lb, lt);
                 }
             }
+            __syncwarp(); // every lane's reads of its ballot words before lane 0 refills them
         };
         int b = 0, uses0 = 0, uses1 = 0;
         int guess_mode = 0; // adaptive: see classify()
@@ -1724,13 +1738,18 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
                 break;
             const int j = s_desc_j[st], nsub = s_desc_nsub[st];
             if (j == 0 && (b ? uses1 : uses0) > 0) {
-                write_survivors(b);                    // super-tile handed off two rounds ago
-                bar_sync(K2_BAR_BASE + 4, K2_CTHREADS); // all warps done with buffer b
+                // super-tile handed off two rounds ago.  Each warp reads only
+                // the ballot words it wrote itself (its own slots) and the
+                // offsets the block scan wrote before the hand-off, so no
+                // barrier is needed before the warp refills buffer b; the
+                // next scan's barrier orders every warp's reads before the
+                // scan overwrites the offsets
+                write_survivors(b);
             }
             const long long base = (long long)sup * super_pts + (long long)j * K2_SUB;
             const V2 *sp = stage + (size_t)st * K2_SUB;
             const int copied = s_desc_copied[st];
-            unsigned *bw = bits + b * K2_ENTRIES + j * K2_GROUPS + warp;
+            unsigned *bw = bits + b * K2_ENTRIES + warp * K2_SLOTS + j * K2_NP; // this warp's slots (j, u)
             if (so.has_f32 && copied == (int)K2_SUB) {
                 // adaptive (warp-uniform): a pass where the accept box left
                 // >= 8 lanes with points outside it (ring-like data) makes
@@ -1771,7 +1790,7 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
             for (int u = 0; u < K2_NP; u++) {
                 const unsigned m = __ballot_sync(FULL, keep & (1u << u));
                 if (lane == 0)
-                    bw[u * K2_CWARPS] = m;
+                    bw[u] = m;
             }
             }
             if (j == nsub - 1) {
@@ -1779,11 +1798,13 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
                 bar_sync(K2_BAR_BASE + 4, K2_CTHREADS);
                 const int E = nsub * K2_GROUPS;
                 const unsigned *bb = bits + b * K2_ENTRIES;
+                // group e (index order) = slot e / 8 of warp e % 8, stored at
+                // [warp][slot]
                 int c[4], sum = 0;
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
                     const int e = 4 * tid + q;
-                    c[q] = e < E ? __popc(bb[e]) : 0;
+                    c[q] = e < E ? __popc(bb[(e % K2_CWARPS) * K2_SLOTS + e / K2_CWARPS]) : 0;
                     sum += c[q];
                 }
                 int inc = sum;
@@ -1806,7 +1827,8 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
                 int *sc = gscan + b * K2_ENTRIES;
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
-                    sc[4 * tid + q] = ex;
+                    const int e = 4 * tid + q;
+                    sc[(e % K2_CWARPS) * K2_SLOTS + e / K2_CWARPS] = ex;
                     ex += c[q];
                 }
                 if (tid == 0) {
@@ -2493,8 +2515,10 @@ ch_status launch_k2(const T *d_xy, long long n, long long index_base, const ch_o
     long long resident = (long long)di.sms * (sizeof(T) == 8 ? di.k2_per_sm_d : di.k2_per_sm_f);
     constexpr long long K2_SUB = k2_sub<T>();
     long long nsub_total = (n + K2_SUB - 1) / K2_SUB;
-    // aim for >= 8 super-tiles per CTA (load balance), <= k2_maxsub sub-tiles each
-    long long subs = (nsub_total + resident * 8 - 1) / (resident * 8);
+    // aim for >= CH_K2_SUPERS super-tiles per CTA (load balance: the last
+    // super-tiles' look-backs wait on their predecessors), <= k2_maxsub
+    // sub-tiles each
+    long long subs = (nsub_total + resident * CH_K2_SUPERS - 1) / (resident * CH_K2_SUPERS);
     subs = std::max<long long>(1, std::min<long long>(subs, (long long)k2_maxsub<T>()));
     long long nsuper = (nsub_total + subs - 1) / subs;
     long long grid = std::max<long long>(1, std::min<long long>(resident, nsuper));
