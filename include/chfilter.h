@@ -385,8 +385,10 @@ ch_status ch_hull_points(const double *h_pts, const int64_t *h_ids, int64_t m,
 /* f1: Algorithm 1 line 4 on the device (future work P:432):
  * the exact strict hull of the m survivors d_surv (indices into d_xy, which
  * holds n_points points), same canonical form as ch_hull_points (DESIGN R8).
- * n_points < 2^32 lets the sorts carry 32-bit ids.  Two stable radix sorts by
- * (x, y), per-chunk exact monotone chains, a tree of exact bridge merges.
+ * n_points < 2^32 lets the sort carry 32-bit ids.  One radix sort by x, each
+ * run of equal x reduced in place to its lowest and highest point (the only
+ * possible strict hull vertices among them), per-chunk exact monotone
+ * chains, a tree of exact bridge merges.
  * Scratch: ch_hull_gpu_temp_bytes(m) bytes at d_tmp.  Hull ids go to h_hull
  * (host, capacity m); synchronizes `stream`. */
 size_t ch_hull_gpu_temp_bytes(int64_t m);

@@ -5,9 +5,13 @@
 // The exact strict hull of the survivors (DESIGN R8: CCW from the
 // lexicographic minimum, duplicates -> lowest id, collinear points excluded),
 // identical to the host monotone chain and the oracle:
-//   1. sort the survivors by (x, y) with two stable radix sorts (y, then x) on
-//      order-preserving 64-bit keys (-0.0 folded into +0.0); equal points
-//      keep increasing-id order;
+//   1. sort the survivors by x (one radix sort on order-preserving 64-bit
+//      keys, -0.0 folded into +0.0), then resolve every run of equal x in
+//      place (k_ties): only the run's lowest point (min y, then lowest id)
+//      and highest point (max y, then lowest id) can be strict hull
+//      vertices -- the points between them lie inside a vertical segment --
+//      so the run becomes [low, low, ..., low, high], which is sorted by
+//      (x, y) and whose copies the chains skip as duplicates;
 //   2. lower and upper chains: one thread per chunk of HG_CHUNK sorted points
 //      runs Andrew's monotone chain (pop while the exact turn is <= 0,
 //      chf::orient_sign; a point equal to its sorted predecessor is skipped,
@@ -44,22 +48,54 @@ __device__ __forceinline__ unsigned long long okey(double d)
 }
 
 template <typename V>
-__global__ void k_ykeys(const double *__restrict__ xy, const long long *__restrict__ surv, long long m,
+__global__ void k_xkeys(const double *__restrict__ xy, const long long *__restrict__ surv, long long m,
                         unsigned long long *__restrict__ key, V *__restrict__ val)
 {
     for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x) {
         const long long id = surv ? surv[j] : j; // NULL: every point of xy, in order
-        key[j] = okey(xy[2 * id + 1]);
+        key[j] = okey(xy[2 * id]);
         val[j] = (V)id;
     }
 }
 
+// Runs of equal x (numeric ==) in the x-sorted points: the thread at a run's
+// head scans it for the lowest point (min y, ties: lowest sort value) and the
+// highest (max y, ties: lowest sort value) and rewrites the run as [low, ...,
+// low, high].  Only those two can be strict hull vertices (every other point
+// of the run lies on the segment between them or equals one of them), the
+// result is sorted by (x, y), and the chains skip the copies (a point equal
+// to its sorted predecessor).  One thread per run: linear in the run length.
 template <typename V>
-__global__ void k_xkeys(const double *__restrict__ xy, const V *__restrict__ val, long long m,
-                        unsigned long long *__restrict__ key)
+__global__ void k_ties(double2 *__restrict__ P, V *__restrict__ val, long long m)
 {
-    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x)
-        key[j] = okey(xy[2 * (long long)val[j]]);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
+        const double x = P[i].x;
+        if ((i > 0 && P[i - 1].x == x) || i + 1 >= m || P[i + 1].x != x)
+            continue; // not the head of a run of >= 2
+        double2 lo = P[i], hi = lo;
+        V vlo = val[i], vhi = vlo;
+        long long e = i + 1;
+        for (; e < m; e++) {
+            const double2 q = P[e];
+            if (q.x != x)
+                break;
+            const V vq = val[e];
+            if (q.y < lo.y || (q.y == lo.y && vq < vlo)) {
+                lo = q;
+                vlo = vq;
+            }
+            if (q.y > hi.y || (q.y == hi.y && vq < vhi)) {
+                hi = q;
+                vhi = vq;
+            }
+        }
+        for (long long k = i; k < e - 1; k++) {
+            P[k] = lo;
+            val[k] = vlo;
+        }
+        P[e - 1] = hi;
+        val[e - 1] = vhi;
+    }
 }
 
 template <typename V>
@@ -354,20 +390,15 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
     auto *bi3 = (long long *)(b + L.o_bi3), *bj3 = (long long *)(b + L.o_bj3), *lm2 = (long long *)(b + L.o_lm2);
 
     const int g = grid_for(m, 256);
-    k_ykeys<V><<<g, 256, 0, st>>>(d_xy, surv, m, k0, v0);
+    k_xkeys<V><<<g, 256, 0, st>>>(d_xy, surv, m, k0, v0);
     cub::DoubleBuffer<unsigned long long> kb(k0, k1);
     cub::DoubleBuffer<V> vb(v0, v1);
     size_t tb = L.sort_tmp;
     if (cub::DeviceRadixSort::SortPairs(d_tmp, tb, kb, vb, (int64_t)m, 0, 64, st) != cudaSuccess)
         return CH_ERR_CUDA;
-    // x keys in the y-sorted order, then a stable sort by x
-    k_xkeys<V><<<g, 256, 0, st>>>(d_xy, vb.Current(), m, kb.Alternate());
-    kb.selector ^= 1;
-    tb = L.sort_tmp;
-    if (cub::DeviceRadixSort::SortPairs(d_tmp, tb, kb, vb, (int64_t)m, 0, 64, st) != cudaSuccess)
-        return CH_ERR_CUDA;
-    const V *val = vb.Current();
+    V *val = vb.Current();
     k_points<V><<<g, 256, 0, st>>>(d_xy, val, m, P);
+    k_ties<V><<<g, 256, 0, st>>>(P, val, m); // equal x: the run's lowest and highest points
 
     auto chains = [&](auto tag) {
         using I = decltype(tag);
