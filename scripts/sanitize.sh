@@ -11,6 +11,17 @@ for dist, n in (("displaced", 300_001), ("circle", 70_000), ("normal", 200_003),
     assert np.array_equal(s, want), dist
     chf.octagon_filter(xy, ws)
     hull, surv, st = chf.hull_end_to_end(xy, ws)
+# K2 with several super-tiles per CTA (buffer reuse without a block barrier,
+# the adaptive box), float64 and float32 storage
+for dist, n in (("displaced", 5_000_003), ("normal", 5_000_003), ("circle", 3_000_001)):
+    for st_ in ("f64", "f32"):
+        xy = synth.points(dist, n, seed=2, device="cuda")
+        if st_ == "f32":
+            xy = xy.float()
+        ws = chf.Workspace(n)
+        s = chf.filter(xy, ws).cpu().numpy()
+        want, _ = oracle.filter_compact(xy.double().cpu().numpy())
+        assert np.array_equal(s, want), (dist, st_)
 print("sanitize workload ok")
 PY
 for tool in memcheck racecheck synccheck; do
