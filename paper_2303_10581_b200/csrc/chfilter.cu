@@ -36,10 +36,10 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 
 #ifndef CH_K1_UNROLL_F
-#define CH_K1_UNROLL_F 6 // K1 wide loads (2 points each) per thread per chunk, float32 storage (8 spills at 80 registers)
+#define CH_K1_UNROLL_F 4 // K1 wide loads (CH_K1_PPL_F points each) per thread per chunk, float32 storage
 #endif
 #ifndef CH_K1_PPL_F
-#define CH_K1_PPL_F 2 // float32 points per K1 wide load: 2 (128 bits) or 4 (256 bits)
+#define CH_K1_PPL_F 4 // float32 points per K1 wide load: 2 (128 bits) or 4 (256 bits)
 #endif
 #ifndef CH_K1_MINB_F
 #define CH_K1_MINB_F 3 // K1 CTAs per SM for float32 storage
