@@ -941,3 +941,40 @@ def test_device_hull_randomized_sweep():
         got = chf.hull_gpu(d, torch.tensor(ids, dtype=torch.int64, device=DEV))
         want = oracle.hull(xy, ids)
         assert np.array_equal(got, want), (case, n, kind)
+
+
+def test_k1_f32_keys_rounding_ties():
+    """K1's float32 fast path compares fl32(x +- y) with the fp64 bests rounded
+    outward; inputs where fl32 and fl64 sums disagree must still give the
+    fp64 extremes (R1, lowest index on ties, R2).  Floats near 2^24 (sums not
+    representable in fp32); points exactly on x + y = 0.75 and x - y = 0.75
+    (fp64 ties, lowest index wins); and a point whose fp64 sum beats that
+    line by 2^-26 while its fp32 sum rounds onto it, at a high index."""
+    rng = np.random.default_rng(11)
+    cases = []
+    # 1. near 2^24: x + y needs 25+ bits
+    a = (np.float32(2 ** 24) + rng.integers(-64, 64, size=300_000)).astype(np.float32)
+    b = (rng.integers(-64, 64, size=300_000) + rng.choice([0.0, 0.5, 0.25], size=300_000)).astype(np.float32)
+    cases.append(np.stack([a, b], 1))
+    # 2. exact fp64 ties on the lines (t has 10 fraction bits, so 0.75 - t is exact)
+    t = (rng.integers(-1024, 1025, size=100_000) / 1024.0 * 0.25).astype(np.float32)
+    line = np.concatenate([np.stack([t, np.float32(0.75) - t], 1), np.stack([t, t - np.float32(0.75)], 1)])
+    noise = rng.uniform(-0.3, 0.3, size=(200_000, 2)).astype(np.float32)
+    pts = np.concatenate([noise, line]).astype(np.float32)
+    pts = pts[rng.permutation(len(pts))]
+    assert (pts[:, 0].astype(np.float64) + pts[:, 1]).max() == 0.75
+    cases.append(pts)
+    # 3. x = 1, y = -(1/4 - 2^-26): fp64 sum 0.75 + 2^-26, fp32 sum 0.75
+    c3 = pts.copy()
+    y3 = np.float32(-(0.25 - 2.0 ** -26))
+    assert float(y3) == -(0.25 - 2.0 ** -26) and np.float32(np.float32(1.0) + y3) == np.float32(0.75)
+    c3[-3] = (np.float32(1.0), y3)
+    cases.append(c3)
+    for xy in cases:
+        d = torch.tensor(xy, device=DEV)
+        ws = chf.Workspace(xy.shape[0])
+        e, _ = chf.extremes8(d, ws)
+        want, idx8 = oracle.filter_compact(xy.astype(np.float64))
+        assert np.array_equal(np.array(e.idx[:]), idx8)
+        assert np.array_equal(chf.filter(d).cpu().numpy(), want)
+    assert idx8[1] == len(c3) - 3   # the lone point is TR
