@@ -1764,34 +1764,41 @@ k2_filter_compact(const T *__restrict__ xy, long long n, long long index_base,
                 if (lane == 0)
                     mbar_arrive(&s_empty[st]); // this warp is done with stage st
             } else {
-            T px[K2_NP], py[K2_NP]; // storage precision; widened exactly where fp64 is needed
-            unsigned valid = (1u << K2_NP) - 1u;
+            // (the per-lane-mask path, in chunks of <= 8 points per thread so
+            // that its registers stay below consume_cert's; rare on the bench
+            // workloads, so the stage is held until the last chunk is read)
+            constexpr int CHK = K2_NP < 8 ? K2_NP : 8;
+#pragma unroll 1
+            for (int h0 = 0; h0 < K2_NP; h0 += CHK) {
+                T px[CHK], py[CHK]; // storage precision; widened exactly where fp64 is needed
+                unsigned valid = (1u << CHK) - 1u;
 #pragma unroll
-            for (int u = 0; u < K2_NP; u++) {
-                const V2 v = sp[u * K2_CTHREADS + tid];
-                px[u] = v.x;
-                py[u] = v.y;
-            }
-            if (copied < (int)K2_SUB) { // the partial last sub-tile (uniform branch)
-                valid = 0;
+                for (int u = 0; u < CHK; u++) {
+                    const V2 v = sp[(h0 + u) * K2_CTHREADS + tid];
+                    px[u] = v.x;
+                    py[u] = v.y;
+                }
+                if (copied < (int)K2_SUB) { // the partial last sub-tile (uniform branch)
+                    valid = 0;
 #pragma unroll
-                for (int u = 0; u < K2_NP; u++) {
-                    const int q = u * K2_CTHREADS + tid;
-                    if (q >= copied && base + q < n)
-                        ld1raw(xy, base + q, px[u], py[u]); // odd float tail point
-                    valid |= (base + q < n ? 1u : 0u) << u;
+                    for (int u = 0; u < CHK; u++) {
+                        const int q = (h0 + u) * K2_CTHREADS + tid;
+                        if (q >= copied && base + q < n)
+                            ld1raw(xy, base + q, px[u], py[u]); // odd float tail point
+                        valid |= (base + q < n ? 1u : 0u) << u;
+                    }
+                }
+                const unsigned keep = so.degenerate ? valid : classify<T, CHK>(so, px, py, valid, guess_mode);
+#pragma unroll
+                for (int u = 0; u < CHK; u++) {
+                    const unsigned m = __ballot_sync(FULL, keep & (1u << u));
+                    if (lane == 0)
+                        bw[h0 + u] = m;
                 }
             }
             __syncwarp();
             if (lane == 0)
                 mbar_arrive(&s_empty[st]); // this warp is done with stage st
-            const unsigned keep = so.degenerate ? valid : classify<T, K2_NP>(so, px, py, valid, guess_mode);
-#pragma unroll
-            for (int u = 0; u < K2_NP; u++) {
-                const unsigned m = __ballot_sync(FULL, keep & (1u << u));
-                if (lane == 0)
-                    bw[u] = m;
-            }
             }
             if (j == nsub - 1) {
                 // ---- end of super-tile: group prefix (block scan) + aggregate ----
