@@ -5,13 +5,17 @@
 // The exact strict hull of the survivors (DESIGN R8: CCW from the
 // lexicographic minimum, duplicates -> lowest id, collinear points excluded),
 // identical to the host monotone chain and the oracle:
-//   1. sort the survivors by x (one radix sort on order-preserving 64-bit
-//      keys, -0.0 folded into +0.0), then resolve every run of equal x in
-//      place (k_ties): only the run's lowest point (min y, then lowest id)
-//      and highest point (max y, then lowest id) can be strict hull
-//      vertices -- the points between them lie inside a vertical segment --
-//      so the run becomes [low, low, ..., low, high], which is sorted by
-//      (x, y) and whose copies the chains skip as duplicates;
+//   1. sort the survivors by x: a hand-written LSD radix sort (radix_sort.cuh,
+//      four 8-bit onesweep passes) on 32-bit keys that quantise x linearly
+//      and monotonically over the survivors' x range, then every run of equal
+//      keys sorted by x exactly (a thread per short run, a CTA per long one,
+//      which runs the same radix ranking on the 64-bit order-preserving keys
+//      of x, -0.0 folded into +0.0); in the same step every run of equal x is
+//      resolved: only the run's lowest point (min y, then lowest id) and
+//      highest point (max y, then lowest id) can be strict hull vertices --
+//      the points between them lie inside a vertical segment -- so the run
+//      becomes [low, low, ..., low, high], which is sorted by (x, y) and
+//      whose copies the chains skip as duplicates;
 //   2. lower and upper chains: one thread per chunk of HG_CHUNK sorted points
 //      runs Andrew's monotone chain (pop while the exact turn is <= 0,
 //      chf::orient_sign; a point equal to its sorted predecessor is skipped,
@@ -26,7 +30,6 @@
 // group span is a power of two).
 #include <cuda_runtime.h>
 
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cstdint>
@@ -34,6 +37,8 @@
 
 #include "../../include/chfilter.h"
 #include "exact.cuh"
+#include "internal.h"
+#include "radix_sort.cuh"
 
 namespace {
 
@@ -47,39 +52,133 @@ __device__ __forceinline__ unsigned long long okey(double d)
     return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
 }
 
-template <typename V>
-__global__ void k_xkeys(const double *__restrict__ xy, const long long *__restrict__ surv, long long m,
-                        unsigned long long *__restrict__ key, V *__restrict__ val)
+__device__ __forceinline__ double okey_inv(unsigned long long k)
 {
+    return __longlong_as_double((long long)((k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+__device__ __forceinline__ unsigned long long shfl_xor64(unsigned long long v, int o)
+{
+    return __shfl_xor_sync(0xffffffffu, v, o);
+}
+
+// Sort values (survivor ids, or positions when surv == NULL) and their x to X,
+// plus min / max of x as order-preserving keys (mm[0] min, mm[1] max; the
+// caller sets them to ~0 and 0).
+template <typename V>
+__global__ void k_gather_x(const double *__restrict__ xy, const long long *__restrict__ surv, long long m,
+                           double *__restrict__ X, V *__restrict__ val, unsigned long long *__restrict__ mm)
+{
+    unsigned long long lo = ~0ull, hi = 0;
     for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x) {
         const long long id = surv ? surv[j] : j; // NULL: every point of xy, in order
-        key[j] = okey(xy[2 * id]);
+        const double x = xy[2 * id];
+        X[j] = x;
         val[j] = (V)id;
+        const unsigned long long o = okey(x);
+        lo = o < lo ? o : lo;
+        hi = o > hi ? o : hi;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = shfl_xor64(lo, o), b = shfl_xor64(hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], lo);
+        atomicMax(&mm[1], hi);
     }
 }
 
-// Runs of equal x (numeric ==) in the x-sorted points: the thread at a run's
-// head scans it for the lowest point (min y, ties: lowest sort value) and the
-// highest (max y, ties: lowest sort value) and rewrites the run as [low, ...,
-// low, high].  Only those two can be strict hull vertices (every other point
-// of the run lies on the segment between them or equals one of them), the
-// result is sorted by (x, y), and the chains skip the copies (a point equal
-// to its sorted predecessor).  One thread per run: linear in the run length.
-template <typename V>
-__global__ void k_ties(double2 *__restrict__ P, V *__restrict__ val, long long m)
+// The 32-bit sort key: x quantised linearly over [lo, hi] of the survivors,
+// floor((x/2 - lo/2) * (2^32 - 256) / (hi/2 - lo/2)), every operation rounded
+// to nearest (monotone), so x1 < x2 implies key1 <= key2 and key1 < key2
+// implies x1 < x2: sorting by the key puts the points in x order up to runs
+// of equal keys, which k_fix_runs / k_fix_big then sort by x exactly.  The
+// halves keep hi/2 - lo/2 finite; equal x (also -0.0 / +0.0) gives equal keys.
+struct Quant {
+    double h_lo, s;
+};
+__device__ __forceinline__ Quant quant_params(const unsigned long long *mm)
 {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
-        const double x = P[i].x;
-        if ((i > 0 && P[i - 1].x == x) || i + 1 >= m || P[i + 1].x != x)
-            continue; // not the head of a run of >= 2
-        double2 lo = P[i], hi = lo;
-        V vlo = val[i], vhi = vlo;
-        long long e = i + 1;
-        for (; e < m; e++) {
-            const double2 q = P[e];
-            if (q.x != x)
-                break;
-            const V vq = val[e];
+    const double lo = okey_inv(mm[0]), hi = okey_inv(mm[1]);
+    const double h_lo = __dmul_rn(lo, 0.5);
+    const double d = __dsub_rn(__dmul_rn(hi, 0.5), h_lo);
+    const double s = d > 0.0 ? fmin(__ddiv_rn(4294967040.0, d), 1.7976931348623157e308) : 0.0;
+    return {h_lo, s};
+}
+__device__ __forceinline__ unsigned quant(double x, const Quant &q)
+{
+    const double t = __dmul_rn(__dsub_rn(__dmul_rn(x, 0.5), q.h_lo), q.s);
+    return (unsigned)fmin(floor(t), 4294967295.0);
+}
+
+// Keys from X, and the 256-bin histogram of each of the four 8-bit digits
+// (hist[4][256], zeroed by the caller).  HG_KH_ITEMS loads in flight per
+// thread; plain shared-memory atomics (lanes of a warp collide only on equal
+// digits).
+constexpr int HG_KH_ITEMS = 8;
+__global__ void __launch_bounds__(256) k_keys_hist(const double *__restrict__ X, long long m,
+                                                   const unsigned long long *__restrict__ mm, unsigned *__restrict__ key,
+                                                   unsigned long long *__restrict__ hist)
+{
+    __shared__ unsigned h[4][chrs::RS_BINS];
+    for (int b = threadIdx.x; b < 4 * chrs::RS_BINS; b += blockDim.x)
+        (&h[0][0])[b] = 0;
+    __syncthreads();
+    const Quant q = quant_params(mm);
+    const long long stride = (long long)gridDim.x * blockDim.x * HG_KH_ITEMS;
+    for (long long j0 = (long long)blockIdx.x * blockDim.x * HG_KH_ITEMS + threadIdx.x; j0 < m; j0 += stride) {
+        double x[HG_KH_ITEMS];
+#pragma unroll
+        for (int u = 0; u < HG_KH_ITEMS; u++) {
+            const long long j = j0 + (long long)u * blockDim.x;
+            x[u] = j < m ? X[j] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < HG_KH_ITEMS; u++) {
+            const long long j = j0 + (long long)u * blockDim.x;
+            if (j < m) {
+                const unsigned k = quant(x[u], q);
+                key[j] = k;
+#pragma unroll
+                for (int p = 0; p < 4; p++)
+                    atomicAdd(&h[p][(k >> (8 * p)) & 255u], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < 4 * chrs::RS_BINS; b += blockDim.x) {
+        const unsigned c = (&h[0][0])[b];
+        if (c)
+            atomicAdd(&hist[b], (unsigned long long)c);
+    }
+}
+
+template <typename V>
+__global__ void k_points(const double *__restrict__ xy, const V *__restrict__ val, long long m,
+                         double2 *__restrict__ P)
+{
+    const double2 *__restrict__ xy2 = reinterpret_cast<const double2 *>(xy);
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x)
+        P[j] = xy2[(long long)val[j]];
+}
+
+// Runs of equal x (numeric ==) inside [a, e), which is sorted by x: each run
+// of >= 2 becomes [low, ..., low, high] -- low = min y (ties: lowest sort
+// value), high = max y (ties: lowest sort value).  Only those two can be
+// strict hull vertices (every other point of the run lies on the segment
+// between them or equals one of them); the result is sorted by (x, y) and the
+// chains skip the copies (a point equal to its sorted predecessor).
+template <typename V> __device__ __forceinline__ void ties_local(double2 *p, V *v, int L)
+{
+    for (int i = 0; i < L;) {
+        int e = i + 1;
+        double2 lo = p[i], hi = lo;
+        V vlo = v[i], vhi = vlo;
+        for (; e < L && p[e].x == p[i].x; e++) {
+            const double2 q = p[e];
+            const V vq = v[e];
             if (q.y < lo.y || (q.y == lo.y && vq < vlo)) {
                 lo = q;
                 vlo = vq;
@@ -89,22 +188,260 @@ __global__ void k_ties(double2 *__restrict__ P, V *__restrict__ val, long long m
                 vhi = vq;
             }
         }
-        for (long long k = i; k < e - 1; k++) {
-            P[k] = lo;
-            val[k] = vlo;
+        if (e - i >= 2) {
+            for (int k = i; k < e - 1; k++) {
+                p[k] = lo;
+                v[k] = vlo;
+            }
+            p[e - 1] = hi;
+            v[e - 1] = vhi;
         }
-        P[e - 1] = hi;
-        val[e - 1] = vhi;
+        i = e;
+    }
+}
+template <typename V> __device__ void ties_global(double2 *P, V *val, long long i, long long e)
+{
+    double2 lo = P[i], hi = lo;
+    V vlo = val[i], vhi = vlo;
+    for (long long k = i + 1; k < e; k++) {
+        const double2 q = P[k];
+        const V vq = val[k];
+        if (q.y < lo.y || (q.y == lo.y && vq < vlo)) {
+            lo = q;
+            vlo = vq;
+        }
+        if (q.y > hi.y || (q.y == hi.y && vq < vhi)) {
+            hi = q;
+            vhi = vq;
+        }
+    }
+    for (long long k = i; k < e - 1; k++) {
+        P[k] = lo;
+        val[k] = vlo;
+    }
+    P[e - 1] = hi;
+    val[e - 1] = vhi;
+}
+
+// Runs of equal 32-bit key in the key-sorted points.  A run of at most
+// HG_SMALL_RUN is sorted by x (insertion sort) and its equal-x runs resolved
+// (ties_local) by the thread at its head; a longer one is queued for
+// k_fix_big (runs[2 r] = start, runs[2 r + 1] = length).
+constexpr int HG_SMALL_RUN = 32;
+template <typename V>
+__global__ void k_fix_runs(const unsigned *__restrict__ key, double2 *__restrict__ P, V *__restrict__ val, long long m,
+                           long long *__restrict__ runs, unsigned long long *__restrict__ nruns)
+{
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned k = key[i];
+        if ((i > 0 && key[i - 1] == k) || i + 1 >= m || key[i + 1] != k)
+            continue; // not the head of a run of >= 2
+        long long e = i + 2;
+        while (e < m && e - i <= HG_SMALL_RUN && key[e] == k)
+            e++;
+        if (e - i > HG_SMALL_RUN) {
+            while (e < m && key[e] == k)
+                e++;
+            const unsigned long long r = atomicAdd(nruns, 1ull);
+            runs[2 * r] = i;
+            runs[2 * r + 1] = e - i;
+            continue;
+        }
+        const int L = (int)(e - i);
+        if (L == 2) { // the common case, in registers
+            double2 p0 = P[i], p1 = P[i + 1];
+            V v0 = val[i], v1 = val[i + 1];
+            if (p1.x < p0.x || (p1.x == p0.x && (p1.y < p0.y || (p1.y == p0.y && v1 < v0)))) {
+                const double2 tp = p0;
+                p0 = p1;
+                p1 = tp;
+                const V tv = v0;
+                v0 = v1;
+                v1 = tv;
+            }
+            // equal x: [low, high] is the (x, y, value) order, except for
+            // equal points, where high takes the lowest value too
+            if (p1.x == p0.x && p1.y == p0.y)
+                v1 = v0;
+            P[i] = p0;
+            P[i + 1] = p1;
+            val[i] = v0;
+            val[i + 1] = v1;
+            continue;
+        }
+        double2 p[HG_SMALL_RUN];
+        V v[HG_SMALL_RUN];
+        for (int t = 0; t < L; t++) { // insertion sort by x (equal x in any order)
+            const double2 q = P[i + t];
+            const V vq = val[i + t];
+            int u = t;
+            for (; u > 0 && p[u - 1].x > q.x; u--) {
+                p[u] = p[u - 1];
+                v[u] = v[u - 1];
+            }
+            p[u] = q;
+            v[u] = vq;
+        }
+        ties_local(p, v, L);
+        for (int t = 0; t < L; t++) {
+            P[i + t] = p[t];
+            val[i + t] = v[t];
+        }
     }
 }
 
+// The long runs, one CTA per run (grid-stride over the queue): 64-bit
+// order-preserving keys of x, a single-CTA LSD sort over the digits where the
+// run's keys differ (chrs::cta_sort_pass), the points and values permuted by
+// the sorted positions (through ka/kb, free by now), then the equal-x runs.
+// A run whose x are all equal is one equal-x run (a block-wide lowest/highest
+// point).  Scratch at the run's own positions [a, a + L): ka, kb (8-byte
+// words), ia, ib (32-bit positions; a run is shorter than 2^32).
 template <typename V>
-__global__ void k_points(const double *__restrict__ xy, const V *__restrict__ val, long long m,
-                         double2 *__restrict__ P)
+__global__ void __launch_bounds__(chrs::RS_THREADS) k_fix_big(double2 *__restrict__ P, V *__restrict__ val,
+                                                            const long long *__restrict__ runs,
+                                                            const unsigned long long *__restrict__ nruns,
+                                                            unsigned long long *ka, unsigned long long *kb,
+                                                            unsigned *ia, unsigned *ib)
 {
-    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x) {
-        const long long id = (long long)val[j];
-        P[j] = make_double2(xy[2 * id], xy[2 * id + 1]);
+    using S = chrs::TileSmem<unsigned long long, unsigned>;
+    extern __shared__ __align__(16) unsigned char fb_smem[];
+    S &s = *reinterpret_cast<S *>(fb_smem);
+    const long long nr = (long long)*nruns;
+    for (long long r = blockIdx.x; r < nr; r += gridDim.x) {
+        const long long a = runs[2 * r], L = runs[2 * r + 1];
+        unsigned long long lo = ~0ull, hi = 0;
+        for (long long t = threadIdx.x; t < L; t += blockDim.x) {
+            const unsigned long long o = okey(P[a + t].x);
+            ka[a + t] = o;
+            ia[a + t] = (unsigned)t;
+            lo = o < lo ? o : lo;
+            hi = o > hi ? o : hi;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long x0 = shfl_xor64(lo, o), x1 = shfl_xor64(hi, o);
+            lo = x0 < lo ? x0 : lo;
+            hi = x1 > hi ? x1 : hi;
+        }
+        if (threadIdx.x == 0) {
+            s.lo = ~0ull;
+            s.hi = 0;
+        }
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&s.lo, lo);
+            atomicMax(&s.hi, hi);
+        }
+        __syncthreads();
+        lo = s.lo;
+        hi = s.hi;
+        __syncthreads();
+        if (lo == hi) {
+            // one equal-x run: lowest and highest point, block-wide
+            double2 plo = P[a], phi = plo;
+            V vlo = val[a], vhi = vlo;
+            for (long long t = threadIdx.x; t < L; t += blockDim.x) {
+                const double2 q = P[a + t];
+                const V vq = val[a + t];
+                if (q.y < plo.y || (q.y == plo.y && vq < vlo)) {
+                    plo = q;
+                    vlo = vq;
+                }
+                if (q.y > phi.y || (q.y == phi.y && vq < vhi)) {
+                    phi = q;
+                    vhi = vq;
+                }
+            }
+            // per-thread candidates through the tile's shared arrays, combined by thread 0
+            double2 (*s_p)[chrs::RS_THREADS] = reinterpret_cast<double2 (*)[chrs::RS_THREADS]>(s.key);
+            V (*s_v)[chrs::RS_THREADS] = reinterpret_cast<V (*)[chrs::RS_THREADS]>(s.val);
+            s_p[0][threadIdx.x] = plo;
+            s_v[0][threadIdx.x] = vlo;
+            s_p[1][threadIdx.x] = phi;
+            s_v[1][threadIdx.x] = vhi;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int u = 1; u < chrs::RS_THREADS; u++) {
+                    const double2 q = s_p[0][u];
+                    const V vq = s_v[0][u];
+                    if (q.y < plo.y || (q.y == plo.y && vq < vlo)) {
+                        plo = q;
+                        vlo = vq;
+                    }
+                    const double2 q2 = s_p[1][u];
+                    const V vq2 = s_v[1][u];
+                    if (q2.y > phi.y || (q2.y == phi.y && vq2 < vhi)) {
+                        phi = q2;
+                        vhi = vq2;
+                    }
+                }
+                s_p[0][0] = plo;
+                s_v[0][0] = vlo;
+                s_p[1][0] = phi;
+                s_v[1][0] = vhi;
+            }
+            __syncthreads();
+            plo = s_p[0][0];
+            vlo = s_v[0][0];
+            phi = s_p[1][0];
+            vhi = s_v[1][0];
+            for (long long t = threadIdx.x; t < L - 1; t += blockDim.x) {
+                P[a + t] = plo;
+                val[a + t] = vlo;
+            }
+            if (threadIdx.x == 0) {
+                P[a + L - 1] = phi;
+                val[a + L - 1] = vhi;
+            }
+            __syncthreads();
+            continue;
+        }
+        // LSD passes over the bytes below the highest differing bit
+        const int top = 63 - __clzll((long long)(lo ^ hi));
+        unsigned long long *kin = ka, *kout = kb;
+        unsigned *iin = ia, *iout = ib;
+        for (int shift = 0; shift <= top; shift += 8) {
+            if (chrs::cta_sort_pass<unsigned long long, unsigned>(s, kin, kout, iin, iout, a, L, shift)) {
+                unsigned long long *tk = kin;
+                kin = kout;
+                kout = tk;
+                unsigned *ti = iin;
+                iin = iout;
+                iout = ti;
+            }
+            __syncthreads();
+        }
+        // permute: positions iin[a + t] (run-relative) in x order, staged in
+        // the run's own 8-byte words of ka / kb (free now)
+        double *tx = reinterpret_cast<double *>(ka + a), *ty = reinterpret_cast<double *>(kb + a);
+        const unsigned *srt = iin + a;
+        for (long long t = threadIdx.x; t < L; t += blockDim.x) {
+            const double2 q = P[a + srt[t]];
+            tx[t] = q.x;
+            ty[t] = q.y;
+        }
+        __syncthreads();
+        for (long long t = threadIdx.x; t < L; t += blockDim.x)
+            P[a + t] = make_double2(tx[t], ty[t]);
+        __syncthreads();
+        V *tv = reinterpret_cast<V *>(ka + a); // sizeof(V) <= 8
+        for (long long t = threadIdx.x; t < L; t += blockDim.x)
+            tv[t] = val[a + srt[t]];
+        __syncthreads();
+        for (long long t = threadIdx.x; t < L; t += blockDim.x)
+            val[a + t] = tv[t];
+        __syncthreads();
+        // equal-x runs inside the sorted run, one thread per run head
+        for (long long t = threadIdx.x; t < L; t += blockDim.x) {
+            const double x = P[a + t].x;
+            if ((t > 0 && P[a + t - 1].x == x) || t + 1 >= L || P[a + t + 1].x != x)
+                continue;
+            long long e = t + 2;
+            while (e < L && P[a + e].x == x)
+                e++;
+            ties_global(P, val, a + t, a + e);
+        }
+        __syncthreads();
     }
 }
 
@@ -340,22 +677,23 @@ static I *chain_gpu(const double2 *P, long long m, int rev, I *pos_a, I *pos_b, 
 }
 
 // Scratch layout of ch_hull_gpu_async for m survivors (all 256-B aligned).
+// The radix sort's control block (status words, histograms, tickets, min /
+// max, the long-run count) is contiguous so one memset clears it.
 struct HullTmp {
-    size_t sort_tmp = 0, total = 0;
+    size_t total = 0;
     size_t o_k0, o_k1, o_v0, o_v1, o_P, o_pa, o_pb, o_pc, o_pd, o_la, o_lb, o_lc, o_ld, o_bi, o_bj, o_out;
-    size_t o_bi2, o_bj2, o_lm, o_bi3, o_bj3, o_lm2;
+    size_t o_bi2, o_bj2, o_lm, o_bi3, o_bj3, o_lm2, o_runs, o_ctl, ctl_bytes;
+    size_t o_hist, o_tk, o_mm, o_nruns; // inside the control block
+    long long ntiles;
     explicit HullTmp(long long m)
     {
         if (m < 1)
             m = 1;
         const size_t nchunks = (size_t)((m + HG_CHUNK - 1) / HG_CHUNK), cap = nchunks * HG_CHUNK;
         const size_t isz = m < (1ll << 32) ? 4 : 8; // chain position width
-        cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
-        cub::DoubleBuffer<long long> vb(nullptr, nullptr);
-        cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, kb, vb, (int64_t)m);
+        ntiles = (m + chrs::RS_TILE - 1) / chrs::RS_TILE;
         size_t p = 0;
         auto take = [&](size_t b) { const size_t o = p; p += (b + 255) & ~(size_t)255; return o; };
-        take(sort_tmp);
         o_k0 = take((size_t)m * 8); o_k1 = take((size_t)m * 8);
         o_v0 = take((size_t)m * 8); o_v1 = take((size_t)m * 8);
         o_P = take((size_t)m * 16);
@@ -366,9 +704,24 @@ struct HullTmp {
         o_bi2 = take(nchunks * 8 + 8); o_bj2 = take(nchunks * 8 + 8); o_lm = take(nchunks * 8 + 8);
         o_bi3 = take(nchunks * 8 + 8); o_bj3 = take(nchunks * 8 + 8); o_lm2 = take(nchunks * 8 + 8);
         o_out = take((size_t)m * 8 + 8);
+        o_runs = take(((size_t)m / (HG_SMALL_RUN + 1) + 1) * 16);
+        // control block: status | hist[4][256] | tickets[4] | mm[2] | nruns
+        const size_t st = (size_t)ntiles * chrs::RS_BINS * 8;
+        o_hist = st;
+        o_tk = o_hist + 4 * chrs::RS_BINS * 8;
+        o_mm = o_tk + 4 * 8;
+        o_nruns = o_mm + 2 * 8;
+        ctl_bytes = o_nruns + 8;
+        o_ctl = take(ctl_bytes);
         total = p;
     }
 };
+
+template <typename F> static void set_smem(F *f, size_t bytes)
+{
+    if (bytes > 48 * 1024)
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 
 // The pipeline with sort values (survivor ids) of type V.
 template <typename V>
@@ -389,16 +742,43 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
     auto *bi2 = (long long *)(b + L.o_bi2), *bj2 = (long long *)(b + L.o_bj2), *lm = (long long *)(b + L.o_lm);
     auto *bi3 = (long long *)(b + L.o_bi3), *bj3 = (long long *)(b + L.o_bj3), *lm2 = (long long *)(b + L.o_lm2);
 
+    auto *ctl = (unsigned char *)(b + L.o_ctl);
+    auto *status = (unsigned long long *)ctl;
+    auto *hist = (unsigned long long *)(ctl + L.o_hist);
+    auto *tk = (unsigned long long *)(ctl + L.o_tk);
+    auto *mm = (unsigned long long *)(ctl + L.o_mm);
+    auto *nruns = (unsigned long long *)(ctl + L.o_nruns);
+    auto *runs = (long long *)(b + L.o_runs);
+    if (cudaMemsetAsync(ctl, 0, L.ctl_bytes, st) != cudaSuccess || cudaMemsetAsync(mm, 0xff, 8, st) != cudaSuccess)
+        return chi::fail(CH_ERR_CUDA, "device hull: memset");
+
+    // 1. x and the sort values, min / max of x; 2. 32-bit keys + histograms
     const int g = grid_for(m, 256);
-    k_xkeys<V><<<g, 256, 0, st>>>(d_xy, surv, m, k0, v0);
-    cub::DoubleBuffer<unsigned long long> kb(k0, k1);
-    cub::DoubleBuffer<V> vb(v0, v1);
-    size_t tb = L.sort_tmp;
-    if (cub::DeviceRadixSort::SortPairs(d_tmp, tb, kb, vb, (int64_t)m, 0, 64, st) != cudaSuccess)
-        return CH_ERR_CUDA;
-    V *val = vb.Current();
+    double *X = (double *)k0;
+    auto *keyA = (unsigned *)k1, *keyB = (unsigned *)k0;
+    k_gather_x<V><<<g, 256, 0, st>>>(d_xy, surv, m, X, v0, mm);
+    k_keys_hist<<<std::min(g, 148 * 4), 256, 0, st>>>(X, m, mm, keyA, hist);
+    // 3. four stable 8-bit passes (keys k1 -> k0 -> k1 -> k0 -> k1, values v0 -> v1 -> ... -> v0)
+    const size_t smem = sizeof(chrs::TileSmem<unsigned, V>);
+    auto pass_kernel = m <= 0xffffffffll ? chrs::k_rs_pass<unsigned, V, unsigned> : chrs::k_rs_pass<unsigned, V, long long>;
+    set_smem(pass_kernel, smem);
+    unsigned *kin = keyA, *kout = keyB;
+    V *vin = v0, *vout = v1;
+    for (int pass = 0; pass < 4; pass++) {
+        pass_kernel<<<(unsigned)L.ntiles, chrs::RS_THREADS, smem, st>>>(kin, kout, vin, vout, m, 8 * pass, pass,
+                                                                     hist + pass * chrs::RS_BINS, status, tk + pass);
+        std::swap(kin, kout);
+        std::swap(vin, vout);
+    }
+    V *val = vin; // == v0
+    // 4. the points in key order; runs of equal key sorted by x exactly, equal x resolved
     k_points<V><<<g, 256, 0, st>>>(d_xy, val, m, P);
-    k_ties<V><<<g, 256, 0, st>>>(P, val, m); // equal x: the run's lowest and highest points
+    k_fix_runs<V><<<g, 256, 0, st>>>(kin, P, val, m, runs, nruns);
+    const size_t fsmem = sizeof(chrs::TileSmem<unsigned long long, unsigned>);
+    set_smem(k_fix_big<V>, fsmem);
+    k_fix_big<V><<<148 * 2, chrs::RS_THREADS, fsmem, st>>>(P, val, runs, nruns, (unsigned long long *)k0,
+                                                          (unsigned long long *)k1, (unsigned *)v1,
+                                                          (unsigned *)v1 + m);
 
     auto chains = [&](auto tag) {
         using I = decltype(tag);
@@ -411,7 +791,8 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
         chains((unsigned)0);
     else
         chains((long long)0);
-    return cudaGetLastError() == cudaSuccess ? CH_OK : CH_ERR_CUDA;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? CH_OK : chi::fail(CH_ERR_CUDA, std::string("device hull: ") + cudaGetErrorString(e));
 }
 
 extern "C" {
@@ -491,8 +872,9 @@ ch_status ch_hull_gpu(const double *d_xy, int64_t n_points, const int64_t *d_sur
     cudaStreamSynchronize(st);
     cudaMemcpyAsync(h_hull, d_out, (size_t)nh * 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    if (cudaGetLastError() != cudaSuccess)
-        return CH_ERR_CUDA;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return chi::fail(CH_ERR_CUDA, std::string("ch_hull_gpu: ") + cudaGetErrorString(e));
     *h_n_hull = nh;
     return CH_OK;
 }

@@ -943,6 +943,68 @@ def test_device_hull_randomized_sweep():
         assert np.array_equal(got, want), (case, n, kind)
 
 
+def _quantum_cluster_sets():
+    """Point sets whose x collide in the device hull's 32-bit sort key (x
+    quantised over the survivors' x range, 2^32 - 256 steps): the equal-key
+    runs must then be sorted by the exact x (short runs by one thread, long
+    ones by one CTA with a 64-bit radix sort over the run)."""
+    rng = np.random.default_rng(2024)
+    base = rng.random((20_000, 2))
+    # 1. a long run of distinct x inside one quantum (~2.3e-10 wide), several tiles long
+    c = np.stack([0.5 + rng.random(50_000) * 1e-12, rng.random(50_000)], 1)
+    yield "cluster50k", np.concatenate([base, c])
+    # 2. one tile or less: 40 and 4097 points in one quantum, next to each other
+    c1 = np.stack([0.25 + rng.random(40) * 1e-13, rng.random(40)], 1)
+    c2 = np.stack([0.75 + rng.random(4097) * 1e-13, rng.random(4097) * 3 - 1], 1)
+    yield "clusters40_4097", np.concatenate([base, c1, c2])
+    # 3. a giant vertical line (every x equal): one equal-x run, resolved block-wide
+    v = np.stack([np.full(120_000, 0.125), rng.random(120_000) * 4 - 2], 1)
+    yield "vertical120k", np.concatenate([base, v])
+    # 4. x = -tiny, -0.0, +0.0, +tiny around 0 in [-1, 1]: one key, order-preserving 64-bit keys that
+    #    differ in their top byte (8 digit passes), duplicates among them
+    t = rng.choice([-1e-300, -0.0, 0.0, 1e-300, 5e-324, -5e-324], size=3000)
+    z = np.stack([t, rng.integers(-3, 4, size=3000) / 4.0], 1)
+    yield "signed_tiny", np.concatenate([rng.random((5000, 2)) * 2 - 1, z])
+    # 5. many short runs with equal x inside (ties inside a run of the fast path)
+    xs = np.round(rng.random(200_000), 12)
+    yield "rounded12", np.stack([xs, rng.random(200_000)], 1)
+    # 6. two distinct x values only, both long runs of equal x, keys 0 and 2^32 - 256
+    yield "two_columns", np.stack([rng.integers(0, 2, 70_000) * 1.0, rng.random(70_000)], 1)
+    # 7. a circle where runs of the same key hold whole arcs: x range 1, points within 1e-9 of x = +-1
+    th = rng.random(300_000) * 1e-4
+    circ = np.stack([np.cos(th), np.sin(th)], 1)
+    yield "circle_cap", np.concatenate([circ, -circ, [[0.0, 0.0]]])
+
+
+def test_device_hull_equal_key_runs():
+    """The device hull's sort (hand-written radix sort on quantised keys, then
+    the exact x order inside equal-key runs) on inputs built to make long and
+    short equal-key runs, equal-x runs inside them, and an all-equal run:
+    every hull equals the oracle's exact hull, for all points as candidates
+    and for a subset, and through the 64-bit sort-value instantiation."""
+    import ctypes
+    lib = chf._lib.load()
+    for name, xy in _quantum_cluster_sets():
+        n = len(xy)
+        d = torch.tensor(xy, device=DEV)
+        for sub in (False, True):
+            ids = np.arange(n) if not sub else np.sort(np.random.default_rng(n).choice(n, n - n // 5, replace=False))
+            idt = torch.tensor(ids, dtype=torch.int64, device=DEV)
+            got = chf.hull_gpu(d, idt)
+            want = oracle.hull(xy, ids)
+            assert np.array_equal(got, want), (name, sub)
+        m = n
+        tb = int(lib.ch_hull_gpu_temp_bytes(m))
+        tmp = torch.empty(tb, dtype=torch.uint8, device=DEV)
+        out = np.zeros(m, dtype=np.int64)
+        h = ctypes.c_int64(0)
+        allids = torch.arange(n, dtype=torch.int64, device=DEV)
+        st = lib.ch_hull_gpu(chf._ptr(d), (1 << 33) + 1, chf._ptr(allids), m, out.ctypes.data_as(ctypes.c_void_p),
+                             ctypes.byref(h), chf._ptr(tmp), tb, chf._stream(None))
+        assert st == 0
+        assert np.array_equal(out[: h.value], oracle.hull(xy)), (name, "64-bit values")
+
+
 def test_k1_f32_keys_rounding_ties():
     """K1's float32 fast path compares fl32(x +- y) with the fp64 bests rounded
     outward; inputs where fl32 and fl64 sums disagree must still give the
