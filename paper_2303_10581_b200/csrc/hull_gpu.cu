@@ -16,7 +16,7 @@
 //      the points between them lie inside a vertical segment -- so the run
 //      becomes [low, low, ..., low, high], which is sorted by (x, y) and
 //      whose copies the chains skip as duplicates;
-//   2. lower and upper chains: one thread per chunk of HG_CHUNK sorted points
+//   2. lower and upper chains: one thread per chunk of 2^chunk_log2(m) sorted points
 //      runs Andrew's monotone chain (pop while the exact turn is <= 0,
 //      chf::orient_sign; a point equal to its sorted predecessor is skipped,
 //      so the lowest id survives); the upper chain is the same routine on the
@@ -32,6 +32,8 @@
 
 
 #include <algorithm>
+#include <cmath>
+#include <string>
 #include <cstdint>
 #include <vector>
 
@@ -42,7 +44,17 @@
 
 namespace {
 
-constexpr long long HG_CHUNK = 512;
+// Points per chunk chain: a power of two from 16 (few survivors: enough
+// threads for the serial walks) to 512 (many: fewer merge levels).
+constexpr int HG_LGC_MIN = 4, HG_LGC_MAX = 9;
+constexpr long long HG_FLAT_M = 1ll << 22; // fewer sorted points: every merge level materialised
+inline int chunk_log2(long long m)
+{
+    int lgc = HG_LGC_MIN;
+    while (lgc < HG_LGC_MAX && (m >> (lgc + 16)) > 0) // ~2^16 chunks or more before it doubles
+        lgc++;
+    return lgc;
+}
 constexpr int HG_THREADS = 128;
 
 __device__ __forceinline__ unsigned long long okey(double d)
@@ -445,18 +457,205 @@ __global__ void __launch_bounds__(chrs::RS_THREADS) k_fix_big(double2 *__restric
     }
 }
 
+// ------------------------------------------------ second filtering round --
+// Before the sort (ch_hull_gpu only: it synchronizes anyway), the survivors
+// are filtered once more, Akl-Toussaint style with HG_DIRS directions instead
+// of the octagon's 8: the approximate extremes of a strided sample in HG_DIRS
+// directions (fp32 dot products; any input points will do) form a polygon
+// V[0..nv) of input points, and a survivor p is discarded only if it lies
+// STRICTLY inside a fan triangle (V[0], V[j], V[j+1]), decided by the exact
+// orientation sign (chf::orient_sign) on all three edges.  Strictly inside a
+// triangle of input points is strictly inside their hull, so p is neither a
+// hull vertex nor on the hull boundary: the hull of the rest is the hull of
+// the survivors, whatever the polygon looks like (the fp64 binary search for j
+// only picks the triangle to test).  On ring-like survivors (C4) this removes
+// most of them; on a circle (every survivor a hull vertex) nothing, and the
+// original list is used.
+constexpr int HG_DIRS = 64;
+constexpr long long HG_REFINE_MIN = 1ll << 16; // fewer survivors: no second round
+constexpr long long HG_SAMPLE = 1ll << 18;     // sample the direction extremes are taken over
+struct Dirs {
+    float u[HG_DIRS][2];
+};
+struct RefinePoly { // device scratch
+    double2 v[HG_DIRS];
+    int nv;
+};
+
+// best[k] = max over the sample of (orderable fp32 u_k . p) << 32 | sample
+// index (zeroed by the caller).  Thread t of a 64-thread group owns direction
+// t % 64; the group's threads read the same point (one broadcast load).
+__global__ void __launch_bounds__(256) k_dir_extremes(const double *__restrict__ xy, const long long *__restrict__ surv,
+                                                      long long stride, long long nsample, const Dirs D,
+                                                      unsigned long long *__restrict__ best)
+{
+    const int k = threadIdx.x % HG_DIRS;
+    const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / HG_DIRS;
+    const long long ng = (long long)gridDim.x * blockDim.x / HG_DIRS;
+    const float ux = D.u[k][0], uy = D.u[k][1];
+    unsigned long long b = 0;
+    for (long long s0 = g; s0 < nsample; s0 += 4 * ng) { // four points' loads in flight
+        long long id[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const long long s = s0 + u * ng;
+            id[u] = s < nsample ? (surv ? surv[s * stride] : s * stride) : -1;
+        }
+        double2 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            q[u] = id[u] >= 0 ? reinterpret_cast<const double2 *>(xy)[id[u]] : make_double2(0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            if (id[u] < 0)
+                continue;
+            const float d = __fmaf_rn(ux, (float)q[u].x, __fmul_rn(uy, (float)q[u].y));
+            const unsigned bits = __float_as_uint(d);
+            const unsigned ok = (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u);
+            const unsigned long long key = ((unsigned long long)ok << 32) | (unsigned long long)(s0 + u * ng);
+            b = key > b ? key : b;
+        }
+    }
+    atomicMax(&best[k], b);
+}
+
+// The polygon: the extremes in direction order (counterclockwise), equal
+// consecutive points dropped (also across the wrap); nv < 3 -> no polygon.
+__global__ void k_refine_poly(const double *__restrict__ xy, const long long *__restrict__ surv, long long stride,
+                              const unsigned long long *__restrict__ best, RefinePoly *poly)
+{
+    __shared__ double2 e[HG_DIRS];
+    for (int k = threadIdx.x; k < HG_DIRS; k += blockDim.x) { // the extreme points, loaded in parallel
+        const long long pos = (long long)(best[k] & 0xffffffffull) * stride;
+        const long long id = surv ? surv[pos] : pos;
+        e[k] = reinterpret_cast<const double2 *>(xy)[id];
+    }
+    __syncthreads();
+    if (threadIdx.x != 0)
+        return;
+    int nv = 0;
+    for (int k = 0; k < HG_DIRS; k++) {
+        const double2 q = e[k];
+        if (nv > 0 && q.x == poly->v[nv - 1].x && q.y == poly->v[nv - 1].y)
+            continue;
+        poly->v[nv++] = q;
+    }
+    while (nv > 1 && poly->v[nv - 1].x == poly->v[0].x && poly->v[nv - 1].y == poly->v[0].y)
+        nv--;
+    poly->nv = nv >= 3 ? nv : 0;
+}
+
+// Strictly inside p's fan triangle of the polygon V[0..nv) (nv >= 3)?  The
+// triangle is picked by a binary search on the fp64 (inexact) side of
+// V0 -> V[mid]; the decision is the exact orientation on its three edges.
+__device__ __forceinline__ bool refine_inside(const double2 *V, int nv, double2 p)
+{
+    int lo = 1, hi = nv - 1;
+    const double2 a = V[0];
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        const double2 b = V[mid];
+        const double o = __dsub_rn(__dmul_rn(__dsub_rn(b.x, a.x), __dsub_rn(p.y, a.y)),
+                                   __dmul_rn(__dsub_rn(b.y, a.y), __dsub_rn(p.x, a.x)));
+        if (o >= 0.0)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    const double2 b = V[lo], c = V[lo + 1];
+    return chf::orient_sign(a.x, a.y, b.x, b.y, p.x, p.y) > 0 && chf::orient_sign(b.x, b.y, c.x, c.y, p.x, p.y) > 0 &&
+           chf::orient_sign(c.x, c.y, a.x, a.y, p.x, p.y) > 0;
+}
+
+// The round's expected yield: how many of the sample points it would drop.
+__global__ void __launch_bounds__(256) k_refine_probe(const double *__restrict__ xy,
+                                                      const long long *__restrict__ surv, long long stride,
+                                                      long long nsample, const RefinePoly *__restrict__ poly,
+                                                      unsigned long long *__restrict__ ndrop)
+{
+    __shared__ double2 V[HG_DIRS];
+    if (threadIdx.x < HG_DIRS)
+        V[threadIdx.x] = poly->v[threadIdx.x];
+    __syncthreads();
+    const int nv = poly->nv;
+    unsigned c = 0;
+    if (nv >= 3)
+        for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < nsample;
+             s += (long long)gridDim.x * blockDim.x) {
+            const long long pos = s * stride;
+            const long long id = surv ? surv[pos] : pos;
+            c += refine_inside(V, nv, reinterpret_cast<const double2 *>(xy)[id]) ? 1u : 0u;
+        }
+    for (int o = 16; o > 0; o >>= 1)
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c)
+        atomicAdd(ndrop, (unsigned long long)c);
+}
+
+// Keeps every survivor not strictly inside its fan triangle: kept[] gets
+// their ids, tile by tile (HG_RF_ITEMS x 256 survivors, one atomic per tile
+// for the tile's place; the order across tiles is arbitrary -- the hull
+// pipeline does not depend on it), *nkept the count.
+constexpr int HG_RF_ITEMS = 16;
+__global__ void __launch_bounds__(256) k_refine_filter(const double *__restrict__ xy, const long long *__restrict__ surv,
+                                                       long long m, const RefinePoly *__restrict__ poly,
+                                                       long long *__restrict__ kept,
+                                                       unsigned long long *__restrict__ nkept)
+{
+    __shared__ double2 V[HG_DIRS];
+    __shared__ int s_wcnt[HG_RF_ITEMS][8];
+    __shared__ unsigned long long s_base;
+    if (threadIdx.x < HG_DIRS)
+        V[threadIdx.x] = poly->v[threadIdx.x];
+    __syncthreads();
+    const int nv = poly->nv;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt = chrs::lanemask_lt();
+    constexpr long long TILE = 256LL * HG_RF_ITEMS;
+    for (long long t0 = (long long)blockIdx.x * TILE; t0 < m; t0 += (long long)gridDim.x * TILE) {
+        unsigned bal[HG_RF_ITEMS];
+        long long ids[HG_RF_ITEMS];
+#pragma unroll
+        for (int i = 0; i < HG_RF_ITEMS; i++) {
+            const long long j = t0 + 256LL * i + threadIdx.x;
+            bool keep = false;
+            ids[i] = 0;
+            if (j < m) {
+                ids[i] = surv ? surv[j] : j;
+                keep = nv < 3 || !refine_inside(V, nv, reinterpret_cast<const double2 *>(xy)[ids[i]]);
+            }
+            bal[i] = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0)
+                s_wcnt[i][w] = __popc(bal[i]);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) { // the tile's exclusive prefix over (item, warp), in place, and its place
+            int run = 0;
+            for (int i = 0; i < HG_RF_ITEMS; i++)
+                for (int ww = 0; ww < 8; ww++) {
+                    const int c = s_wcnt[i][ww];
+                    s_wcnt[i][ww] = run;
+                    run += c;
+                }
+            s_base = run ? atomicAdd(nkept, (unsigned long long)run) : 0ull;
+        }
+        __syncthreads();
+        const unsigned long long base = s_base;
+#pragma unroll
+        for (int i = 0; i < HG_RF_ITEMS; i++)
+            if ((bal[i] >> lane) & 1u)
+                kept[base + s_wcnt[i][w] + __popc(bal[i] & lt)] = ids[i];
+        __syncthreads(); // s_wcnt / s_base are rewritten by the next tile
+    }
+}
+
 struct Seq {
     const double2 *P;
     long long m;
     int rev; // 0: lower chain (increasing order), 1: upper chain (reversed)
+    int lgc; // log2 of the chunk size
     __device__ __forceinline__ long long fwd(long long r) const { return rev ? m - 1 - r : r; }
     __device__ __forceinline__ double2 at(long long r) const { return P[fwd(r)]; }
-    // equal to its sorted predecessor (so only the lowest id of a run is used)
-    __device__ __forceinline__ bool dup(long long r) const
-    {
-        const long long f = fwd(r);
-        return f > 0 && P[f].x == P[f - 1].x && P[f].y == P[f - 1].y;
-    }
 };
 
 __device__ __forceinline__ int turn(const double2 &a, const double2 &b, const double2 &c)
@@ -471,7 +670,7 @@ __global__ void k_chunk_chain(Seq s, long long nchunks, I *__restrict__ pos, lon
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nchunks)
         return;
-    const long long start = t * HG_CHUNK, end = min(start + HG_CHUNK, s.m);
+    const long long start = t << s.lgc, end = min(start + (1ll << s.lgc), s.m);
     long long top = 0;
     double2 p1 = make_double2(0, 0), p2 = make_double2(0, 0); // stack[top-1], stack[top-2]
     // One new point per step, loaded a step ahead: the next point in
@@ -506,13 +705,14 @@ __global__ void k_chunk_chain(Seq s, long long nchunks, I *__restrict__ pos, lon
 }
 
 // Chain access for the merges.  Mat: the chains as stored (the chain of the
-// group starting at chunk L is pos[L HG_CHUNK ...]).  Merged: the chains of
+// group starting at chunk L is pos[L << lgc ...]).  Merged: the chains of
 // the groups one merge level up, not materialised: group L (2w chunks) is
 // A[0..i] ++ B[j..] of its two halves (i, j of its pair p = L / 2w).
 template <typename I> struct Mat {
     using Idx = I;
     const I *pos;
-    __device__ __forceinline__ I at(long long L, long long q) const { return pos[L * HG_CHUNK + q]; }
+    int lgc;
+    __device__ __forceinline__ I at(long long L, long long q) const { return pos[(L << lgc) + q]; }
 };
 template <typename Inner> struct Merged {
     using Idx = typename Inner::Idx;
@@ -560,7 +760,7 @@ __global__ void k_bridge(Seq s, long long nchunks, long long W, const Acc acc, c
 }
 
 // Parallel copy of every merged chain (groups of 2W chunks): A[0..i] then
-// B[j..], A and B read through `acc`.  The group span 2 W HG_CHUNK is a power
+// B[j..], A and B read through `acc`.  The group span 2 W 2^lgc is a power
 // of two: group and offset by shift and mask.
 template <typename I, typename Acc>
 __global__ void k_merge_copy(long long m_cap, long long nchunks, long long W, int span_log2, const Acc acc,
@@ -624,22 +824,22 @@ static I *chain_gpu(const double2 *P, long long m, int rev, I *pos_a, I *pos_b, 
                     long long *bi, long long *bj, long long *bi2, long long *bj2, long long *bi3, long long *bj3,
                     long long *len_m, long long *len_m2, const long long **d_len, cudaStream_t st)
 {
-    const long long nchunks = (m + HG_CHUNK - 1) / HG_CHUNK;
-    const long long m_cap = nchunks * HG_CHUNK;
-    Seq s{P, m, rev};
+    const int lgc = chunk_log2(m); // log2 of the chunk size
+    const long long nchunks = (m + (1ll << lgc) - 1) >> lgc;
+    const long long m_cap = nchunks << lgc;
+    Seq s{P, m, rev, lgc};
     k_chunk_chain<I><<<(unsigned)((nchunks + HG_THREADS - 1) / HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, pos_a,
                                                                                                   len_a);
-    static_assert((HG_CHUNK & (HG_CHUNK - 1)) == 0, "chunk size is a power of two");
-    int lgw = 0, lgc = 0; // log2 w, log2 HG_CHUNK
-    while ((1ll << lgc) < HG_CHUNK)
-        lgc++;
-    // Up to three merge levels per copy: each level's bridges read the chains
+    int lgw = 0; // log2 w
+    // Up to three merge levels per copy (m >= HG_FLAT_M): each level's bridges read the chains
     // of the level below through Merged (not materialised), then one copy
     // materialises them -- a third of the copies of one level at a time.
     for (long long w = 1; w < nchunks;) {
         const long long np1 = (nchunks + 2 * w - 1) / (2 * w);
-        const Mat<I> m0{pos_a};
-        if (2 * w >= nchunks) {
+        const Mat<I> m0{pos_a, lgc};
+        // few points: one merge level per copy (the copies are cheap, and the
+        // bridge walks -- serial, latency-bound -- then read flat chains)
+        if (2 * w >= nchunks || m < HG_FLAT_M) {
             k_bridge<I><<<blocks_for(np1, HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, w, m0, len_a, bi, bj, len_b);
             k_merge_copy<I><<<grid_for(m_cap, 256), 256, 0, st>>>(m_cap, nchunks, w, lgw + 1 + lgc, m0, len_b, bi,
                                                                   bj, pos_b);
@@ -689,7 +889,8 @@ struct HullTmp {
     {
         if (m < 1)
             m = 1;
-        const size_t nchunks = (size_t)((m + HG_CHUNK - 1) / HG_CHUNK), cap = nchunks * HG_CHUNK;
+        const int lgc = chunk_log2(m);
+        const size_t nchunks = (size_t)((m + (1ll << lgc) - 1) >> lgc), cap = nchunks << lgc;
         const size_t isz = m < (1ll << 32) ? 4 : 8; // chain position width
         ntiles = (m + chrs::RS_TILE - 1) / chrs::RS_TILE;
         size_t p = 0;
@@ -798,9 +999,16 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
 extern "C" {
 
 // Device scratch for ch_hull_gpu / ch_hull_gpu_async on m survivors.
+// (the second round's scratch follows the pipeline's: the kept ids, then
+// the polygon, the direction extremes, the kept count and the probe's count)
+static size_t refine_offset(int64_t m) { return (HullTmp(m).total + 255) & ~(size_t)255; }
+static size_t refine_bytes(int64_t m)
+{
+    return ((size_t)(m < 1 ? 1 : m) * 8 + 255) / 256 * 256 + sizeof(RefinePoly) + HG_DIRS * 8 + 16 + 256;
+}
 size_t ch_hull_gpu_temp_bytes(int64_t m)
 {
-    return HullTmp(m).total;
+    return refine_offset(m) + refine_bytes(m);
 }
 
 // The device hull, asynchronous: hull ids to d_hull (device, capacity m), the
@@ -862,9 +1070,56 @@ ch_status ch_hull_gpu(const double *d_xy, int64_t n_points, const int64_t *d_sur
     const HullTmp L(m);
     if (tmp_bytes < L.total)
         return CH_ERR_WORKSPACE;
-    int64_t *d_out = (int64_t *)((char *)d_tmp + L.o_out);
-    int64_t *d_nh = d_out + m; // the word after the ids (o_out holds m + 1 words)
-    ch_status s = ch_hull_gpu_async(d_xy, n_points, d_surv, m, d_out, d_nh, d_tmp, tmp_bytes, stream);
+    // the second filtering round (see k_refine_filter) when the survivors
+    // are many and the scratch has room for it
+    const int64_t *surv = d_surv;
+    int64_t m2 = m;
+    if (m >= HG_REFINE_MIN && tmp_bytes >= refine_offset(m) + refine_bytes(m)) {
+        char *rb = (char *)d_tmp + refine_offset(m);
+        auto *kept = (long long *)rb;
+        auto *poly = (RefinePoly *)(rb + ((size_t)m * 8 + 255) / 256 * 256);
+        auto *best = (unsigned long long *)(poly + 1);
+        auto *nkept = best + HG_DIRS;
+        Dirs D;
+        for (int k = 0; k < HG_DIRS; k++) {
+            const double th = 2.0 * 3.14159265358979323846 * k / HG_DIRS;
+            D.u[k][0] = (float)std::cos(th);
+            D.u[k][1] = (float)std::sin(th);
+        }
+        const long long stride = m > HG_SAMPLE ? m / HG_SAMPLE : 1;
+        const long long nsample = (m + stride - 1) / stride;
+        if (cudaMemsetAsync(best, 0, (HG_DIRS + 2) * 8, st) != cudaSuccess)
+            return chi::fail(CH_ERR_CUDA, "device hull: memset");
+        k_dir_extremes<<<148 * 4, 256, 0, st>>>(d_xy, (const long long *)d_surv, stride, nsample, D, best);
+        k_refine_poly<<<1, HG_DIRS, 0, st>>>(d_xy, (const long long *)d_surv, stride, best, poly);
+        // the yield on the sample decides whether the full round pays (a
+        // circle: nothing to drop, every survivor is a hull vertex)
+        k_refine_probe<<<grid_for(nsample, 256), 256, 0, st>>>(d_xy, (const long long *)d_surv, stride, nsample, poly,
+                                                               nkept + 1);
+        unsigned long long ndrop = 0;
+        cudaMemcpyAsync(&ndrop, nkept + 1, 8, cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess)
+            return chi::fail(CH_ERR_CUDA, std::string("device hull (second round): ") +
+                                              cudaGetErrorString(cudaGetLastError()));
+        if (4 * ndrop >= (unsigned long long)nsample) { // >= 25% of the sample dropped
+            const long long tiles = (m + 256LL * HG_RF_ITEMS - 1) / (256LL * HG_RF_ITEMS);
+            k_refine_filter<<<(unsigned)std::min<long long>(tiles, 148 * 8), 256, 0, st>>>(
+                d_xy, (const long long *)d_surv, m, poly, kept, nkept);
+            unsigned long long nk = 0;
+            cudaMemcpyAsync(&nk, nkept, 8, cudaMemcpyDeviceToHost, st);
+            if (cudaStreamSynchronize(st) != cudaSuccess)
+                return chi::fail(CH_ERR_CUDA, std::string("device hull (second round): ") +
+                                                  cudaGetErrorString(cudaGetLastError()));
+            if ((int64_t)nk < m && nk > 0) {
+                surv = (const int64_t *)kept;
+                m2 = (int64_t)nk;
+            }
+        }
+    }
+    const HullTmp L2(m2);
+    int64_t *d_out = (int64_t *)((char *)d_tmp + L2.o_out);
+    int64_t *d_nh = d_out + m2; // the word after the ids (o_out holds m + 1 words)
+    ch_status s = ch_hull_gpu_async(d_xy, n_points, surv, m2, d_out, d_nh, d_tmp, L2.total, stream);
     if (s != CH_OK)
         return s;
     int64_t nh = 0;

@@ -1005,6 +1005,43 @@ def test_device_hull_equal_key_runs():
         assert np.array_equal(out[: h.value], oracle.hull(xy)), (name, "64-bit values")
 
 
+def test_device_hull_second_round():
+    """ch_hull_gpu's second filtering round (64-direction polygon of input
+    points, a survivor dropped only when strictly inside a fan triangle by the
+    exact orientation): hulls equal the oracle's on sets that put many points
+    on polygon edges, diagonals and vertices (duplicates with higher and lower
+    ids), dense collinear hull sides, and rings; ch_hull_gpu_async (no second
+    round) agrees."""
+    rng = np.random.default_rng(99)
+    sets = []
+    # a square: dense sides (collinear, not strict vertices), corners duplicated, interior points
+    t = rng.random(40_000)
+    side = np.concatenate([np.stack([t, np.zeros_like(t)], 1), np.stack([np.ones_like(t), t], 1),
+                           np.stack([t, np.ones_like(t)], 1), np.stack([np.zeros_like(t), t], 1)])
+    corners = np.array([[0.0, 0.0], [1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
+    sq = np.concatenate([rng.random((60_000, 2)), side, np.repeat(corners, 5, 0)])
+    sets.append(("square", sq[rng.permutation(len(sq))]))
+    # an integer octagon-ish grid: many points exactly on diagonals / edges of any polygon of grid points
+    g = rng.integers(-50, 51, size=(200_000, 2)).astype(np.float64)
+    g = g[np.abs(g[:, 0]) + np.abs(g[:, 1]) <= 70]
+    sets.append(("diamond_grid", g))
+    # a ring (C4-like) and a thin ring with duplicates of its outer points
+    th = rng.random(300_000) * 2 * np.pi
+    r = 0.25 * (1 + 0.1 * (2 * rng.random(300_000) - 1))
+    ring = np.stack([r * np.cos(th), r * np.sin(th)], 1)
+    sets.append(("ring", ring))
+    outer = ring[np.argsort(-r)[:500]]
+    sets.append(("ring_dups", np.concatenate([outer, ring, outer])))
+    for name, xy in sets:
+        d = torch.tensor(xy, device=DEV)
+        ids = torch.arange(len(xy), dtype=torch.int64, device=DEV)
+        got = chf.hull_gpu(d, ids)                   # ch_hull_gpu: with the second round
+        h, c = chf.hull_gpu_async(d, ids)            # ch_hull_gpu_async: without it
+        want = oracle.hull(xy)
+        assert np.array_equal(got, want), name
+        assert np.array_equal(h[: int(c.item())].cpu().numpy(), want), name
+
+
 def test_k1_f32_keys_rounding_ties():
     """K1's float32 fast path compares fl32(x +- y) with the fp64 bests rounded
     outward; inputs where fl32 and fl64 sums disagree must still give the
