@@ -385,10 +385,13 @@ ch_status ch_hull_points(const double *h_pts, const int64_t *h_ids, int64_t m,
 /* f1: Algorithm 1 line 4 on the device (future work P:432):
  * the exact strict hull of the m survivors d_surv (indices into d_xy, which
  * holds n_points points), same canonical form as ch_hull_points (DESIGN R8).
- * n_points < 2^32 lets the sort carry 32-bit ids.  One radix sort by x, each
- * run of equal x reduced in place to its lowest and highest point (the only
- * possible strict hull vertices among them), per-chunk exact monotone
- * chains, a tree of exact bridge merges.
+ * n_points < 2^32 lets the sort carry 32-bit ids.  For m >= 2^16 a second
+ * filtering round first drops survivors strictly inside a triangle of input
+ * points (exact orientation; 64-direction extremes of a sample), then one
+ * hand-written radix sort by x (32-bit monotone keys, equal-key runs sorted
+ * exactly), each run of equal x reduced in place to its lowest and highest
+ * point (the only possible strict hull vertices among them), per-chunk
+ * exact monotone chains, a tree of exact bridge merges.
  * Scratch: ch_hull_gpu_temp_bytes(m) bytes at d_tmp.  Hull ids go to h_hull
  * (host, capacity m); synchronizes `stream`. */
 size_t ch_hull_gpu_temp_bytes(int64_t m);
@@ -398,7 +401,8 @@ ch_status ch_hull_gpu(const double *d_xy, int64_t n_points, const int64_t *d_sur
  * between the device and host"): ids to d_hull (device, capacity m), the
  * count to *d_n_hull (device int64).  Fully asynchronous on `stream`; d_tmp
  * (ch_hull_gpu_temp_bytes(m)) must stay untouched until the stream reaches
- * this point.  m == 0 writes a zero count. */
+ * this point.  m == 0 writes a zero count.  (No second filtering round:
+ * its kept count would need a host synchronization.) */
 ch_status ch_hull_gpu_async(const double *d_xy, int64_t n_points, const int64_t *d_surv, int64_t m,
                             int64_t *d_hull, int64_t *d_n_hull, void *d_tmp, size_t tmp_bytes, void *stream);
 

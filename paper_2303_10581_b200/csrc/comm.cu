@@ -506,8 +506,8 @@ ch_status ch_hull_end_to_end_dist(ch_comm *c, const double *d_xy_shard, int64_t 
     int64_t nh = 0;
     if (is_root) {
         int64_t *d_nh = (int64_t *)hout + std::max<int64_t>(total, 1);
-        s = ch_hull_gpu_pts_async((const double *)pts, (const int64_t *)ids, total, (int64_t *)hout, d_nh, htmp, hb,
-                                  stream);
+        s = chi::hull_pts_refined((const double *)pts, (const int64_t *)ids, total, (int64_t *)hout, d_nh, htmp, hb,
+                                  st);
         if (s == CH_OK) {
             cudaMemcpyAsync(&nh, d_nh, 8, cudaMemcpyDeviceToHost, st);
             cudaStreamSynchronize(st);

@@ -996,9 +996,6 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
     return e == cudaSuccess ? CH_OK : chi::fail(CH_ERR_CUDA, std::string("device hull: ") + cudaGetErrorString(e));
 }
 
-extern "C" {
-
-// Device scratch for ch_hull_gpu / ch_hull_gpu_async on m survivors.
 // (the second round's scratch follows the pipeline's: the kept ids, then
 // the polygon, the direction extremes, the kept count and the probe's count)
 static size_t refine_offset(int64_t m) { return (HullTmp(m).total + 255) & ~(size_t)255; }
@@ -1006,6 +1003,62 @@ static size_t refine_bytes(int64_t m)
 {
     return ((size_t)(m < 1 ? 1 : m) * 8 + 255) / 256 * 256 + sizeof(RefinePoly) + HG_DIRS * 8 + 16 + 256;
 }
+// The second filtering round (k_refine_filter) on survivors surv[0..m) of
+// d_xy (surv NULL: every point), when they are many and the scratch
+// (ch_hull_gpu_temp_bytes(m)) has room: *surv_out / *m_out = the kept ids
+// (in the scratch, past HullTmp(m)) and their count, else surv / m.
+// Synchronizes `st`.
+static ch_status refine_round(const double *d_xy, const long long *surv, long long m, void *d_tmp, size_t tmp_bytes,
+                              cudaStream_t st, const long long **surv_out, int64_t *m_out)
+{
+    *surv_out = surv;
+    *m_out = m;
+    if (!(m >= HG_REFINE_MIN && tmp_bytes >= refine_offset(m) + refine_bytes(m)))
+        return CH_OK;
+    char *rb = (char *)d_tmp + refine_offset(m);
+    auto *kept = (long long *)rb;
+    auto *poly = (RefinePoly *)(rb + ((size_t)m * 8 + 255) / 256 * 256);
+    auto *best = (unsigned long long *)(poly + 1);
+    auto *nkept = best + HG_DIRS;
+    Dirs D;
+    for (int k = 0; k < HG_DIRS; k++) {
+        const double th = 2.0 * 3.14159265358979323846 * k / HG_DIRS;
+        D.u[k][0] = (float)std::cos(th);
+        D.u[k][1] = (float)std::sin(th);
+    }
+    const long long stride = m > HG_SAMPLE ? m / HG_SAMPLE : 1;
+    const long long nsample = (m + stride - 1) / stride;
+    if (cudaMemsetAsync(best, 0, (HG_DIRS + 2) * 8, st) != cudaSuccess)
+        return chi::fail(CH_ERR_CUDA, "device hull: memset");
+    k_dir_extremes<<<148 * 4, 256, 0, st>>>(d_xy, surv, stride, nsample, D, best);
+    k_refine_poly<<<1, HG_DIRS, 0, st>>>(d_xy, surv, stride, best, poly);
+    // the yield on the sample decides whether the full round pays (a
+    // circle: nothing to drop, every survivor is a hull vertex)
+    k_refine_probe<<<grid_for(nsample, 256), 256, 0, st>>>(d_xy, surv, stride, nsample, poly, nkept + 1);
+    unsigned long long ndrop = 0;
+    cudaMemcpyAsync(&ndrop, nkept + 1, 8, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+        return chi::fail(CH_ERR_CUDA, std::string("device hull (second round): ") +
+                                          cudaGetErrorString(cudaGetLastError()));
+    if (4 * ndrop < (unsigned long long)nsample) // < 25% of the sample dropped
+        return CH_OK;
+    const long long tiles = (m + 256LL * HG_RF_ITEMS - 1) / (256LL * HG_RF_ITEMS);
+    k_refine_filter<<<(unsigned)std::min<long long>(tiles, 148 * 8), 256, 0, st>>>(d_xy, surv, m, poly, kept, nkept);
+    unsigned long long nk = 0;
+    cudaMemcpyAsync(&nk, nkept, 8, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+        return chi::fail(CH_ERR_CUDA, std::string("device hull (second round): ") +
+                                          cudaGetErrorString(cudaGetLastError()));
+    if ((long long)nk < m && nk > 0) {
+        *surv_out = kept;
+        *m_out = (int64_t)nk;
+    }
+    return CH_OK;
+}
+
+extern "C" {
+
+// Device scratch for ch_hull_gpu / ch_hull_gpu_async on m survivors.
 size_t ch_hull_gpu_temp_bytes(int64_t m)
 {
     return refine_offset(m) + refine_bytes(m);
@@ -1032,6 +1085,31 @@ ch_status ch_hull_gpu_async(const double *d_xy, int64_t n_points, const int64_t 
                                                                     (long long *)d_hull, (long long *)d_n_hull, d_tmp,
                                                                     L, st);
 }
+
+} // extern "C"
+
+// The root's hull stage of ch_hull_end_to_end_dist: ch_hull_gpu_pts_async
+// preceded by the second filtering round (so it synchronizes `stream`).
+ch_status chi::hull_pts_refined(const double *d_pts, const int64_t *d_ids, int64_t m, int64_t *d_hull,
+                                int64_t *d_n_hull, void *d_tmp, size_t tmp_bytes, cudaStream_t st)
+{
+    if (m <= 0 || !d_pts || !d_ids || !d_tmp)
+        return ch_hull_gpu_pts_async(d_pts, d_ids, m, d_hull, d_n_hull, d_tmp, tmp_bytes, st);
+    const long long *kept = nullptr;
+    int64_t m2 = m;
+    ch_status s = refine_round(d_pts, nullptr, m, d_tmp, tmp_bytes, st, &kept, &m2);
+    if (s != CH_OK || kept == nullptr)
+        return s != CH_OK ? s : ch_hull_gpu_pts_async(d_pts, d_ids, m, d_hull, d_n_hull, d_tmp, tmp_bytes, st);
+    // positions kept[0..m2) into d_pts; the ids through the idmap d_ids
+    const HullTmp L2(m2);
+    return m2 <= (1ll << 32) ? hull_async<unsigned>(d_pts, kept, m2, (long long *)d_hull, (long long *)d_n_hull, d_tmp,
+                                                     L2, st, (const long long *)d_ids)
+                             : hull_async<unsigned long long>(d_pts, kept, m2, (long long *)d_hull,
+                                                              (long long *)d_n_hull, d_tmp, L2, st,
+                                                              (const long long *)d_ids);
+}
+
+extern "C" {
 
 // The hull of m points given by their coordinates d_pts (e.g. survivors
 // gathered from every rank, in increasing id order) and ids d_ids.  Same
@@ -1070,56 +1148,16 @@ ch_status ch_hull_gpu(const double *d_xy, int64_t n_points, const int64_t *d_sur
     const HullTmp L(m);
     if (tmp_bytes < L.total)
         return CH_ERR_WORKSPACE;
-    // the second filtering round (see k_refine_filter) when the survivors
-    // are many and the scratch has room for it
+    // the second filtering round (see k_refine_filter)
     const int64_t *surv = d_surv;
     int64_t m2 = m;
-    if (m >= HG_REFINE_MIN && tmp_bytes >= refine_offset(m) + refine_bytes(m)) {
-        char *rb = (char *)d_tmp + refine_offset(m);
-        auto *kept = (long long *)rb;
-        auto *poly = (RefinePoly *)(rb + ((size_t)m * 8 + 255) / 256 * 256);
-        auto *best = (unsigned long long *)(poly + 1);
-        auto *nkept = best + HG_DIRS;
-        Dirs D;
-        for (int k = 0; k < HG_DIRS; k++) {
-            const double th = 2.0 * 3.14159265358979323846 * k / HG_DIRS;
-            D.u[k][0] = (float)std::cos(th);
-            D.u[k][1] = (float)std::sin(th);
-        }
-        const long long stride = m > HG_SAMPLE ? m / HG_SAMPLE : 1;
-        const long long nsample = (m + stride - 1) / stride;
-        if (cudaMemsetAsync(best, 0, (HG_DIRS + 2) * 8, st) != cudaSuccess)
-            return chi::fail(CH_ERR_CUDA, "device hull: memset");
-        k_dir_extremes<<<148 * 4, 256, 0, st>>>(d_xy, (const long long *)d_surv, stride, nsample, D, best);
-        k_refine_poly<<<1, HG_DIRS, 0, st>>>(d_xy, (const long long *)d_surv, stride, best, poly);
-        // the yield on the sample decides whether the full round pays (a
-        // circle: nothing to drop, every survivor is a hull vertex)
-        k_refine_probe<<<grid_for(nsample, 256), 256, 0, st>>>(d_xy, (const long long *)d_surv, stride, nsample, poly,
-                                                               nkept + 1);
-        unsigned long long ndrop = 0;
-        cudaMemcpyAsync(&ndrop, nkept + 1, 8, cudaMemcpyDeviceToHost, st);
-        if (cudaStreamSynchronize(st) != cudaSuccess)
-            return chi::fail(CH_ERR_CUDA, std::string("device hull (second round): ") +
-                                              cudaGetErrorString(cudaGetLastError()));
-        if (4 * ndrop >= (unsigned long long)nsample) { // >= 25% of the sample dropped
-            const long long tiles = (m + 256LL * HG_RF_ITEMS - 1) / (256LL * HG_RF_ITEMS);
-            k_refine_filter<<<(unsigned)std::min<long long>(tiles, 148 * 8), 256, 0, st>>>(
-                d_xy, (const long long *)d_surv, m, poly, kept, nkept);
-            unsigned long long nk = 0;
-            cudaMemcpyAsync(&nk, nkept, 8, cudaMemcpyDeviceToHost, st);
-            if (cudaStreamSynchronize(st) != cudaSuccess)
-                return chi::fail(CH_ERR_CUDA, std::string("device hull (second round): ") +
-                                                  cudaGetErrorString(cudaGetLastError()));
-            if ((int64_t)nk < m && nk > 0) {
-                surv = (const int64_t *)kept;
-                m2 = (int64_t)nk;
-            }
-        }
-    }
+    ch_status s = refine_round(d_xy, (const long long *)d_surv, m, d_tmp, tmp_bytes, st, (const long long **)&surv, &m2);
+    if (s != CH_OK)
+        return s;
     const HullTmp L2(m2);
     int64_t *d_out = (int64_t *)((char *)d_tmp + L2.o_out);
     int64_t *d_nh = d_out + m2; // the word after the ids (o_out holds m + 1 words)
-    ch_status s = ch_hull_gpu_async(d_xy, n_points, surv, m2, d_out, d_nh, d_tmp, L2.total, stream);
+    s = ch_hull_gpu_async(d_xy, n_points, surv, m2, d_out, d_nh, d_tmp, L2.total, stream);
     if (s != CH_OK)
         return s;
     int64_t nh = 0;

@@ -31,5 +31,10 @@ ch_status pack_status(const void *d_ws, bool empty, int64_t *d_words, cudaStream
 ch_status empty_record(void *d_ext, cudaStream_t st);
 // Device address of the workspace's (global) extremes record.
 const void *ws_extremes(const void *d_ws);
+// The device hull of m gathered points d_pts with ids d_ids (increasing),
+// after the second filtering round (hull_gpu.cu); synchronizes `st`.
+// Scratch ch_hull_gpu_temp_bytes(m).
+ch_status hull_pts_refined(const double *d_pts, const int64_t *d_ids, int64_t m, int64_t *d_hull, int64_t *d_n_hull,
+                           void *d_tmp, size_t tmp_bytes, cudaStream_t st);
 
 } // namespace chi

@@ -6,20 +6,20 @@
 // pass, no separate upsweep):
 //   * one kernel quantises the keys and builds the 256-bin histogram of every
 //     pass at once (hull_gpu.cu, k_keys_hist);
-//   * per pass, each CTA claims the next 4096-item tile with an atomic ticket
-//     (so every tile it waits on is already resident), ranks the tile's items
-//     by digit -- warp w owns items [512 w, 512 w + 512), 16 rounds of 32,
-//     the lanes of a round that share a digit find each other through a
-//     shared atomicOr of lane bits, so the rank is stable (tile order) --
-//     publishes the tile's
-//     per-digit counts, then a decoupled look-back (one thread per digit)
-//     over earlier tiles' published counts gives the tile's global offset per
-//     digit; the tile is reordered by digit in shared memory and written out,
-//     so lanes with the same digit write consecutive addresses.
+//   * per pass, each CTA claims the next RS_TILE-item tile with an atomic
+//     ticket (so every tile it waits on is already resident) and ranks the
+//     tile's items by digit: warp w owns items [RS_WARP_ITEMS w, ...) in
+//     RS_ITEMS rounds of 32, and the lanes of a round that share a digit find
+//     each other through a shared atomicOr of lane bits, so the rank is stable
+//     (tile order).  It publishes the tile's per-digit counts; a decoupled
+//     look-back (one thread per digit) over earlier tiles' counts gives the
+//     tile's global offset per digit; the tile is reordered by digit in
+//     shared memory and written out, so lanes with the same digit write
+//     consecutive addresses.
 //   * status words are {flag:2, pass tag:2, count:60}: one memset per sort
 //     clears them, the tag keeps a pass from reading the previous pass's
 //     words.
-// cta_sort_run: the same ranking inside ONE CTA over a segment of global
+// cta_sort_pass: the same ranking inside ONE CTA over a segment of global
 // memory, tiles in order (no look-back) -- the device hull's fallback for runs
 // of equal quantised keys longer than a thread sorts by itself.
 #pragma once
