@@ -65,6 +65,9 @@ def parse():
                          "else nccl")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",  # noqa: E501
                     help="replay the step as a CUDA graph (ch_graph_launch); auto: 1 GPU and n <= 2^20")
+    ap.add_argument("--hull-reps", type=int, default=3,
+                    help="a8: time the hull of the step's survivors this many times after the filter's timed "
+                         "region (0: off; 1 GPU, float64 storage)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU work for the oracle baseline")
     return ap.parse_args()
@@ -558,6 +561,40 @@ def run_ours(a):
                "api": "ch_filter_host (C ABI, pinned host input)" if not multi else "DistFilter + host copies"}
         del h_xy, h_out, d_stage
 
+    # ---- a8: the hull of the survivors, timed separately (north_star), after
+    # the filter's timed region; CUDA events around each call ----
+    hull = None
+    if not multi and a.hull_reps > 0 and a.storage == "f64":
+        lib = chf._lib.load()
+        tb = int(lib.ch_hull_gpu_temp_bytes(max(s_local, 1)))
+        if 2 * tb + 16 * s_local < 0.9 * torch.cuda.mem_get_info()[0]:   # ch_hull_gpu allocates its own
+            surv = out[:s_local].clone()
+            tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
+            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t_sync, t_async, nh = [], [], 0
+            for r in range(a.hull_reps + 1):            # the first call is an untimed warm-up
+                torch.cuda.synchronize()
+                h0.record(stream)
+                ids = chf.hull_gpu(xy, surv)            # ch_hull_gpu: synchronizes, ids to host
+                h1.record(stream)
+                torch.cuda.synchronize()
+                if r:
+                    t_sync.append(h0.elapsed_time(h1))
+                h0.record(stream)
+                hd, hc = chf.hull_gpu_async(xy, surv, tmp)
+                h1.record(stream)
+                torch.cuda.synchronize()
+                if r:
+                    t_async.append(h0.elapsed_time(h1))
+                nh = len(ids)
+                assert int(hc.item()) == nh
+            hull = {"ms": float(np.median(t_sync)), "ms_on_device": float(np.median(t_async)), "n_hull": nh,
+                    "survivors": s_local, "reps": a.hull_reps,
+                    "api": "ms: ch_hull_gpu (second filtering round, radix sort by x, exact monotone chains; "
+                           "hull ids copied to the host); ms_on_device: ch_hull_gpu_async (ids stay on the "
+                           "device, no second round); median over reps, CUDA events; not part of value"}
+            del tmp, surv, hd, hc
+
     # ---- CPU oracle baseline (rank 0, N = 1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -585,7 +622,7 @@ def run_ours(a):
                        "exchange": exchange if multi else None},
             "survivors": s_total, "survivor_ratio": s_total / n_total,
             "hbm_frac": roof["step_frac"],
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "hull": hull,
             "gpu_launches": launches_per_step * K, "clocks": clk.summary(),
             "exchange_ms": ex_ms if multi else 0.0,
             "transport": ({"exchange": exchange, "ranks": world,

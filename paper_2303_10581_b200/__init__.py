@@ -292,11 +292,13 @@ def hull_gpu(xy: torch.Tensor, surv: torch.Tensor, stream=None) -> np.ndarray:
     m = int(surv.shape[0])
     tb = int(lib.ch_hull_gpu_temp_bytes(m))
     tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=xy.device)
-    out = np.zeros(max(m, 1), dtype=np.int64)
+    # the ids land in pinned host memory (torch's caching host allocator):
+    # a pageable buffer would make the copy, not the hull, the cost
+    out = torch.empty(max(m, 1), dtype=torch.int64, pin_memory=True)
     h = ctypes.c_int64(0)
-    _lib.check(lib.ch_hull_gpu(_ptr(xy), xy.shape[0], _ptr(surv), m, out.ctypes.data_as(ctypes.c_void_p),
+    _lib.check(lib.ch_hull_gpu(_ptr(xy), xy.shape[0], _ptr(surv), m, ctypes.c_void_p(out.data_ptr()),
                                ctypes.byref(h), _ptr(tmp), tb, _stream(stream)), "ch_hull_gpu")
-    return out[: h.value].copy()
+    return out[: h.value].numpy()
 
 
 def hull_gpu_async(xy: torch.Tensor, surv: torch.Tensor, tmp: torch.Tensor | None = None, stream=None):
