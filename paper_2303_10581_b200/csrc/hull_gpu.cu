@@ -805,6 +805,231 @@ __global__ void k_assemble(long long m, const I *__restrict__ low, const long lo
         out[g] = g < a ? id(val[low[g]]) : id(val[m - 1 - (long long)up[g - a]]);
 }
 
+// ---------------------------------------------- merges without copies --
+// (HG_RANGES) Each chunk c keeps the surviving part of its own chain,
+// pos[(c << lgc) + lo[c] .. + hi[c]); a group's chain is the concatenation of
+// its chunks' parts, so a merge only moves the cut points: the bridge walk
+// steps (chunk, slot) cursors over non-empty chunks, then one thread per
+// chunk applies the cut (A keeps up to (cA, sA), B from (cB, sB)).  After the
+// last level one scan of the part lengths places every part in the output.
+#ifndef HG_RANGES
+#define HG_RANGES 1
+#endif
+struct Ranges {
+    int *lo, *hi;
+};
+
+template <typename I>
+__global__ void k_ranges_init(long long nchunks, const long long *__restrict__ len, Ranges R)
+{
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += (long long)gridDim.x * blockDim.x) {
+        R.lo[c] = 0;
+        R.hi[c] = (int)len[c];
+    }
+}
+
+// Bridge of groups A = chunks [L, L + W) and B = [L + W, L + 2W) (clipped to
+// nchunks): the same two-pointer walk as k_bridge (i moves back while the turn
+// A[i-1], A[i], B[j] is <= 0, j forward while A[i], B[j], B[j+1] is), on
+// cursors.  Writes the cut (cA, sA + 1, cB, sB); cA = -1: one side is empty,
+// nothing to cut.
+template <typename I>
+__global__ void k_bridge_r(Seq s, long long nchunks, long long W, const I *__restrict__ pos, const Ranges R,
+                           long long *__restrict__ cutA, long long *__restrict__ cutB, int *__restrict__ cutS)
+{
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long L = 2 * p * W, M = L + W;
+    if (L >= nchunks)
+        return;
+    const long long aend = min(M, nchunks), bend = min(M + W, nchunks);
+    const long long np = (nchunks + 2 * W - 1) / (2 * W);
+    long long cA = aend - 1;
+    while (cA >= L && R.hi[cA] == R.lo[cA])
+        cA--;
+    long long cB = M;
+    while (cB < bend && R.hi[cB] == R.lo[cB])
+        cB++;
+    if (cA < L || cB >= bend) {
+        cutA[p] = -1;
+        return;
+    }
+    const int lgc = s.lgc;
+    int sA = R.hi[cA] - 1, loA = R.lo[cA];
+    int sB = R.lo[cB], hiB = R.hi[cB];
+    auto pt = [&](long long c, int sl) { return s.at((long long)pos[(c << lgc) + sl]); };
+    double2 pA = pt(cA, sA), pB = pt(cB, sB);
+    while (true) {
+        bool changed = false;
+        while (true) { // i > 0 and turn(A[i-1], A[i], B[j]) <= 0: i--
+            long long pc = cA;
+            int ps = sA - 1, plo = loA;
+            if (sA == loA) {
+                pc = cA - 1;
+                while (pc >= L && R.hi[pc] == R.lo[pc])
+                    pc--;
+                if (pc < L)
+                    break;
+                ps = R.hi[pc] - 1;
+                plo = R.lo[pc];
+            }
+            const double2 q = pt(pc, ps);
+            if (turn(q, pA, pB) > 0)
+                break;
+            cA = pc;
+            sA = ps;
+            loA = plo;
+            pA = q;
+            changed = true;
+        }
+        while (true) { // j < lb - 1 and turn(A[i], B[j], B[j+1]) <= 0: j++
+            long long nc = cB;
+            int ns = sB + 1, nhi = hiB;
+            if (ns == hiB) {
+                nc = cB + 1;
+                while (nc < bend && R.hi[nc] == R.lo[nc])
+                    nc++;
+                if (nc >= bend)
+                    break;
+                ns = R.lo[nc];
+                nhi = R.hi[nc];
+            }
+            const double2 q = pt(nc, ns);
+            if (turn(pA, pB, q) > 0)
+                break;
+            cB = nc;
+            sB = ns;
+            hiB = nhi;
+            pB = q;
+            changed = true;
+        }
+        if (!changed)
+            break;
+    }
+    cutA[p] = cA;
+    cutB[p] = cB;
+    cutS[p] = sA + 1;  // A's new end slot in chunk cA
+    cutS[np + p] = sB; // B's new start slot in chunk cB
+}
+
+__global__ void k_cut(long long nchunks, long long W, int lg2w, const long long *__restrict__ cutA,
+                      const long long *__restrict__ cutB, const int *__restrict__ cutS, Ranges R)
+{
+    const long long np = (nchunks + 2 * W - 1) / (2 * W);
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += (long long)gridDim.x * blockDim.x) {
+        const long long p = c >> lg2w;
+        const long long ca = cutA[p];
+        if (ca < 0)
+            continue;
+        if (c < (p << lg2w) + W) { // in A
+            if (c > ca)
+                R.hi[c] = R.lo[c];
+            else if (c == ca)
+                R.hi[c] = cutS[p];
+        } else {                   // in B
+            const long long cb = cutB[p];
+            if (c < cb)
+                R.lo[c] = R.hi[c];
+            else if (c == cb)
+                R.lo[c] = cutS[np + p];
+        }
+    }
+}
+
+// Exclusive scan of the part lengths hi - lo of both chains (blockIdx.y):
+// HG_SCAN_B lengths per block, block sums, then the offsets; tot[y] = the
+// chain's length.
+constexpr int HG_SCAN_B = 1024;
+__global__ void __launch_bounds__(HG_SCAN_B) k_scan_sums(long long nchunks, const Ranges R0, const Ranges R1,
+                                                         long long *__restrict__ bsum)
+{
+    const Ranges R = blockIdx.y ? R1 : R0;
+    const long long c = (long long)blockIdx.x * HG_SCAN_B + threadIdx.x;
+    int v = c < nchunks ? R.hi[c] - R.lo[c] : 0;
+    __shared__ int ws[HG_SCAN_B / 32];
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0)
+        ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int i = 0; i < HG_SCAN_B / 32; i++)
+            t += ws[i];
+        bsum[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+__global__ void k_scan_bsums(int nb, long long *__restrict__ bsum, long long *__restrict__ tot)
+{
+    // one thread per chain: the block sums are few (nchunks / 1024)
+    if (threadIdx.x >= 2)
+        return;
+    long long *b = bsum + (long long)threadIdx.x * nb, run = 0;
+    for (int i = 0; i < nb; i++) {
+        const long long t = b[i];
+        b[i] = run;
+        run += t;
+    }
+    tot[threadIdx.x] = run;
+}
+__global__ void __launch_bounds__(HG_SCAN_B) k_scan_offsets(long long nchunks, const Ranges R0, const Ranges R1,
+                                                            const long long *__restrict__ bsum, long long *__restrict__ pre0,
+                                                            long long *__restrict__ pre1)
+{
+    const Ranges R = blockIdx.y ? R1 : R0;
+    long long *pre = blockIdx.y ? pre1 : pre0;
+    const long long c = (long long)blockIdx.x * HG_SCAN_B + threadIdx.x;
+    const int v = c < nchunks ? R.hi[c] - R.lo[c] : 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o)
+            inc += t;
+    }
+    __shared__ int ws[HG_SCAN_B / 32];
+    if (lane == 31)
+        ws[w] = inc;
+    __syncthreads();
+    int base = 0;
+    for (int i = 0; i < w; i++)
+        base += ws[i];
+    if (c < nchunks)
+        pre[c] = bsum[blockIdx.y * gridDim.x + blockIdx.x] + base + inc - v;
+}
+
+// lower[0 .. nl-1) then upper[0 .. nu-1) (as k_assemble), read from the
+// chunks' parts: slot sl of chunk c is element pre[c] + sl - lo[c] of its chain.
+template <typename I, typename V>
+__global__ void k_assemble_r(long long m, int lgc, long long nchunks, const I *__restrict__ pl, const Ranges Rl,
+                             const long long *__restrict__ prel, const I *__restrict__ pu, const Ranges Ru,
+                             const long long *__restrict__ preu, const long long *__restrict__ tot,
+                             const V *__restrict__ val, const long long *__restrict__ idmap, long long *__restrict__ out,
+                             long long *__restrict__ d_nh)
+{
+    auto id = [&](V v) { return idmap ? idmap[(long long)v] : (long long)v; };
+    const long long nl = tot[0], nu = tot[1];
+    const long long a = nl - 1, total = nl <= 1 ? 1 : a + (nu - 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        *d_nh = total;
+    const long long cap = nchunks << lgc, mask = (1ll << lgc) - 1;
+    for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < cap; g += (long long)gridDim.x * blockDim.x) {
+        const long long c = g >> lgc;
+        const int sl = (int)(g & mask);
+        const int lol = Rl.lo[c];
+        if (sl >= lol && sl < Rl.hi[c]) {
+            const long long e = prel[c] + sl - lol;
+            if (nl <= 1 ? e == 0 : e < a) // (nl <= 1: a single distinct point, the lowest id)
+                out[e] = id(val[(long long)pl[g]]);
+        }
+        const int lou = Ru.lo[c];
+        if (nl > 1 && sl >= lou && sl < Ru.hi[c]) {
+            const long long e = preu[c] + sl - lou;
+            if (e < nu - 1)
+                out[a + e] = id(val[m - 1 - (long long)pu[g]]);
+        }
+    }
+}
+
 // One thread per item (the bridges: not grid-stride).
 unsigned blocks_for(long long items, int threads) { return (unsigned)std::max<long long>(1, (items + threads - 1) / threads); }
 
@@ -874,6 +1099,26 @@ static I *chain_gpu(const double2 *P, long long m, int rev, I *pos_a, I *pos_b, 
     }
     *d_len = len_a;
     return pos_a;
+}
+
+// One chain with HG_RANGES: chunk chains into pos, parts initialised, the
+// merge levels as cuts.  The parts stay in (pos, R).  Asynchronous.
+template <typename I>
+static void chain_gpu_ranges(const double2 *P, long long m, int rev, I *pos, Ranges R, long long *len_tmp,
+                             long long *cutA, long long *cutB, int *cutS, cudaStream_t st)
+{
+    const int lgc = chunk_log2(m);
+    const long long nchunks = (m + (1ll << lgc) - 1) >> lgc;
+    Seq s{P, m, rev, lgc};
+    k_chunk_chain<I><<<(unsigned)((nchunks + HG_THREADS - 1) / HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, pos,
+                                                                                                  len_tmp);
+    k_ranges_init<I><<<grid_for(nchunks, 256), 256, 0, st>>>(nchunks, len_tmp, R);
+    int lgw = 0;
+    for (long long w = 1; w < nchunks; w *= 2, lgw++) {
+        const long long np = (nchunks + 2 * w - 1) / (2 * w);
+        k_bridge_r<I><<<blocks_for(np, HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, w, pos, R, cutA, cutB, cutS);
+        k_cut<<<grid_for(nchunks, 256), 256, 0, st>>>(nchunks, w, lgw + 1, cutA, cutB, cutS, R);
+    }
 }
 
 // Scratch layout of ch_hull_gpu_async for m survivors (all 256-B aligned).
@@ -983,10 +1228,27 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
 
     auto chains = [&](auto tag) {
         using I = decltype(tag);
+#if HG_RANGES
+        // lower parts in (pa, la/lb as lo/hi), upper in (pc, lc/ld); cuts in
+        // bi / bj / bi2; offsets in lm / lm2, block sums in bj3, totals in bj2
+        const int lgc = chunk_log2(m);
+        const long long nchunks = (m + (1ll << lgc) - 1) >> lgc;
+        const Ranges Rl{(int *)la, (int *)lb}, Ru{(int *)lc, (int *)ld};
+        chain_gpu_ranges<I>(P, m, 0, (I *)pa, Rl, bi3, bi, bj, (int *)bi2, st);
+        chain_gpu_ranges<I>(P, m, 1, (I *)pc, Ru, bi3, bi, bj, (int *)bi2, st);
+        const unsigned nb = (unsigned)((nchunks + HG_SCAN_B - 1) / HG_SCAN_B);
+        k_scan_sums<<<dim3(nb, 2), HG_SCAN_B, 0, st>>>(nchunks, Rl, Ru, bj3);
+        k_scan_bsums<<<1, 32, 0, st>>>((int)nb, bj3, bj2);
+        k_scan_offsets<<<dim3(nb, 2), HG_SCAN_B, 0, st>>>(nchunks, Rl, Ru, bj3, lm, lm2);
+        k_assemble_r<I, V><<<grid_for(nchunks << lgc, 256), 256, 0, st>>>(m, lgc, nchunks, (const I *)pa, Rl, lm,
+                                                                          (const I *)pc, Ru, lm2, bj2, val, idmap,
+                                                                          d_hull, d_n_hull);
+#else
         const long long *d_hl, *d_hu;
         const I *low = chain_gpu<I>(P, m, 0, (I *)pa, (I *)pb, la, lb, bi, bj, bi2, bj2, bi3, bj3, lm, lm2, &d_hl, st);
         const I *up = chain_gpu<I>(P, m, 1, (I *)pc, (I *)pd, lc, ld, bi, bj, bi2, bj2, bi3, bj3, lm, lm2, &d_hu, st);
         k_assemble<I, V><<<grid_for(m, 256), 256, 0, st>>>(m, low, d_hl, up, d_hu, val, idmap, d_hull, d_n_hull);
+#endif
     };
     if (m < (1ll << 32))
         chains((unsigned)0);
