@@ -1,0 +1,7 @@
+# k_points load variants: time and DRAM bytes (ncu) on the 1e8 circle
+mkdir -p gpurun_out
+for v in 0 1 2 3; do
+  CH_NVCC_EXTRA="-DHG_PTS_LD=$v" python -m paper_2303_10581_b200.build --force > /dev/null 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,lts__t_sectors_srcunit_tex_op_read.sum --clock-control none --profile-from-start off -k regex:k_points --csv python scripts/hull_prof.py 2>/dev/null | grep -o '"gpu__time_duration.sum".*\|"dram__bytes_read.sum".*\|"lts__t_sectors_srcunit_tex_op_read.sum".*' | sed "s/^/v$v /" | cut -c1-120
+done
+python -m paper_2303_10581_b200.build --force > /dev/null 2>&1
