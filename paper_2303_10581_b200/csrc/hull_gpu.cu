@@ -32,6 +32,7 @@
 
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 #include <cstdint>
@@ -815,16 +816,25 @@ __global__ void k_assemble(long long m, const I *__restrict__ low, const long lo
 #ifndef HG_RANGES
 #define HG_RANGES 1
 #endif
+// nx / pv: links between a group's non-empty chunks (a cut links A's last
+// kept chunk to B's first, skipping the emptied ones); head / tail: a group's
+// first and last non-empty chunk (-1: empty), indexed by the group's first
+// chunk -- so a bridge walk never scans emptied chunks.
 struct Ranges {
-    int *lo, *hi;
+    int *lo, *hi, *nx, *pv;
 };
 
 template <typename I>
-__global__ void k_ranges_init(long long nchunks, const long long *__restrict__ len, Ranges R)
+__global__ void k_ranges_init(long long nchunks, const long long *__restrict__ len, Ranges R, int *__restrict__ head,
+                              int *__restrict__ tail)
 {
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += (long long)gridDim.x * blockDim.x) {
+        const int l = (int)len[c];
         R.lo[c] = 0;
-        R.hi[c] = (int)len[c];
+        R.hi[c] = l;
+        R.nx[c] = (int)c + 1;
+        R.pv[c] = (int)c - 1;
+        head[c] = tail[c] = l > 0 ? (int)c : -1;
     }
 }
 
@@ -835,22 +845,23 @@ __global__ void k_ranges_init(long long nchunks, const long long *__restrict__ l
 // nothing to cut.
 template <typename I>
 __global__ void k_bridge_r(Seq s, long long nchunks, long long W, const I *__restrict__ pos, const Ranges R,
-                           long long *__restrict__ cutA, long long *__restrict__ cutB, int *__restrict__ cutS)
+                           int *__restrict__ head, int *__restrict__ tail, long long *__restrict__ cutA,
+                           long long *__restrict__ cutB, int *__restrict__ cutS)
 {
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long L = 2 * p * W, M = L + W;
     if (L >= nchunks)
         return;
-    const long long aend = min(M, nchunks), bend = min(M + W, nchunks);
+    const long long bend = min(M + W, nchunks);
     const long long np = (nchunks + 2 * W - 1) / (2 * W);
-    long long cA = aend - 1;
-    while (cA >= L && R.hi[cA] == R.lo[cA])
-        cA--;
-    long long cB = M;
-    while (cB < bend && R.hi[cB] == R.lo[cB])
-        cB++;
-    if (cA < L || cB >= bend) {
+    long long cA = tail[L];
+    long long cB = M < nchunks ? head[M] : -1;
+    if (cA < 0 || cB < 0) { // one side empty: the group is the other side, uncut
         cutA[p] = -1;
+        if (cA < 0 && cB >= 0) {
+            head[L] = head[M];
+            tail[L] = tail[M];
+        }
         return;
     }
     const int lgc = s.lgc;
@@ -864,9 +875,9 @@ __global__ void k_bridge_r(Seq s, long long nchunks, long long W, const I *__res
             long long pc = cA;
             int ps = sA - 1, plo = loA;
             if (sA == loA) {
-                pc = cA - 1;
-                while (pc >= L && R.hi[pc] == R.lo[pc])
-                    pc--;
+                pc = R.pv[cA];
+                while (pc >= L && R.hi[pc] == R.lo[pc]) // (chunks empty from the start)
+                    pc = R.pv[pc];
                 if (pc < L)
                     break;
                 ps = R.hi[pc] - 1;
@@ -885,9 +896,9 @@ __global__ void k_bridge_r(Seq s, long long nchunks, long long W, const I *__res
             long long nc = cB;
             int ns = sB + 1, nhi = hiB;
             if (ns == hiB) {
-                nc = cB + 1;
+                nc = R.nx[cB];
                 while (nc < bend && R.hi[nc] == R.lo[nc])
-                    nc++;
+                    nc = R.nx[nc];
                 if (nc >= bend)
                     break;
                 ns = R.lo[nc];
@@ -909,6 +920,9 @@ __global__ void k_bridge_r(Seq s, long long nchunks, long long W, const I *__res
     cutB[p] = cB;
     cutS[p] = sA + 1;  // A's new end slot in chunk cA
     cutS[np + p] = sB; // B's new start slot in chunk cB
+    R.nx[cA] = (int)cB;
+    R.pv[cB] = (int)cA;
+    tail[L] = tail[M]; // head[L] stays: A keeps its first element
 }
 
 __global__ void k_cut(long long nchunks, long long W, int lg2w, const long long *__restrict__ cutA,
@@ -1105,18 +1119,19 @@ static I *chain_gpu(const double2 *P, long long m, int rev, I *pos_a, I *pos_b, 
 // merge levels as cuts.  The parts stay in (pos, R).  Asynchronous.
 template <typename I>
 static void chain_gpu_ranges(const double2 *P, long long m, int rev, I *pos, Ranges R, long long *len_tmp,
-                             long long *cutA, long long *cutB, int *cutS, cudaStream_t st)
+                             int *head, int *tail, long long *cutA, long long *cutB, int *cutS, cudaStream_t st)
 {
     const int lgc = chunk_log2(m);
     const long long nchunks = (m + (1ll << lgc) - 1) >> lgc;
     Seq s{P, m, rev, lgc};
     k_chunk_chain<I><<<(unsigned)((nchunks + HG_THREADS - 1) / HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, pos,
                                                                                                   len_tmp);
-    k_ranges_init<I><<<grid_for(nchunks, 256), 256, 0, st>>>(nchunks, len_tmp, R);
+    k_ranges_init<I><<<grid_for(nchunks, 256), 256, 0, st>>>(nchunks, len_tmp, R, head, tail);
     int lgw = 0;
     for (long long w = 1; w < nchunks; w *= 2, lgw++) {
         const long long np = (nchunks + 2 * w - 1) / (2 * w);
-        k_bridge_r<I><<<blocks_for(np, HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, w, pos, R, cutA, cutB, cutS);
+        k_bridge_r<I><<<blocks_for(np, HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, w, pos, R, head, tail, cutA,
+                                                                        cutB, cutS);
         k_cut<<<grid_for(nchunks, 256), 256, 0, st>>>(nchunks, w, lgw + 1, cutA, cutB, cutS, R);
     }
 }
@@ -1226,16 +1241,27 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
                                                           (unsigned long long *)k1, (unsigned *)v1,
                                                           (unsigned *)v1 + m);
 
+    // merges as cuts (m >= cuts_min) or by copies (fewer points: flat levels
+    // are cheaper than cursor walks); CH_HULL_CUTS_MIN overrides the
+    // threshold (tests run both paths on small inputs)
+    long long cuts_min = HG_FLAT_M;
+    if (const char *e = getenv("CH_HULL_CUTS_MIN"))
+        cuts_min = atoll(e);
     auto chains = [&](auto tag) {
         using I = decltype(tag);
 #if HG_RANGES
-        // lower parts in (pa, la/lb as lo/hi), upper in (pc, lc/ld); cuts in
-        // bi / bj / bi2; offsets in lm / lm2, block sums in bj3, totals in bj2
+      if (m >= cuts_min) {
+        // lower parts in (pa, la/lb as lo/hi + links), upper in (pc, lc/ld);
+        // cuts in bi / bj / bi2, group heads / tails in bi3, chunk lengths
+        // then block sums in bj3, offsets in lm / lm2, totals in bj2
         const int lgc = chunk_log2(m);
         const long long nchunks = (m + (1ll << lgc) - 1) >> lgc;
-        const Ranges Rl{(int *)la, (int *)lb}, Ru{(int *)lc, (int *)ld};
-        chain_gpu_ranges<I>(P, m, 0, (I *)pa, Rl, bi3, bi, bj, (int *)bi2, st);
-        chain_gpu_ranges<I>(P, m, 1, (I *)pc, Ru, bi3, bi, bj, (int *)bi2, st);
+        // (la..ld hold 2 nchunks + 2 ints each: lo or hi, then a link array)
+        const Ranges Rl{(int *)la, (int *)lb, (int *)la + nchunks, (int *)lb + nchunks};
+        const Ranges Ru{(int *)lc, (int *)ld, (int *)lc + nchunks, (int *)ld + nchunks};
+        int *head = (int *)bi3, *tail = (int *)bi3 + nchunks;
+        chain_gpu_ranges<I>(P, m, 0, (I *)pa, Rl, bj3, head, tail, bi, bj, (int *)bi2, st);
+        chain_gpu_ranges<I>(P, m, 1, (I *)pc, Ru, bj3, head, tail, bi, bj, (int *)bi2, st);
         const unsigned nb = (unsigned)((nchunks + HG_SCAN_B - 1) / HG_SCAN_B);
         k_scan_sums<<<dim3(nb, 2), HG_SCAN_B, 0, st>>>(nchunks, Rl, Ru, bj3);
         k_scan_bsums<<<1, 32, 0, st>>>((int)nb, bj3, bj2);
@@ -1243,12 +1269,13 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
         k_assemble_r<I, V><<<grid_for(nchunks << lgc, 256), 256, 0, st>>>(m, lgc, nchunks, (const I *)pa, Rl, lm,
                                                                           (const I *)pc, Ru, lm2, bj2, val, idmap,
                                                                           d_hull, d_n_hull);
-#else
+        return;
+      }
+#endif
         const long long *d_hl, *d_hu;
         const I *low = chain_gpu<I>(P, m, 0, (I *)pa, (I *)pb, la, lb, bi, bj, bi2, bj2, bi3, bj3, lm, lm2, &d_hl, st);
         const I *up = chain_gpu<I>(P, m, 1, (I *)pc, (I *)pd, lc, ld, bi, bj, bi2, bj2, bi3, bj3, lm, lm2, &d_hu, st);
         k_assemble<I, V><<<grid_for(m, 256), 256, 0, st>>>(m, low, d_hl, up, d_hu, val, idmap, d_hull, d_n_hull);
-#endif
     };
     if (m < (1ll << 32))
         chains((unsigned)0);

@@ -1042,6 +1042,52 @@ def test_device_hull_second_round():
         assert np.array_equal(h[: int(c.item())].cpu().numpy(), want), name
 
 
+def test_device_hull_merges_as_cuts_small_inputs(monkeypatch):
+    """The merges-as-cuts path (per-chunk parts, linked non-empty chunks;
+    taken by the library from 2^22 sorted points) forced on small inputs
+    through CH_HULL_CUTS_MIN=0: the randomized sweep's hard shapes (grids with
+    duplicates and collinear runs, circles, rings, vertical ties, chunk
+    boundaries) and the golden sets give the oracle's hull."""
+    monkeypatch.setenv("CH_HULL_CUTS_MIN", "0")
+    for ex in load_golden():
+        d = torch.tensor(ex["points"], device=DEV)
+        s = torch.tensor(ex["survivors"], dtype=torch.int64, device=DEV)
+        assert list(chf.hull_gpu(d, s)) == ex["hull"], ex["name"]
+    rng = np.random.default_rng(1234)
+    for case in range(20):
+        n = int(rng.choice([1, 2, 3, 17, 511, 513, 4_097, 65_537, 300_000]))
+        kind = case % 4
+        if kind == 0:
+            xy = rng.integers(-20, 21, size=(n, 2)).astype(np.float64)
+        elif kind == 1:
+            t = rng.uniform(0, 2 * np.pi, n)
+            xy = np.stack([np.cos(t), np.sin(t)], 1)
+        elif kind == 2:
+            t = rng.uniform(0, 2 * np.pi, n)
+            r = rng.uniform(0.9, 1.0, n)
+            xy = np.stack([r * np.cos(t), r * np.sin(t)], 1)
+        else:
+            xy = rng.normal(0, 1, size=(n, 2))
+            xy[:, 0] = np.round(xy[:, 0], 1)
+        d = torch.tensor(xy, device=DEV)
+        ids = np.sort(rng.choice(n, size=max(1, n - n // 7), replace=False)) if case % 2 else np.arange(n)
+        idt = torch.tensor(ids, dtype=torch.int64, device=DEV)
+        want = oracle.hull(xy, ids)
+        assert np.array_equal(chf.hull_gpu(d, idt), want), (case, n, kind)
+        h, c = chf.hull_gpu_async(d, idt)
+        assert np.array_equal(h[: int(c.item())].cpu().numpy(), want), (case, n, kind, "async")
+
+
+def test_device_hull_cuts_path_large_circle():
+    """A circle above 2^22 points: the library's own choice is the cuts path;
+    every point is a hull vertex, so every merge keeps nearly everything."""
+    n = (1 << 22) + 12_345
+    xy = synth.points("circle", n, seed=8, device=DEV)
+    ids = torch.arange(n, dtype=torch.int64, device=DEV)
+    h, c = chf.hull_gpu_async(xy, ids)
+    assert np.array_equal(h[: int(c.item())].cpu().numpy(), oracle.hull(xy.cpu().numpy()))
+
+
 def test_k1_f32_keys_rounding_ties():
     """K1's float32 fast path compares fl32(x +- y) with the fp64 bests rounded
     outward; inputs where fl32 and fl64 sums disagree must still give the
