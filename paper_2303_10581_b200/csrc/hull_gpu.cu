@@ -665,6 +665,16 @@ __device__ __forceinline__ int turn(const double2 &a, const double2 &b, const do
 }
 
 // Andrew's monotone chain over one chunk; the stack lives in pos[start..].
+// Points are loaded HG_PF steps ahead of their turn
+// (a shift register): q[0] is the current point in traversal order, q[1] the
+// next -- in the upper chain's (reversed) order also the sorted predecessor
+// P[f - 1] the duplicate test needs, so the reversed walk loads one point
+// past its chunk; in the lower chain's order the predecessor is the previous
+// point, kept in a register.
+#ifndef HG_PF
+#define HG_PF 4
+#endif
+
 template <typename I>
 __global__ void k_chunk_chain(Seq s, long long nchunks, I *__restrict__ pos, long long *__restrict__ len)
 {
@@ -672,20 +682,25 @@ __global__ void k_chunk_chain(Seq s, long long nchunks, I *__restrict__ pos, lon
     if (t >= nchunks)
         return;
     const long long start = t << s.lgc, end = min(start + (1ll << s.lgc), s.m);
+    // the last traversal index loaded: the chunk's, or one past it (reversed walk)
+    const long long lend = s.rev ? min(end, s.m - 1) : end - 1;
+    auto ld = [&](long long rr) { return rr <= lend ? s.at(rr) : make_double2(0, 0); };
     long long top = 0;
     double2 p1 = make_double2(0, 0), p2 = make_double2(0, 0); // stack[top-1], stack[top-2]
-    // One new point per step, loaded a step ahead: the next point in
-    // traversal order, which in the upper chain's (reversed) order is also
-    // the sorted predecessor P[f - 1] the duplicate test needs; in the lower
-    // chain's order the predecessor is the previous point, kept in a register.
+    double2 q[HG_PF + 1];
+#pragma unroll
+    for (int k = 0; k <= HG_PF; k++)
+        q[k] = ld(start + k);
     const long long f0 = s.fwd(start);
-    double2 cur = s.P[f0];
     double2 pred = (!s.rev && f0 > 0) ? s.P[f0 - 1] : make_double2(0, 0);
     for (long long r = start; r < end; r++) {
+        const double2 cur = q[0];
+#pragma unroll
+        for (int k = 0; k < HG_PF; k++)
+            q[k] = q[k + 1];
+        q[HG_PF] = ld(r + HG_PF + 1);
         const long long f = s.fwd(r);
-        const bool have_nx = s.rev ? f > 0 : r + 1 < end;
-        const double2 nx = have_nx ? s.P[s.rev ? f - 1 : f + 1] : cur;
-        const double2 pd = s.rev ? nx : pred;
+        const double2 pd = s.rev ? q[0] : pred;
         const bool dup = f > 0 && cur.x == pd.x && cur.y == pd.y;
         if (!dup) {
             while (top >= 2 && turn(p2, p1, cur) <= 0) {
@@ -700,7 +715,6 @@ __global__ void k_chunk_chain(Seq s, long long nchunks, I *__restrict__ pos, lon
             p1 = cur;
         }
         pred = cur;
-        cur = nx;
     }
     len[t] = top;
 }
