@@ -97,7 +97,19 @@ __global__ void k_gather_x(const double *__restrict__ xy, const long long *__res
         lo = a < lo ? a : lo;
         hi = b > hi ? b : hi;
     }
+    // one atomic pair per block (per warp, ~m/16 atomics on two words serialise)
+    __shared__ unsigned long long s_lo[32], s_hi[32];
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if ((threadIdx.x & 31) == 0) {
+        s_lo[w] = lo;
+        s_hi[w] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < nw; i++) {
+            lo = s_lo[i] < lo ? s_lo[i] : lo;
+            hi = s_hi[i] > hi ? s_hi[i] : hi;
+        }
         atomicMin(&mm[0], lo);
         atomicMax(&mm[1], hi);
     }
@@ -1039,21 +1051,27 @@ __global__ void k_assemble_r(long long m, int lgc, long long nchunks, const I *_
     const long long a = nl - 1, total = nl <= 1 ? 1 : a + (nu - 1);
     if (blockIdx.x == 0 && threadIdx.x == 0)
         *d_nh = total;
-    const long long cap = nchunks << lgc, mask = (1ll << lgc) - 1;
-    for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < cap; g += (long long)gridDim.x * blockDim.x) {
-        const long long c = g >> lgc;
-        const int sl = (int)(g & mask);
-        const int lol = Rl.lo[c];
-        if (sl >= lol && sl < Rl.hi[c]) {
-            const long long e = prel[c] + sl - lol;
+    // one warp per chunk: its parts' bounds and offsets once, then 32 slots
+    // at a time (coalesced reads of the positions and writes of the ids)
+    const int lane = threadIdx.x & 31;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nchunks; c += nwarps) {
+        const long long base = c << lgc;
+        const int lol = Rl.lo[c], hil = Rl.hi[c];
+        const long long pl0 = prel[c] - lol;
+        for (int sl = lol + lane; sl < hil; sl += 32) {
+            const long long e = pl0 + sl;
             if (nl <= 1 ? e == 0 : e < a) // (nl <= 1: a single distinct point, the lowest id)
-                out[e] = id(val[(long long)pl[g]]);
+                out[e] = id(val[(long long)pl[base + sl]]);
         }
-        const int lou = Ru.lo[c];
-        if (nl > 1 && sl >= lou && sl < Ru.hi[c]) {
-            const long long e = preu[c] + sl - lou;
-            if (e < nu - 1)
-                out[a + e] = id(val[m - 1 - (long long)pu[g]]);
+        if (nl > 1) {
+            const int lou = Ru.lo[c], hiu = Ru.hi[c];
+            const long long pu0 = preu[c] - lou;
+            for (int sl = lou + lane; sl < hiu; sl += 32) {
+                const long long e = pu0 + sl;
+                if (e < nu - 1)
+                    out[a + e] = id(val[m - 1 - (long long)pu[base + sl]]);
+            }
         }
     }
 }
@@ -1280,7 +1298,7 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
         k_scan_sums<<<dim3(nb, 2), HG_SCAN_B, 0, st>>>(nchunks, Rl, Ru, bj3);
         k_scan_bsums<<<1, 32, 0, st>>>((int)nb, bj3, bj2);
         k_scan_offsets<<<dim3(nb, 2), HG_SCAN_B, 0, st>>>(nchunks, Rl, Ru, bj3, lm, lm2);
-        k_assemble_r<I, V><<<grid_for(nchunks << lgc, 256), 256, 0, st>>>(m, lgc, nchunks, (const I *)pa, Rl, lm,
+        k_assemble_r<I, V><<<grid_for(nchunks * 32, 256), 256, 0, st>>>(m, lgc, nchunks, (const I *)pa, Rl, lm,
                                                                           (const I *)pc, Ru, lm2, bj2, val, idmap,
                                                                           d_hull, d_n_hull);
         return;
