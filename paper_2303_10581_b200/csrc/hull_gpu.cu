@@ -253,14 +253,40 @@ template <typename V> __device__ void ties_global(double2 *P, V *val, long long 
 // (ties_local) by the thread at its head; a longer one is queued for
 // k_fix_big (runs[2 r] = start, runs[2 r + 1] = length).
 constexpr int HG_SMALL_RUN = 32;
+constexpr int HG_FIX_W = 4; // k_fix_runs: 32-key windows per warp iteration
 template <typename V>
 __global__ void k_fix_runs(const unsigned *__restrict__ key, double2 *__restrict__ P, V *__restrict__ val, long long m,
                            long long *__restrict__ runs, unsigned long long *__restrict__ nruns)
 {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
-        const unsigned k = key[i];
-        if ((i > 0 && key[i - 1] == k) || i + 1 >= m || key[i + 1] != k)
-            continue; // not the head of a run of >= 2
+    // warps walk 32-key windows, HG_FIX_W windows' loads in flight; the
+    // neighbours come by shuffles (the window's edge lanes load theirs)
+    const int lane = threadIdx.x & 31;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (long long wb = w0 * 32; wb < m; wb += nwarps * 32 * HG_FIX_W) {
+        unsigned kc[HG_FIX_W], kp[HG_FIX_W], kn[HG_FIX_W];
+#pragma unroll
+        for (int u = 0; u < HG_FIX_W; u++) {
+            const long long i = wb + (long long)u * nwarps * 32 + lane;
+            kc[u] = i < m ? key[i] : 0u;
+            kp[u] = (lane == 0 && i > 0 && i - 1 < m) ? key[i - 1] : 0u;
+            kn[u] = (lane == 31 && i + 1 < m) ? key[i + 1] : 0u;
+        }
+        unsigned heads = 0;
+#pragma unroll
+        for (int u = 0; u < HG_FIX_W; u++) {
+            const long long i = wb + (long long)u * nwarps * 32 + lane;
+            const unsigned up = __shfl_up_sync(0xffffffffu, kc[u], 1), dn = __shfl_down_sync(0xffffffffu, kc[u], 1);
+            const unsigned prv = lane == 0 ? kp[u] : up, nxt = lane == 31 ? kn[u] : dn;
+            // the head of a run of >= 2 equal keys
+            const bool h = i < m && !(i > 0 && prv == kc[u]) && i + 1 < m && nxt == kc[u];
+            heads |= (h ? 1u : 0u) << u;
+        }
+        for (int wu = 0; wu < HG_FIX_W; wu++) {
+        if (!((heads >> wu) & 1u))
+            continue;
+        const long long i = wb + (long long)wu * nwarps * 32 + lane;
+        const unsigned k = key[i]; // (reloaded: a dynamic index into kc would put it in local memory)
         long long e = i + 2;
         while (e < m && e - i <= HG_SMALL_RUN && key[e] == k)
             e++;
@@ -311,6 +337,7 @@ __global__ void k_fix_runs(const unsigned *__restrict__ key, double2 *__restrict
         for (int t = 0; t < L; t++) {
             P[i + t] = p[t];
             val[i + t] = v[t];
+        }
         }
     }
 }
