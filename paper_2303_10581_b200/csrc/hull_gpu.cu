@@ -248,12 +248,39 @@ template <typename V> __device__ void ties_global(double2 *P, V *val, long long 
     val[e - 1] = vhi;
 }
 
+// The end of a run in sorted data: the first e in [lo, hi) with !same(e)
+// (hi if none), given same(lo - 1) and a monotone same (true, then false):
+// galloping then binary search, O(log run length) probes instead of a
+// serial scan (a single run can hold every point).
+template <typename F> __device__ __forceinline__ long long run_end(long long lo, long long hi, F same)
+{
+    long long step = 1, ok = lo - 1; // same(ok) holds
+    while (true) {
+        const long long p = ok + step;
+        if (p >= hi || !same(p)) {
+            hi = p < hi ? p : hi;
+            break;
+        }
+        ok = p;
+        step *= 2;
+    }
+    while (hi - ok > 1) { // same(ok), !same(hi) (or hi the bound)
+        const long long mid = ok + (hi - ok) / 2;
+        if (same(mid))
+            ok = mid;
+        else
+            hi = mid;
+    }
+    return hi;
+}
+
 // Runs of equal 32-bit key in the key-sorted points.  A run of at most
 // HG_SMALL_RUN is sorted by x (insertion sort) and its equal-x runs resolved
 // (ties_local) by the thread at its head; a longer one is queued for
 // k_fix_big (runs[2 r] = start, runs[2 r + 1] = length).
 constexpr int HG_SMALL_RUN = 32;
 constexpr int HG_FIX_W = 4; // k_fix_runs: 32-key windows per warp iteration
+constexpr long long HG_TIE_SERIAL = 256; // k_fix_big: longer equal-x runs are reduced block-wide
 template <typename V>
 __global__ void k_fix_runs(const unsigned *__restrict__ key, double2 *__restrict__ P, V *__restrict__ val, long long m,
                            long long *__restrict__ runs, unsigned long long *__restrict__ nruns)
@@ -291,8 +318,7 @@ __global__ void k_fix_runs(const unsigned *__restrict__ key, double2 *__restrict
         while (e < m && e - i <= HG_SMALL_RUN && key[e] == k)
             e++;
         if (e - i > HG_SMALL_RUN) {
-            while (e < m && key[e] == k)
-                e++;
+            e = run_end(e, m, [&](long long q) { return key[q] == k; });
             const unsigned long long r = atomicAdd(nruns, 1ull);
             runs[2 * r] = i;
             runs[2 * r + 1] = e - i;
@@ -342,6 +368,71 @@ __global__ void k_fix_runs(const unsigned *__restrict__ key, double2 *__restrict
     }
 }
 
+// One run of equal x, [a, a + L), reduced block-wide to [low, ..., low,
+// high] (ties_local's rule); the candidates go through the tile's shared
+// arrays.  Every thread of the CTA; ends with a barrier.
+template <typename V>
+__device__ void ties_block(double2 *__restrict__ P, V *__restrict__ val, long long a, long long L,
+                           chrs::TileSmem<unsigned long long, unsigned> &s)
+{
+    double2 plo = P[a], phi = plo;
+    V vlo = val[a], vhi = vlo;
+    for (long long t = threadIdx.x; t < L; t += blockDim.x) {
+        const double2 q = P[a + t];
+        const V vq = val[a + t];
+        if (q.y < plo.y || (q.y == plo.y && vq < vlo)) {
+            plo = q;
+            vlo = vq;
+        }
+        if (q.y > phi.y || (q.y == phi.y && vq < vhi)) {
+            phi = q;
+            vhi = vq;
+        }
+    }
+    double2 (*s_p)[chrs::RS_THREADS] = reinterpret_cast<double2 (*)[chrs::RS_THREADS]>(s.key);
+    V (*s_v)[chrs::RS_THREADS] = reinterpret_cast<V (*)[chrs::RS_THREADS]>(s.val);
+    __syncthreads(); // (s.key / s.val may hold the caller's data until here)
+    s_p[0][threadIdx.x] = plo;
+    s_v[0][threadIdx.x] = vlo;
+    s_p[1][threadIdx.x] = phi;
+    s_v[1][threadIdx.x] = vhi;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int u = 1; u < chrs::RS_THREADS; u++) {
+            const double2 q = s_p[0][u];
+            const V vq = s_v[0][u];
+            if (q.y < plo.y || (q.y == plo.y && vq < vlo)) {
+                plo = q;
+                vlo = vq;
+            }
+            const double2 q2 = s_p[1][u];
+            const V vq2 = s_v[1][u];
+            if (q2.y > phi.y || (q2.y == phi.y && vq2 < vhi)) {
+                phi = q2;
+                vhi = vq2;
+            }
+        }
+        s_p[0][0] = plo;
+        s_v[0][0] = vlo;
+        s_p[1][0] = phi;
+        s_v[1][0] = vhi;
+    }
+    __syncthreads();
+    plo = s_p[0][0];
+    vlo = s_v[0][0];
+    phi = s_p[1][0];
+    vhi = s_v[1][0];
+    for (long long t = threadIdx.x; t < L - 1; t += blockDim.x) {
+        P[a + t] = plo;
+        val[a + t] = vlo;
+    }
+    if (threadIdx.x == 0) {
+        P[a + L - 1] = phi;
+        val[a + L - 1] = vhi;
+    }
+    __syncthreads();
+}
+
 // The long runs, one CTA per run (grid-stride over the queue): 64-bit
 // order-preserving keys of x, a single-CTA LSD sort over the digits where the
 // run's keys differ (chrs::cta_sort_pass), the points and values permuted by
@@ -388,64 +479,8 @@ __global__ void __launch_bounds__(chrs::RS_THREADS) k_fix_big(double2 *__restric
         lo = s.lo;
         hi = s.hi;
         __syncthreads();
-        if (lo == hi) {
-            // one equal-x run: lowest and highest point, block-wide
-            double2 plo = P[a], phi = plo;
-            V vlo = val[a], vhi = vlo;
-            for (long long t = threadIdx.x; t < L; t += blockDim.x) {
-                const double2 q = P[a + t];
-                const V vq = val[a + t];
-                if (q.y < plo.y || (q.y == plo.y && vq < vlo)) {
-                    plo = q;
-                    vlo = vq;
-                }
-                if (q.y > phi.y || (q.y == phi.y && vq < vhi)) {
-                    phi = q;
-                    vhi = vq;
-                }
-            }
-            // per-thread candidates through the tile's shared arrays, combined by thread 0
-            double2 (*s_p)[chrs::RS_THREADS] = reinterpret_cast<double2 (*)[chrs::RS_THREADS]>(s.key);
-            V (*s_v)[chrs::RS_THREADS] = reinterpret_cast<V (*)[chrs::RS_THREADS]>(s.val);
-            s_p[0][threadIdx.x] = plo;
-            s_v[0][threadIdx.x] = vlo;
-            s_p[1][threadIdx.x] = phi;
-            s_v[1][threadIdx.x] = vhi;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                for (int u = 1; u < chrs::RS_THREADS; u++) {
-                    const double2 q = s_p[0][u];
-                    const V vq = s_v[0][u];
-                    if (q.y < plo.y || (q.y == plo.y && vq < vlo)) {
-                        plo = q;
-                        vlo = vq;
-                    }
-                    const double2 q2 = s_p[1][u];
-                    const V vq2 = s_v[1][u];
-                    if (q2.y > phi.y || (q2.y == phi.y && vq2 < vhi)) {
-                        phi = q2;
-                        vhi = vq2;
-                    }
-                }
-                s_p[0][0] = plo;
-                s_v[0][0] = vlo;
-                s_p[1][0] = phi;
-                s_v[1][0] = vhi;
-            }
-            __syncthreads();
-            plo = s_p[0][0];
-            vlo = s_v[0][0];
-            phi = s_p[1][0];
-            vhi = s_v[1][0];
-            for (long long t = threadIdx.x; t < L - 1; t += blockDim.x) {
-                P[a + t] = plo;
-                val[a + t] = vlo;
-            }
-            if (threadIdx.x == 0) {
-                P[a + L - 1] = phi;
-                val[a + L - 1] = vhi;
-            }
-            __syncthreads();
+        if (lo == hi) { // one equal-x run: lowest and highest point, block-wide
+            ties_block(P, val, a, L, s);
             continue;
         }
         // LSD passes over the bytes below the highest differing bit
@@ -483,15 +518,33 @@ __global__ void __launch_bounds__(chrs::RS_THREADS) k_fix_big(double2 *__restric
         for (long long t = threadIdx.x; t < L; t += blockDim.x)
             val[a + t] = tv[t];
         __syncthreads();
-        // equal-x runs inside the sorted run, one thread per run head
+        // equal-x runs inside the sorted run: one thread per run head (its
+        // end by galloping search); runs longer than HG_TIE_SERIAL are
+        // listed and reduced block-wide
+        if (threadIdx.x == 0)
+            s.tile = 0; // (the count of listed long runs)
+        __syncthreads();
+        long long *longs = reinterpret_cast<long long *>(s.gofs); // up to RS_BINS / 2 (start, end) pairs
         for (long long t = threadIdx.x; t < L; t += blockDim.x) {
             const double x = P[a + t].x;
             if ((t > 0 && P[a + t - 1].x == x) || t + 1 >= L || P[a + t + 1].x != x)
                 continue;
-            long long e = t + 2;
-            while (e < L && P[a + e].x == x)
-                e++;
-            ties_global(P, val, a + t, a + e);
+            const long long e = run_end(t + 2, L, [&](long long q) { return P[a + q].x == x; });
+            if (e - t > HG_TIE_SERIAL) {
+                const unsigned long long slot = atomicAdd(&s.tile, 1ull);
+                if (slot < chrs::RS_BINS / 2) {
+                    longs[2 * slot] = a + t;
+                    longs[2 * slot + 1] = a + e;
+                    continue;
+                }
+            }
+            ties_global(P, val, a + t, a + e); // short, or the list is full
+        }
+        __syncthreads();
+        const long long nlong = (long long)min(s.tile, (unsigned long long)(chrs::RS_BINS / 2));
+        for (long long r2 = 0; r2 < nlong; r2++) {
+            const long long b0 = longs[2 * r2], b1 = longs[2 * r2 + 1];
+            ties_block(P, val, b0, b1 - b0, s);
         }
         __syncthreads();
     }

@@ -970,6 +970,13 @@ def _quantum_cluster_sets():
     yield "rounded12", np.stack([xs, rng.random(200_000)], 1)
     # 6. two distinct x values only, both long runs of equal x, keys 0 and 2^32 - 256
     yield "two_columns", np.stack([rng.integers(0, 2, 70_000) * 1.0, rng.random(70_000)], 1)
+    # 6b. one x value for almost every point (a single equal-key run of ~all points; its end by
+    #     galloping search, its ties block-wide), and a long equal-x run inside a longer key run
+    v = np.stack([np.full(400_000, 0.5), rng.random(400_000)], 1)
+    yield "one_x_value", np.concatenate([v, rng.random((1000, 2))])
+    w = np.stack([np.full(300_000, 0.5), rng.random(300_000) * 2 - 1], 1)
+    w2 = np.stack([0.5 + rng.random(5000) * 1e-13, rng.random(5000)], 1)
+    yield "long_tie_in_run", np.concatenate([rng.random((2000, 2)), w, w2])
     # 7. a circle where runs of the same key hold whole arcs: x range 1, points within 1e-9 of x = +-1
     th = rng.random(300_000) * 1e-4
     circ = np.stack([np.cos(th), np.sin(th)], 1)
