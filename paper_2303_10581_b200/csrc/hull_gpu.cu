@@ -454,10 +454,8 @@ __global__ void __launch_bounds__(chrs::RS_THREADS) k_fix_big(double2 *__restric
     for (long long r = blockIdx.x; r < nr; r += gridDim.x) {
         const long long a = runs[2 * r], L = runs[2 * r + 1];
         unsigned long long lo = ~0ull, hi = 0;
-        for (long long t = threadIdx.x; t < L; t += blockDim.x) {
+        for (long long t = threadIdx.x; t < L; t += blockDim.x) { // (read-only: an all-equal run needs no keys)
             const unsigned long long o = okey(P[a + t].x);
-            ka[a + t] = o;
-            ia[a + t] = (unsigned)t;
             lo = o < lo ? o : lo;
             hi = o > hi ? o : hi;
         }
@@ -483,6 +481,11 @@ __global__ void __launch_bounds__(chrs::RS_THREADS) k_fix_big(double2 *__restric
             ties_block(P, val, a, L, s);
             continue;
         }
+        for (long long t = threadIdx.x; t < L; t += blockDim.x) {
+            ka[a + t] = okey(P[a + t].x);
+            ia[a + t] = (unsigned)t;
+        }
+        __syncthreads();
         // LSD passes over the bytes below the highest differing bit
         const int top = 63 - __clzll((long long)(lo ^ hi));
         unsigned long long *kin = ka, *kout = kb;
