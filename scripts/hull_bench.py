@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--sizes", nargs="+", type=float, default=[1e8])
     ap.add_argument("--dists", nargs="+", default=["normal", "circle", "displaced"])
     ap.add_argument("--host-max", type=float, default=1e8, help="largest survivor count for the host path")
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_hull.txt"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "hull_bench.txt"))
     a = ap.parse_args()
     rows = []
     for nf in a.sizes:
