@@ -281,6 +281,67 @@ template <typename F> __device__ __forceinline__ long long run_end(long long lo,
 constexpr int HG_SMALL_RUN = 32;
 constexpr int HG_FIX_W = 4; // k_fix_runs: 32-key windows per warp iteration
 constexpr long long HG_TIE_SERIAL = 256; // k_fix_big: longer equal-x runs are reduced block-wide
+// The run of equal keys headed at i (i is a head of a run of >= 2): sorted
+// by x and its equal-x runs resolved here when short (ties_local), else
+// queued for k_fix_big as (start, length).
+template <typename V>
+__device__ __forceinline__ void fix_run(long long i, const unsigned *__restrict__ key, double2 *__restrict__ P,
+                                        V *__restrict__ val, long long m, long long *__restrict__ runs,
+                                        unsigned long long *__restrict__ nruns)
+{
+    const unsigned k = key[i];
+    long long e = i + 2;
+    while (e < m && e - i <= HG_SMALL_RUN && key[e] == k)
+        e++;
+    if (e - i > HG_SMALL_RUN) {
+        e = run_end(e, m, [&](long long q) { return key[q] == k; });
+        const unsigned long long r = atomicAdd(nruns, 1ull);
+        runs[2 * r] = i;
+        runs[2 * r + 1] = e - i;
+        return;
+    }
+    const int L = (int)(e - i);
+    if (L == 2) { // the common case, in registers
+        double2 p0 = P[i], p1 = P[i + 1];
+        V v0 = val[i], v1 = val[i + 1];
+        if (p1.x < p0.x || (p1.x == p0.x && (p1.y < p0.y || (p1.y == p0.y && v1 < v0)))) {
+            const double2 tp = p0;
+            p0 = p1;
+            p1 = tp;
+            const V tv = v0;
+            v0 = v1;
+            v1 = tv;
+        }
+        // equal x: [low, high] is the (x, y, value) order, except for
+        // equal points, where high takes the lowest value too
+        if (p1.x == p0.x && p1.y == p0.y)
+            v1 = v0;
+        P[i] = p0;
+        P[i + 1] = p1;
+        val[i] = v0;
+        val[i + 1] = v1;
+        return;
+    }
+    double2 p[HG_SMALL_RUN];
+    V v[HG_SMALL_RUN];
+    for (int t = 0; t < L; t++) { // insertion sort by x (equal x in any order)
+        const double2 q = P[i + t];
+        const V vq = val[i + t];
+        int u = t;
+        for (; u > 0 && p[u - 1].x > q.x; u--) {
+            p[u] = p[u - 1];
+            v[u] = v[u - 1];
+        }
+        p[u] = q;
+        v[u] = vq;
+    }
+    ties_local(p, v, L);
+    for (int t = 0; t < L; t++) {
+        P[i + t] = p[t];
+        val[i + t] = v[t];
+    }
+}
+
 template <typename V>
 __global__ void k_fix_runs(const unsigned *__restrict__ key, double2 *__restrict__ P, V *__restrict__ val, long long m,
                            long long *__restrict__ runs, unsigned long long *__restrict__ nruns)
@@ -309,62 +370,9 @@ __global__ void k_fix_runs(const unsigned *__restrict__ key, double2 *__restrict
             const bool h = i < m && !(i > 0 && prv == kc[u]) && i + 1 < m && nxt == kc[u];
             heads |= (h ? 1u : 0u) << u;
         }
-        for (int wu = 0; wu < HG_FIX_W; wu++) {
-        if (!((heads >> wu) & 1u))
-            continue;
-        const long long i = wb + (long long)wu * nwarps * 32 + lane;
-        const unsigned k = key[i]; // (reloaded: a dynamic index into kc would put it in local memory)
-        long long e = i + 2;
-        while (e < m && e - i <= HG_SMALL_RUN && key[e] == k)
-            e++;
-        if (e - i > HG_SMALL_RUN) {
-            e = run_end(e, m, [&](long long q) { return key[q] == k; });
-            const unsigned long long r = atomicAdd(nruns, 1ull);
-            runs[2 * r] = i;
-            runs[2 * r + 1] = e - i;
-            continue;
-        }
-        const int L = (int)(e - i);
-        if (L == 2) { // the common case, in registers
-            double2 p0 = P[i], p1 = P[i + 1];
-            V v0 = val[i], v1 = val[i + 1];
-            if (p1.x < p0.x || (p1.x == p0.x && (p1.y < p0.y || (p1.y == p0.y && v1 < v0)))) {
-                const double2 tp = p0;
-                p0 = p1;
-                p1 = tp;
-                const V tv = v0;
-                v0 = v1;
-                v1 = tv;
-            }
-            // equal x: [low, high] is the (x, y, value) order, except for
-            // equal points, where high takes the lowest value too
-            if (p1.x == p0.x && p1.y == p0.y)
-                v1 = v0;
-            P[i] = p0;
-            P[i + 1] = p1;
-            val[i] = v0;
-            val[i + 1] = v1;
-            continue;
-        }
-        double2 p[HG_SMALL_RUN];
-        V v[HG_SMALL_RUN];
-        for (int t = 0; t < L; t++) { // insertion sort by x (equal x in any order)
-            const double2 q = P[i + t];
-            const V vq = val[i + t];
-            int u = t;
-            for (; u > 0 && p[u - 1].x > q.x; u--) {
-                p[u] = p[u - 1];
-                v[u] = v[u - 1];
-            }
-            p[u] = q;
-            v[u] = vq;
-        }
-        ties_local(p, v, L);
-        for (int t = 0; t < L; t++) {
-            P[i + t] = p[t];
-            val[i + t] = v[t];
-        }
-        }
+        for (int wu = 0; wu < HG_FIX_W; wu++)
+            if ((heads >> wu) & 1u)
+                fix_run(wb + (long long)wu * nwarps * 32 + lane, key, P, val, m, runs, nruns);
     }
 }
 
