@@ -401,8 +401,8 @@ ch_status ch_hull_gpu(const double *d_xy, int64_t n_points, const int64_t *d_sur
  * between the device and host"): ids to d_hull (device, capacity m), the
  * count to *d_n_hull (device int64).  Fully asynchronous on `stream`; d_tmp
  * (ch_hull_gpu_temp_bytes(m)) must stay untouched until the stream reaches
- * this point.  m == 0 writes a zero count.  (No second filtering round:
- * its kept count would need a host synchronization.) */
+ * this point.  m == 0 writes a zero count.  The second filtering round runs
+ * here too, decided on the device (its count never reaches the host). */
 ch_status ch_hull_gpu_async(const double *d_xy, int64_t n_points, const int64_t *d_surv, int64_t m,
                             int64_t *d_hull, int64_t *d_n_hull, void *d_tmp, size_t tmp_bytes, void *stream);
 

@@ -56,6 +56,9 @@ inline int chunk_log2(long long m)
         lgc++;
     return lgc;
 }
+// With the count on the device (the asynchronous second round), chunks are
+// sized for m / 16 so a heavily reduced set still gives enough threads.
+inline int chunk_log2_dev(long long m) { return chunk_log2(m >> 4 > 0 ? m >> 4 : 1); }
 constexpr int HG_THREADS = 128;
 
 __device__ __forceinline__ unsigned long long okey(double d)
@@ -80,8 +83,15 @@ __device__ __forceinline__ unsigned long long shfl_xor64(unsigned long long v, i
 // caller sets them to ~0 and 0).
 template <typename V>
 __global__ void k_gather_x(const double *__restrict__ xy, const long long *__restrict__ surv, long long m,
-                           double *__restrict__ X, V *__restrict__ val, unsigned long long *__restrict__ mm)
+                           double *__restrict__ X, V *__restrict__ val, unsigned long long *__restrict__ mm,
+                           const long long *__restrict__ dm, const long long *__restrict__ kept,
+                           const unsigned long long *__restrict__ use_kept)
 {
+    // (dm: the count is on the device; use_kept: the ids come from `kept`)
+    if (dm)
+        m = *dm;
+    if (use_kept && *use_kept)
+        surv = kept;
     unsigned long long lo = ~0ull, hi = 0;
     for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x) {
         const long long id = surv ? surv[j] : j; // NULL: every point of xy, in order
@@ -145,8 +155,10 @@ __device__ __forceinline__ unsigned quant(double x, const Quant &q)
 constexpr int HG_KH_ITEMS = 8;
 __global__ void __launch_bounds__(256) k_keys_hist(const double *__restrict__ X, long long m,
                                                    const unsigned long long *__restrict__ mm, unsigned *__restrict__ key,
-                                                   unsigned long long *__restrict__ hist)
+                                                   unsigned long long *__restrict__ hist, const long long *__restrict__ dm)
 {
+    if (dm)
+        m = *dm;
     __shared__ unsigned h[4][chrs::RS_BINS];
     for (int b = threadIdx.x; b < 4 * chrs::RS_BINS; b += blockDim.x)
         (&h[0][0])[b] = 0;
@@ -182,8 +194,10 @@ __global__ void __launch_bounds__(256) k_keys_hist(const double *__restrict__ X,
 
 template <typename V>
 __global__ void k_points(const double *__restrict__ xy, const V *__restrict__ val, long long m,
-                         double2 *__restrict__ P)
+                         double2 *__restrict__ P, const long long *__restrict__ dm)
 {
+    if (dm)
+        m = *dm;
     const double2 *__restrict__ xy2 = reinterpret_cast<const double2 *>(xy);
     for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (long long)gridDim.x * blockDim.x)
         P[j] = xy2[(long long)val[j]];
@@ -344,8 +358,11 @@ __device__ __forceinline__ void fix_run(long long i, const unsigned *__restrict_
 
 template <typename V>
 __global__ void k_fix_runs(const unsigned *__restrict__ key, double2 *__restrict__ P, V *__restrict__ val, long long m,
-                           long long *__restrict__ runs, unsigned long long *__restrict__ nruns)
+                           long long *__restrict__ runs, unsigned long long *__restrict__ nruns,
+                           const long long *__restrict__ dm)
 {
+    if (dm)
+        m = *dm;
     // warps walk 32-key windows, HG_FIX_W windows' loads in flight; the
     // neighbours come by shuffles (the window's edge lanes load theirs)
     const int lane = threadIdx.x & 31;
@@ -704,8 +721,12 @@ constexpr int HG_RF_ITEMS = 16;
 __global__ void __launch_bounds__(256) k_refine_filter(const double *__restrict__ xy, const long long *__restrict__ surv,
                                                        long long m, const RefinePoly *__restrict__ poly,
                                                        long long *__restrict__ kept,
-                                                       unsigned long long *__restrict__ nkept)
+                                                       unsigned long long *__restrict__ nkept,
+                                                       const unsigned long long *__restrict__ ndrop, long long nsample)
 {
+    // (ndrop: the asynchronous round -- the probe's yield decides on the device)
+    if (ndrop && 4 * *ndrop < (unsigned long long)nsample)
+        return;
     __shared__ double2 V[HG_DIRS];
     __shared__ int s_wcnt[HG_RF_ITEMS][8];
     __shared__ unsigned long long s_base;
@@ -753,11 +774,25 @@ __global__ void __launch_bounds__(256) k_refine_filter(const double *__restrict_
     }
 }
 
+// The asynchronous round's outcome on the device: use the kept list when the
+// probe found the round worth it and it kept fewer than m (and some) points;
+// *dm = the count the pipeline then sorts.
+__global__ void k_refine_finish(long long m, long long nsample, const unsigned long long *__restrict__ ndrop,
+                                const unsigned long long *__restrict__ nkept, unsigned long long *__restrict__ use,
+                                long long *__restrict__ dm)
+{
+    const unsigned long long nk = *nkept;
+    const bool u = 4 * *ndrop >= (unsigned long long)nsample && nk > 0 && (long long)nk < m;
+    *use = u ? 1ull : 0ull;
+    *dm = u ? (long long)nk : m;
+}
+
 struct Seq {
     const double2 *P;
     long long m;
     int rev; // 0: lower chain (increasing order), 1: upper chain (reversed)
     int lgc; // log2 of the chunk size
+    const long long *dm; // nullable: m is on the device (the kernels read it first)
     __device__ __forceinline__ long long fwd(long long r) const { return rev ? m - 1 - r : r; }
     __device__ __forceinline__ double2 at(long long r) const { return P[fwd(r)]; }
 };
@@ -781,6 +816,8 @@ __device__ __forceinline__ int turn(const double2 &a, const double2 &b, const do
 template <typename I>
 __global__ void k_chunk_chain(Seq s, long long nchunks, I *__restrict__ pos, long long *__restrict__ len)
 {
+    if (s.dm)
+        s.m = *s.dm;
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nchunks)
         return;
@@ -965,6 +1002,8 @@ __global__ void k_bridge_r(Seq s, long long nchunks, long long W, const I *__res
                            int *__restrict__ head, int *__restrict__ tail, long long *__restrict__ cutA,
                            long long *__restrict__ cutB, int *__restrict__ cutS)
 {
+    if (s.dm)
+        s.m = *s.dm;
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long L = 2 * p * W, M = L + W;
     if (L >= nchunks)
@@ -1135,8 +1174,10 @@ __global__ void k_assemble_r(long long m, int lgc, long long nchunks, const I *_
                              const long long *__restrict__ prel, const I *__restrict__ pu, const Ranges Ru,
                              const long long *__restrict__ preu, const long long *__restrict__ tot,
                              const V *__restrict__ val, const long long *__restrict__ idmap, long long *__restrict__ out,
-                             long long *__restrict__ d_nh)
+                             long long *__restrict__ d_nh, const long long *__restrict__ dm)
 {
+    if (dm)
+        m = *dm;
     auto id = [&](V v) { return idmap ? idmap[(long long)v] : (long long)v; };
     const long long nl = tot[0], nu = tot[1];
     const long long a = nl - 1, total = nl <= 1 ? 1 : a + (nu - 1);
@@ -1242,11 +1283,11 @@ static I *chain_gpu(const double2 *P, long long m, int rev, I *pos_a, I *pos_b, 
 // merge levels as cuts.  The parts stay in (pos, R).  Asynchronous.
 template <typename I>
 static void chain_gpu_ranges(const double2 *P, long long m, int rev, I *pos, Ranges R, long long *len_tmp,
-                             int *head, int *tail, long long *cutA, long long *cutB, int *cutS, cudaStream_t st)
+                             int *head, int *tail, long long *cutA, long long *cutB, int *cutS, int lgc,
+                             const long long *dm, cudaStream_t st)
 {
-    const int lgc = chunk_log2(m);
     const long long nchunks = (m + (1ll << lgc) - 1) >> lgc;
-    Seq s{P, m, rev, lgc};
+    Seq s{P, m, rev, lgc, dm};
     k_chunk_chain<I><<<(unsigned)((nchunks + HG_THREADS - 1) / HG_THREADS), HG_THREADS, 0, st>>>(s, nchunks, pos,
                                                                                                   len_tmp);
     k_ranges_init<I><<<grid_for(nchunks, 256), 256, 0, st>>>(nchunks, len_tmp, R, head, tail);
@@ -1272,8 +1313,11 @@ struct HullTmp {
     {
         if (m < 1)
             m = 1;
-        const int lgc = chunk_log2(m);
-        const size_t nchunks = (size_t)((m + (1ll << lgc) - 1) >> lgc), cap = nchunks << lgc;
+        // chunk arrays for the smaller of the two chunk sizes (chunk_log2,
+        // chunk_log2_dev); positions for the larger capacity
+        const int lgc = chunk_log2_dev(m), lgc1 = chunk_log2(m);
+        const size_t nchunks = (size_t)((m + (1ll << lgc) - 1) >> lgc);
+        const size_t cap = std::max(nchunks << lgc, (size_t)((m + (1ll << lgc1) - 1) >> lgc1) << lgc1);
         const size_t isz = m < (1ll << 32) ? 4 : 8; // chain position width
         ntiles = (m + chrs::RS_TILE - 1) / chrs::RS_TILE;
         size_t p = 0;
@@ -1313,8 +1357,11 @@ template <typename V>
 // resulting point positions / ids to output ids.
 static ch_status hull_async(const double *d_xy, const long long *surv, long long m, long long *d_hull,
                             long long *d_n_hull, void *d_tmp, const HullTmp &L, cudaStream_t st,
-                            const long long *idmap = nullptr)
+                            const long long *idmap = nullptr, const long long *dm = nullptr,
+                            const long long *kept = nullptr, const unsigned long long *use_kept = nullptr)
 {
+    // dm (nullable): the count is *dm <= m, known on the device only (the
+    // launches are sized for m); use_kept: the ids come from `kept`
     char *b = (char *)d_tmp;
     auto *k0 = (unsigned long long *)(b + L.o_k0), *k1 = (unsigned long long *)(b + L.o_k1);
     auto *v0 = (V *)(b + L.o_v0), *v1 = (V *)(b + L.o_v1);
@@ -1340,8 +1387,8 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
     const int g = grid_for(m, 256);
     double *X = (double *)k0;
     auto *keyA = (unsigned *)k1, *keyB = (unsigned *)k0;
-    k_gather_x<V><<<g, 256, 0, st>>>(d_xy, surv, m, X, v0, mm);
-    k_keys_hist<<<std::min(g, 148 * 4), 256, 0, st>>>(X, m, mm, keyA, hist);
+    k_gather_x<V><<<g, 256, 0, st>>>(d_xy, surv, m, X, v0, mm, dm, kept, use_kept);
+    k_keys_hist<<<std::min(g, 148 * 4), 256, 0, st>>>(X, m, mm, keyA, hist, dm);
     // 3. four stable 8-bit passes (keys k1 -> k0 -> k1 -> k0 -> k1, values v0 -> v1 -> ... -> v0)
     const size_t smem = sizeof(chrs::TileSmem<unsigned, V>);
     auto pass_kernel = m <= 0xffffffffll ? chrs::k_rs_pass<unsigned, V, unsigned> : chrs::k_rs_pass<unsigned, V, long long>;
@@ -1350,14 +1397,15 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
     V *vin = v0, *vout = v1;
     for (int pass = 0; pass < 4; pass++) {
         pass_kernel<<<(unsigned)L.ntiles, chrs::RS_THREADS, smem, st>>>(kin, kout, vin, vout, m, 8 * pass, pass,
-                                                                     hist + pass * chrs::RS_BINS, status, tk + pass);
+                                                                     hist + pass * chrs::RS_BINS, status, tk + pass,
+                                                                     dm);
         std::swap(kin, kout);
         std::swap(vin, vout);
     }
     V *val = vin; // == v0
     // 4. the points in key order; runs of equal key sorted by x exactly, equal x resolved
-    k_points<V><<<g, 256, 0, st>>>(d_xy, val, m, P);
-    k_fix_runs<V><<<g, 256, 0, st>>>(kin, P, val, m, runs, nruns);
+    k_points<V><<<g, 256, 0, st>>>(d_xy, val, m, P, dm);
+    k_fix_runs<V><<<g, 256, 0, st>>>(kin, P, val, m, runs, nruns, dm);
     const size_t fsmem = sizeof(chrs::TileSmem<unsigned long long, unsigned>);
     set_smem(k_fix_big<V>, fsmem);
     k_fix_big<V><<<148 * 2, chrs::RS_THREADS, fsmem, st>>>(P, val, runs, nruns, (unsigned long long *)k0,
@@ -1373,25 +1421,25 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
     auto chains = [&](auto tag) {
         using I = decltype(tag);
 #if HG_RANGES
-      if (m >= cuts_min) {
+      if (m >= cuts_min || dm) { // (the device count: only the cuts handle empty chunks)
         // lower parts in (pa, la/lb as lo/hi + links), upper in (pc, lc/ld);
         // cuts in bi / bj / bi2, group heads / tails in bi3, chunk lengths
         // then block sums in bj3, offsets in lm / lm2, totals in bj2
-        const int lgc = chunk_log2(m);
+        const int lgc = dm ? chunk_log2_dev(m) : chunk_log2(m);
         const long long nchunks = (m + (1ll << lgc) - 1) >> lgc;
         // (la..ld hold 2 nchunks + 2 ints each: lo or hi, then a link array)
         const Ranges Rl{(int *)la, (int *)lb, (int *)la + nchunks, (int *)lb + nchunks};
         const Ranges Ru{(int *)lc, (int *)ld, (int *)lc + nchunks, (int *)ld + nchunks};
         int *head = (int *)bi3, *tail = (int *)bi3 + nchunks;
-        chain_gpu_ranges<I>(P, m, 0, (I *)pa, Rl, bj3, head, tail, bi, bj, (int *)bi2, st);
-        chain_gpu_ranges<I>(P, m, 1, (I *)pc, Ru, bj3, head, tail, bi, bj, (int *)bi2, st);
+        chain_gpu_ranges<I>(P, m, 0, (I *)pa, Rl, bj3, head, tail, bi, bj, (int *)bi2, lgc, dm, st);
+        chain_gpu_ranges<I>(P, m, 1, (I *)pc, Ru, bj3, head, tail, bi, bj, (int *)bi2, lgc, dm, st);
         const unsigned nb = (unsigned)((nchunks + HG_SCAN_B - 1) / HG_SCAN_B);
         k_scan_sums<<<dim3(nb, 2), HG_SCAN_B, 0, st>>>(nchunks, Rl, Ru, bj3);
         k_scan_bsums<<<1, 32, 0, st>>>((int)nb, bj3, bj2);
         k_scan_offsets<<<dim3(nb, 2), HG_SCAN_B, 0, st>>>(nchunks, Rl, Ru, bj3, lm, lm2);
         k_assemble_r<I, V><<<grid_for(nchunks * 32, 256), 256, 0, st>>>(m, lgc, nchunks, (const I *)pa, Rl, lm,
                                                                           (const I *)pc, Ru, lm2, bj2, val, idmap,
-                                                                          d_hull, d_n_hull);
+                                                                          d_hull, d_n_hull, dm);
         return;
       }
 #endif
@@ -1413,7 +1461,7 @@ static ch_status hull_async(const double *d_xy, const long long *surv, long long
 static size_t refine_offset(int64_t m) { return (HullTmp(m).total + 255) & ~(size_t)255; }
 static size_t refine_bytes(int64_t m)
 {
-    return ((size_t)(m < 1 ? 1 : m) * 8 + 255) / 256 * 256 + sizeof(RefinePoly) + HG_DIRS * 8 + 16 + 256;
+    return ((size_t)(m < 1 ? 1 : m) * 8 + 255) / 256 * 256 + sizeof(RefinePoly) + HG_DIRS * 8 + 32 + 256;
 }
 // The second filtering round (k_refine_filter) on survivors surv[0..m) of
 // d_xy (surv NULL: every point), when they are many and the scratch
@@ -1455,7 +1503,8 @@ static ch_status refine_round(const double *d_xy, const long long *surv, long lo
     if (4 * ndrop < (unsigned long long)nsample) // < 25% of the sample dropped
         return CH_OK;
     const long long tiles = (m + 256LL * HG_RF_ITEMS - 1) / (256LL * HG_RF_ITEMS);
-    k_refine_filter<<<(unsigned)std::min<long long>(tiles, 148 * 8), 256, 0, st>>>(d_xy, surv, m, poly, kept, nkept);
+    k_refine_filter<<<(unsigned)std::min<long long>(tiles, 148 * 8), 256, 0, st>>>(d_xy, surv, m, poly, kept, nkept,
+                                                                                   nullptr, 0);
     unsigned long long nk = 0;
     cudaMemcpyAsync(&nk, nkept, 8, cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess)
@@ -1466,6 +1515,44 @@ static ch_status refine_round(const double *d_xy, const long long *surv, long lo
         *m_out = (int64_t)nk;
     }
     return CH_OK;
+}
+
+// The second round without a host synchronization (ch_hull_gpu_async): the
+// probe's yield is read by k_refine_filter and k_refine_finish on the
+// device, which leave *dm (the count) and *use (the kept list or `surv`) for
+// the pipeline.  False when m or the scratch is too small.
+static bool refine_round_async(const double *d_xy, const long long *surv, long long m, void *d_tmp, size_t tmp_bytes,
+                               cudaStream_t st, const long long **kept_out, const long long **dm_out,
+                               const unsigned long long **use_out)
+{
+    if (!(m >= HG_REFINE_MIN && tmp_bytes >= refine_offset(m) + refine_bytes(m)))
+        return false;
+    char *rb = (char *)d_tmp + refine_offset(m);
+    auto *kept = (long long *)rb;
+    auto *poly = (RefinePoly *)(rb + ((size_t)m * 8 + 255) / 256 * 256);
+    auto *best = (unsigned long long *)(poly + 1);
+    auto *nkept = best + HG_DIRS; // nkept[0] kept, [1] the probe's drops, [2] use, [3] dm
+    Dirs D;
+    for (int k = 0; k < HG_DIRS; k++) {
+        const double th = 2.0 * 3.14159265358979323846 * k / HG_DIRS;
+        D.u[k][0] = (float)std::cos(th);
+        D.u[k][1] = (float)std::sin(th);
+    }
+    const long long stride = m > HG_SAMPLE ? m / HG_SAMPLE : 1;
+    const long long nsample = (m + stride - 1) / stride;
+    if (cudaMemsetAsync(best, 0, (HG_DIRS + 4) * 8, st) != cudaSuccess)
+        return false;
+    k_dir_extremes<<<148 * 4, 256, 0, st>>>(d_xy, surv, stride, nsample, D, best);
+    k_refine_poly<<<1, HG_DIRS, 0, st>>>(d_xy, surv, stride, best, poly);
+    k_refine_probe<<<grid_for(nsample, 256), 256, 0, st>>>(d_xy, surv, stride, nsample, poly, nkept + 1);
+    const long long tiles = (m + 256LL * HG_RF_ITEMS - 1) / (256LL * HG_RF_ITEMS);
+    k_refine_filter<<<(unsigned)std::min<long long>(tiles, 148 * 8), 256, 0, st>>>(d_xy, surv, m, poly, kept, nkept,
+                                                                                   nkept + 1, nsample);
+    k_refine_finish<<<1, 1, 0, st>>>(m, nsample, nkept + 1, nkept, nkept + 2, (long long *)(nkept + 3));
+    *kept_out = kept;
+    *use_out = nkept + 2;
+    *dm_out = (const long long *)(nkept + 3);
+    return true;
 }
 
 extern "C" {
@@ -1489,13 +1576,18 @@ ch_status ch_hull_gpu_async(const double *d_xy, int64_t n_points, const int64_t 
     const HullTmp L(m);
     if (tmp_bytes < L.total)
         return CH_ERR_WORKSPACE;
+    // the second filtering round, decided on the device (no host
+    // synchronization) when the scratch has room for it
+    const long long *kept = nullptr, *dm = nullptr;
+    const unsigned long long *use = nullptr;
+    refine_round_async(d_xy, (const long long *)d_surv, m, d_tmp, tmp_bytes, st, &kept, &dm, &use);
     // ids fit 32 bits when the point array does: the sorts then move 12, not
     // 16, bytes per element and pass
     return n_points <= (1ll << 32) ? hull_async<unsigned>(d_xy, (const long long *)d_surv, m, (long long *)d_hull,
-                                                           (long long *)d_n_hull, d_tmp, L, st)
+                                                           (long long *)d_n_hull, d_tmp, L, st, nullptr, dm, kept, use)
                                    : hull_async<unsigned long long>(d_xy, (const long long *)d_surv, m,
                                                                     (long long *)d_hull, (long long *)d_n_hull, d_tmp,
-                                                                    L, st);
+                                                                    L, st, nullptr, dm, kept, use);
 }
 
 } // extern "C"

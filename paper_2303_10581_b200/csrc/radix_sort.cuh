@@ -211,8 +211,12 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_rs_pass(const K *__rest
                                                               const V *__restrict__ vin, V *__restrict__ vout,
                                                               long long m, int shift, int tag,
                                                               const unsigned long long *__restrict__ hist,
-                                                              unsigned long long *status, unsigned long long *ticket)
+                                                              unsigned long long *status, unsigned long long *ticket,
+                                                              const long long *__restrict__ dm = nullptr)
 {
+    // dm (nullable): the key count is on the device (<= m; the grid is sized for m)
+    if (dm)
+        m = *dm < m ? *dm : m;
     extern __shared__ __align__(16) unsigned char rs_smem[];
     TileSmem<K, V> &s = *reinterpret_cast<TileSmem<K, V> *>(rs_smem);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, d = threadIdx.x;
