@@ -282,6 +282,12 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_rs_pass(const K *__rest
             p -= nw;
         }
         st_volatile(my, RS_FLAG_INC | tg | (pre + c));
+#ifdef CH_RS_STATS
+        const long long ntiles = (m + RS_TILE - 1) / RS_TILE;
+        if (d == 0 && atomicAdd(&g_rs_stats[2], 1ull) + 2 == (unsigned long long)ntiles)
+            printf("rs_stats pass tag %d: tiles %lld windows %llu (per digit-tile %.2f) unpublished re-reads %llu\n",
+                   tag, ntiles, g_rs_stats[0], (double)g_rs_stats[0] / RS_BINS / ntiles, g_rs_stats[1]);
+#endif
     }
     O *gofs = reinterpret_cast<O *>(s.gofs);
     gofs[d] = (O)(hb + pre) - (O)s.excl[d];
