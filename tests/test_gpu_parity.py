@@ -1095,6 +1095,25 @@ def test_device_hull_cuts_path_large_circle():
     assert np.array_equal(h[: int(c.item())].cpu().numpy(), oracle.hull(xy.cpu().numpy()))
 
 
+def test_device_hull_sort_tile_and_round_boundaries():
+    """Sizes around the radix sort's tile (6144 keys) and its multiples, and
+    around the second round's 2^16 threshold, on a circle (every point a hull
+    vertex, so any misplaced key changes the hull) and a ring (the round
+    drops most points): ch_hull_gpu and ch_hull_gpu_async equal the oracle."""
+    rng = np.random.default_rng(6144)
+    for n in (6143, 6144, 6145, 12_287, 12_289, 65_535, 65_536, 65_537, 6144 * 11 + 1):
+        th = rng.random(n) * 2 * np.pi
+        for kind in ("circle", "ring"):
+            r = 1.0 if kind == "circle" else 1.0 - 0.05 * rng.random(n)
+            xy = np.stack([r * np.cos(th), r * np.sin(th)], 1)
+            d = torch.tensor(xy, device=DEV)
+            ids = torch.arange(n, dtype=torch.int64, device=DEV)
+            want = oracle.hull(xy)
+            assert np.array_equal(chf.hull_gpu(d, ids), want), (n, kind)
+            h, c = chf.hull_gpu_async(d, ids)
+            assert np.array_equal(h[: int(c.item())].cpu().numpy(), want), (n, kind, "async")
+
+
 def test_k1_f32_keys_rounding_ties():
     """K1's float32 fast path compares fl32(x +- y) with the fp64 bests rounded
     outward; inputs where fl32 and fl64 sums disagree must still give the
