@@ -45,6 +45,9 @@ constexpr int RS_ITEMS = RS_ITEMS_N;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 constexpr int RS_WARP_ITEMS = 32 * RS_ITEMS;
 constexpr int RS_LOOKBACK = 4; // earlier tiles read per look-back round trip
+#ifndef RS_PACK
+#define RS_PACK 1 // 32-bit keys with 32-bit values: one 64-bit shared word per item in the reorder
+#endif
 #ifndef RS_MINB
 #define RS_MINB 2 // resident CTAs per SM the pass kernel's registers are bounded for
 #endif
@@ -196,8 +199,15 @@ __device__ __forceinline__ void local_scatter(TileSmem<K, V> &s, const K (&k)[RS
         if (32 * i + lane < nv) {
             const unsigned d = digit_of(k[i], shift);
             const unsigned pos = s.whist[w][d] + rank[i];
-            s.key[pos] = k[i];
-            s.val[pos] = vsrc[wb + 32 * i];
+            if constexpr (RS_PACK && sizeof(K) == 4 && sizeof(V) == 4) {
+                // key and value as one 64-bit word (the key and value arrays
+                // are contiguous: 2 RS_TILE words)
+                reinterpret_cast<unsigned long long *>(s.key)[pos] =
+                    ((unsigned long long)vsrc[wb + 32 * i] << 32) | (unsigned)k[i];
+            } else {
+                s.key[pos] = k[i];
+                s.val[pos] = vsrc[wb + 32 * i];
+            }
         }
 }
 
@@ -295,10 +305,19 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_rs_pass(const K *__rest
     __syncthreads();
     const int nvalid = (int)(m - base < RS_TILE ? m - base : RS_TILE);
     for (int j = threadIdx.x; j < nvalid; j += RS_THREADS) {
-        const K kk = s.key[j];
+        K kk;
+        V vv;
+        if constexpr (RS_PACK && sizeof(K) == 4 && sizeof(V) == 4) {
+            const unsigned long long kv = reinterpret_cast<const unsigned long long *>(s.key)[j];
+            kk = (K)(unsigned)kv;
+            vv = (V)(kv >> 32);
+        } else {
+            kk = s.key[j];
+            vv = s.val[j];
+        }
         const O g = gofs[digit_of(kk, shift)] + (O)j;
         kout[g] = kk;
-        vout[g] = s.val[j];
+        vout[g] = vv;
     }
 }
 
