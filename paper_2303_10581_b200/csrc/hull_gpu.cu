@@ -57,8 +57,12 @@ inline int chunk_log2(long long m)
     return lgc;
 }
 // With the count on the device (the asynchronous second round), chunks are
-// sized for m / 16 so a heavily reduced set still gives enough threads.
-inline int chunk_log2_dev(long long m) { return chunk_log2(m >> 4 > 0 ? m >> 4 : 1); }
+// sized for m >> HG_DEV_SHIFT so a heavily reduced set still gives enough
+// threads.
+#ifndef HG_DEV_SHIFT
+#define HG_DEV_SHIFT 2 // (A/B: 0 / 1 / 2 / 3 / 4 / 6 -> 1e8 displaced 2.33 / 1.92 / 1.80 / 1.86 / 2.06 / 2.31 ms)
+#endif
+inline int chunk_log2_dev(long long m) { return chunk_log2(m >> HG_DEV_SHIFT > 0 ? m >> HG_DEV_SHIFT : 1); }
 constexpr int HG_THREADS = 128;
 
 __device__ __forceinline__ unsigned long long okey(double d)
