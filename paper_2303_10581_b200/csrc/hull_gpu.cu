@@ -831,6 +831,8 @@ __global__ void k_chunk_chain(Seq s, long long nchunks, I *__restrict__ pos, lon
     auto ld = [&](long long rr) { return rr <= lend ? s.at(rr) : make_double2(0, 0); };
     long long top = 0;
     double2 p1 = make_double2(0, 0), p2 = make_double2(0, 0); // stack[top-1], stack[top-2]
+    double2 p3 = make_double2(0, 0);                          // stack[top-3] when have3
+    bool have3 = false;
     double2 q[HG_PF + 1];
 #pragma unroll
     for (int k = 0; k <= HG_PF; k++)
@@ -850,11 +852,17 @@ __global__ void k_chunk_chain(Seq s, long long nchunks, I *__restrict__ pos, lon
             while (top >= 2 && turn(p2, p1, cur) <= 0) {
                 top--;
                 p1 = p2;
-                if (top >= 2)
-                    p2 = s.at(pos[start + top - 2]);
+                if (top >= 2) {
+                    // stack[top-2]: the cached third entry when valid (a
+                    // single pop, the common case), else reloaded
+                    p2 = have3 ? p3 : s.at(pos[start + top - 2]);
+                    have3 = false;
+                }
             }
             pos[start + top] = (I)r;
             top++;
+            p3 = p2;
+            have3 = top >= 3;
             p2 = p1;
             p1 = cur;
         }
