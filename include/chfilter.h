@@ -385,7 +385,8 @@ ch_status ch_hull_points(const double *h_pts, const int64_t *h_ids, int64_t m,
 /* f1: Algorithm 1 line 4 on the device (future work P:432):
  * the exact strict hull of the m survivors d_surv (indices into d_xy, which
  * holds n_points points), same canonical form as ch_hull_points (DESIGN R8).
- * n_points < 2^32 lets the sort carry 32-bit ids.  For m >= 2^16 a second
+ * n_points < 2^32 lets the sort carry 32-bit ids.  m <= 1024: one CTA
+ * (sort and chains in shared memory).  For m >= 2^16 a second
  * filtering round first drops survivors strictly inside a triangle of input
  * points (exact orientation; 64-direction extremes of a sample), then one
  * hand-written radix sort by x (32-bit monotone keys, equal-key runs sorted

@@ -791,6 +791,107 @@ __global__ void k_refine_finish(long long m, long long nsample, const unsigned l
     *dm = u ? (long long)nk : m;
 }
 
+// ------------------------------------------------------------ small m --
+// At most HG_SMALL_M points: the whole hull in one CTA (one launch instead
+// of the pipeline's ~40, whose launch latency is the cost there).  The
+// points, padded to a power of two with +inf, are sorted by (x, y, id) with
+// a bitonic network in shared memory; the first point of each run of equal
+// (x, y) -- the lowest id -- stands for the run; one thread runs Andrew's
+// lower chain and another the upper chain, popping while the exact turn
+// (chf::orient_sign) is <= 0.  The same canonical hull as the pipeline
+// (DESIGN R8).  surv (nullable: position i) selects the points; idmap
+// (nullable) gives position i's output id.
+constexpr int HG_SMALL_M = 1024;
+__global__ void __launch_bounds__(512) k_small_hull(const double *__restrict__ xy, const long long *__restrict__ surv,
+                                                    const long long *__restrict__ idmap, long long m,
+                                                    long long *__restrict__ out, long long *__restrict__ d_nh)
+{
+    __shared__ double sx[HG_SMALL_M], sy[HG_SMALL_M];
+    __shared__ long long sid[HG_SMALL_M];
+    __shared__ int lst[HG_SMALL_M], ust[HG_SMALL_M];
+    __shared__ int s_nl, s_nu;
+    const int n = (int)m;
+    int n2 = 1;
+    while (n2 < n)
+        n2 <<= 1;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        if (i < n) {
+            const long long id = surv ? surv[i] : i;
+            const double2 q = reinterpret_cast<const double2 *>(xy)[id];
+            sx[i] = q.x;
+            sy[i] = q.y;
+            sid[i] = idmap ? idmap[i] : id;
+        } else {
+            sx[i] = sy[i] = CH_INF;
+            sid[i] = 0x7fffffffffffffffll;
+        }
+    }
+    __syncthreads();
+    auto less = [&](int a, int b) {
+        return sx[a] < sx[b] || (sx[a] == sx[b] && (sy[a] < sy[b] || (sy[a] == sy[b] && sid[a] < sid[b])));
+    };
+    for (int k = 2; k <= n2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const bool up = (i & k) == 0;
+                    if (up ? less(l, i) : less(i, l)) {
+                        const double tx = sx[i], ty = sy[i];
+                        const long long td = sid[i];
+                        sx[i] = sx[l];
+                        sy[i] = sy[l];
+                        sid[i] = sid[l];
+                        sx[l] = tx;
+                        sy[l] = ty;
+                        sid[l] = td;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    // the first point of each run of equal (x, y) stands for the run
+    auto first = [&](int i) { return i == 0 || !(sx[i] == sx[i - 1] && sy[i] == sy[i - 1]); };
+    auto turn_le0 = [&](int a, int b, int c) {
+        return chf::orient_sign(sx[a], sy[a], sx[b], sy[b], sx[c], sy[c]) <= 0;
+    };
+    if (threadIdx.x == 0) { // lower chain, left to right
+        int k = 0;
+        for (int i = 0; i < n; i++) {
+            if (!first(i))
+                continue;
+            while (k >= 2 && turn_le0(lst[k - 2], lst[k - 1], i))
+                k--;
+            lst[k++] = i;
+        }
+        s_nl = k;
+    } else if (threadIdx.x == 32) { // upper chain, right to left (another warp)
+        int k = 0;
+        for (int i = n - 1; i >= 0; i--) {
+            if (!first(i))
+                continue;
+            while (k >= 2 && turn_le0(ust[k - 2], ust[k - 1], i))
+                k--;
+            ust[k++] = i;
+        }
+        s_nu = k;
+    }
+    __syncthreads();
+    const int nl = s_nl, nu = s_nu;
+    if (nl <= 1) { // one distinct point
+        if (threadIdx.x == 0) {
+            out[0] = sid[lst[0]];
+            *d_nh = 1;
+        }
+        return;
+    }
+    const int a = nl - 1, total = a + nu - 1;
+    for (int g = threadIdx.x; g < total; g += blockDim.x)
+        out[g] = g < a ? sid[lst[g]] : sid[ust[g - a]];
+    if (threadIdx.x == 0)
+        *d_nh = total;
+}
+
 struct Seq {
     const double2 *P;
     long long m;
@@ -1588,6 +1689,12 @@ ch_status ch_hull_gpu_async(const double *d_xy, int64_t n_points, const int64_t 
     const HullTmp L(m);
     if (tmp_bytes < L.total)
         return CH_ERR_WORKSPACE;
+    if (m <= HG_SMALL_M) { // one CTA, one launch
+        k_small_hull<<<1, 512, 0, st>>>(d_xy, (const long long *)d_surv, nullptr, m, (long long *)d_hull,
+                                        (long long *)d_n_hull);
+        const cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? CH_OK : chi::fail(CH_ERR_CUDA, std::string("device hull: ") + cudaGetErrorString(e));
+    }
     // the second filtering round, decided on the device (no host
     // synchronization) when the scratch has room for it
     const long long *kept = nullptr, *dm = nullptr;
@@ -1642,6 +1749,12 @@ ch_status ch_hull_gpu_pts_async(const double *d_pts, const int64_t *d_ids, int64
     const HullTmp L(m);
     if (tmp_bytes < L.total)
         return CH_ERR_WORKSPACE;
+    if (m <= HG_SMALL_M) { // one CTA, one launch (positions i, ids d_ids[i])
+        k_small_hull<<<1, 512, 0, st>>>(d_pts, nullptr, (const long long *)d_ids, m, (long long *)d_hull,
+                                        (long long *)d_n_hull);
+        const cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? CH_OK : chi::fail(CH_ERR_CUDA, std::string("device hull: ") + cudaGetErrorString(e));
+    }
     return m <= (1ll << 32) ? hull_async<unsigned>(d_pts, nullptr, m, (long long *)d_hull, (long long *)d_n_hull,
                                                     d_tmp, L, st, (const long long *)d_ids)
                             : hull_async<unsigned long long>(d_pts, nullptr, m, (long long *)d_hull,
